@@ -1,0 +1,204 @@
+/*
+ * galois.h — C ABI of the B200-native GaloisSAT GPU stage (arxiv 2603.28796).
+ *
+ * The library runs the paper's differentiable SAT engine on one GPU per process:
+ * every CNF clause is the polynomial C = 1 - prod_i (1 - s_i) of its literal values
+ * (Eq.1-2); a batch of independent relaxed assignments (restarts or
+ * Shannon cubes, Lemma 1) is sampled with Gumbel noise and a
+ * straight-through argmax (Eq.3-4), scored by the MaxSAT loss
+ * L = -sum_t C_t (Eq.5), updated by Adam (App. A), rounded and
+ * checked exactly against the CNF. The best member (minimal unsat count)
+ * is tracked on the device and, with several GPUs, min-reduced over NCCL.
+ *
+ * Conventions (all functions):
+ *  - Status codes only (enum galois_status); no exception crosses the ABI. The message
+ *    of the last failure on the calling thread is galois_last_error().
+ *  - Input arrays are BORROWED for the duration of the call and copied; output arrays
+ *    are caller-allocated HOST memory unless stated otherwise.
+ *  - Handles are not thread-safe; distinct handles may be used concurrently.
+ *  - An engine binds to the CUDA device current at galois_engine_create and uses a
+ *    library-owned stream unless galois_engine_set_stream is called.
+ *  - After a CUDA / NCCL error or a non-finite iterate the engine is poisoned: every
+ *    later call on it returns GALOIS_E_STATE until it is freed.
+ *  - Host layouts of per-member arrays are member-major: [local member][variable].
+ *  - Member indices in outputs are GLOBAL: rank r owns members
+ *    [r * b_per, min(B, (r+1) * b_per)) with b_per = roundup(ceil(B / world), 32).
+ */
+#ifndef GALOIS_H
+#define GALOIS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct galois_cnf galois_cnf;       /* device-resident CSR + CSC of one CNF, refcounted */
+typedef struct galois_engine galois_engine; /* one rank's slice of the batch                   */
+
+enum galois_status {
+    GALOIS_OK = 0,
+    GALOIS_BUDGET = 1,           /* step budget spent, no satisfying member found            */
+    GALOIS_SAT = 10,             /* the best member satisfies every clause (u* = 0)           */
+    GALOIS_E_ARG = -1,           /* invalid argument (null pointer, bad size, bad hparam)     */
+    GALOIS_E_VAR_RANGE = -2,     /* a literal is 0 or |lit| > num_vars                        */
+    GALOIS_E_OFFSETS = -3,       /* offsets[0] != 0, decreasing offsets, or L >= 2^31         */
+    GALOIS_E_EMPTY_CLAUSE = -4,  /* a clause has no literal: the CNF is trivially UNSAT       */
+    GALOIS_E_OOM = -5,           /* device allocation failed                                   */
+    GALOIS_E_CUDA = -6,          /* CUDA runtime error (incl. no device)                       */
+    GALOIS_E_NCCL = -7,          /* NCCL unavailable or failed                                 */
+    GALOIS_E_NONFINITE = -8,     /* an iterate became NaN/Inf                                  */
+    GALOIS_E_STATE = -9          /* wrong call order, or handle poisoned by an earlier error   */
+};
+
+enum galois_mode { GALOIS_MODE_ST = 0, GALOIS_MODE_SOFT = 1 };
+enum galois_optimizer { GALOIS_ADAM = 0, GALOIS_SGD = 1 };
+
+/* ------------------------------------------------------------------------------ CNF */
+
+/* Load a CNF given as clause-major CSR (a conjunction of clauses, each a
+ * disjunction of literals): clause c holds literals[clause_offsets[c] ..
+ * clause_offsets[c+1]-1], each a DIMACS signed 1-based variable (+v = x_v, -v = not x_v).
+ *   num_vars       n >= 1
+ *   num_clauses    m >= 0
+ *   clause_offsets m+1 int64, host, borrowed; offsets[0] = 0, non-decreasing, L = offsets[m] < 2^31
+ *   literals       L int32, host, borrowed; 1 <= |lit| <= n
+ * Duplicate literals and tautologies are kept verbatim (per-slot polynomial semantics).
+ * Builds on the device: the literal codes, the variable-major transpose (CSC, stable in
+ * the slot order within (variable, sign)) and the hub table of high-degree variables.
+ * Errors: E_ARG, E_OFFSETS, E_VAR_RANGE, E_EMPTY_CLAUSE (validated on the device),
+ * E_OOM, E_CUDA. On error *out is NULL. */
+int galois_cnf_load(int32_t num_vars, int64_t num_clauses, const int64_t *clause_offsets,
+                    const int32_t *literals, galois_cnf **out);
+
+/* Sizes of a loaded CNF (any pointer may be NULL). */
+int galois_cnf_info(const galois_cnf *cnf, int32_t *num_vars, int64_t *num_clauses,
+                    int64_t *num_slots, int32_t *max_width, int32_t *max_degree, int32_t *num_hubs);
+
+/* Copy the device CSC back (test hook): var_off[2n+1] gives, for code 2v+neg, the range
+ * [var_off[code], var_off[code+1]) of occ_slot[L] holding the slots of literal code in
+ * ascending slot order. Any pointer may be NULL. */
+int galois_cnf_get_csc(const galois_cnf *cnf, int32_t *code_off, int32_t *occ_slot);
+
+/* Drop the caller's reference (engines hold their own). NULL is a no-op. */
+void galois_cnf_free(galois_cnf *cnf);
+
+/* --------------------------------------------------------------------------- engine */
+
+/* Create an engine for a global batch of B >= 1 independent members, a budget of
+ * steps >= 0 optimiser steps ("epochs", one full-batch step each), learning
+ * rate lr > 0 (paper 0.5) and RNG seed. Defaults: ST mode, tau = 1, Adam (0.9, 0.999,
+ * 1e-8), check interval 1, no cubes, world = 1. Device memory is allocated and the
+ * logits initialised lazily at the first step/run/get (so setters may follow create). */
+int galois_engine_create(const galois_cnf *cnf, int64_t batch, int32_t steps, float lr,
+                         uint64_t seed, galois_engine **out);
+
+/* One optimiser step t -> t+1 (sample, clause forward, straight-through gradient,
+ * update, round, and the exact check if t+1 is a check point). Returns GALOIS_OK,
+ * GALOIS_SAT once the best member satisfies the CNF (further steps are no-ops), or
+ * GALOIS_BUDGET if the step budget is already spent. Synchronises the stream. */
+int galois_engine_step(galois_engine *eng);
+
+/* Run steps until SAT (GALOIS_SAT) or until the budget is spent (GALOIS_BUDGET). The
+ * host polls an 8-byte device flag once per chunk of steps; kernels of steps enqueued
+ * after the stop are no-ops, so the recorded best and step count are exact. */
+int galois_engine_run(galois_engine *eng);
+
+/* Like run, but enqueues at most max_steps further steps and does not synchronise the
+ * stream (the caller times / synchronises, e.g. with events on the same stream).
+ * Returns OK (or BUDGET if nothing was left to enqueue). */
+int galois_engine_enqueue(galois_engine *eng, int32_t max_steps);
+
+/* Best member over all check points so far, min over (unsat, step, global member)
+ * lexicographically ("minimal clause loss"): its noise-free rounding (n bytes
+ * 0/1, host; may be NULL), unsat count, global member index and step. With world > 1
+ * this is collective (all ranks must call it; the winner's bits are broadcast). */
+int galois_best_assignment(galois_engine *eng, uint8_t *values, int32_t *unsat,
+                           int64_t *global_b, int32_t *step);
+
+/* Exact unsat counts of the local members at the last check point (b_loc int32, host),
+ * and the global index of the first local member (may be NULL). */
+int galois_unsat_counts(galois_engine *eng, int32_t *counts, int64_t *first_global_b);
+
+/* Local slice and progress: number of local members, first global member, steps done,
+ * whether the engine stopped on SAT. Any pointer may be NULL. */
+int galois_engine_info(galois_engine *eng, int64_t *local_batch, int64_t *first_global_b,
+                       int32_t *steps_done, int32_t *stopped);
+
+void galois_engine_free(galois_engine *eng);
+
+/* Thread-local message of the last failure ("" if none). */
+const char *galois_last_error(void);
+
+/* ------------------------------------------- setters (before the first step, else E_STATE) */
+
+/* 0 = straight-through (paper, Eq.4), 1 = fully soft forward (debug mode for
+ * finite-difference checks; ~10x more memory traffic). */
+int galois_engine_set_mode(galois_engine *eng, int32_t mode);
+
+/* tau > 0 (Eq.3; paper 1.0), Adam beta1, beta2 in [0,1), eps > 0, optimizer
+ * 0 = Adam (App. A), 1 = plain gradient step theta -= lr g. */
+int galois_engine_set_hparams(galois_engine *eng, float tau, float beta1, float beta2, float eps,
+                              int32_t optimizer);
+
+/* Check (round + exact count + best update) at t = 0, every k >= 1 steps, and at the
+ * last step of the budget. */
+int galois_engine_set_check_interval(galois_engine *eng, int32_t k);
+
+/* Cube pins (Lemma 1): d variables (1-based, distinct, 0 <= d <= 30); member b
+ * fixes variable vars[r] to bit r of alpha = b mod 2^d (sorted ascending by variable
+ * index). Pinned variables are frozen (no update) and forced in every sample/rounding. */
+int galois_engine_set_cubes(galois_engine *eng, int32_t d, const int32_t *vars);
+
+/* Join an NCCL communicator of `world` ranks (one per GPU) created from a 128-byte
+ * ncclUniqueId produced by galois_comm_unique_id on one rank and shared by the caller.
+ * The communicator is initialised (collectively) at the first step. */
+int galois_engine_set_comm(galois_engine *eng, int32_t rank, int32_t world, const void *nccl_unique_id);
+
+/* Use the caller's CUDA stream (a cudaStream_t, e.g. torch.cuda.current_stream()). */
+int galois_engine_set_stream(galois_engine *eng, void *cuda_stream);
+
+/* Test hook: also store the per-step clause signal G and gradient g1 (see get_grad). */
+int galois_engine_set_debug(galois_engine *eng, int32_t enable);
+
+/* Record CUDA events around every kernel launch (see galois_engine_kernel_times). */
+int galois_engine_set_profiling(galois_engine *eng, int32_t enable);
+
+/* Produce a 128-byte ncclUniqueId into out (on one rank). E_NCCL if NCCL is absent. */
+int galois_comm_unique_id(void *out128);
+
+/* ------------------------------------------------------ test hooks (parity / resume) */
+
+/* Reduced iterate of the local members, host [b_loc][n] float each (NULL to skip):
+ * z = theta_1 - theta_0, m = Adam first moment of theta_1, v = second moment; t = steps. */
+int galois_engine_get_iterate(galois_engine *eng, float *z, float *m, float *v, int32_t *t);
+
+/* Overwrite the iterate (same layout) and the step counter; recomputes the rounding R_t
+ * and the next sample X_{t+1}; clears the stop flag (the best record is kept). */
+int galois_engine_set_iterate(galois_engine *eng, const float *z, const float *m, const float *v,
+                              int32_t t);
+
+/* Of the last step (requires set_debug(1) before the first step): the clause signal
+ * G = sum over occurrences of sigma * E (int32; ST mode) and dL/dtheta_1 = -G p q / tau
+ * (float), host [b_loc][n] each (NULL to skip). */
+int galois_engine_get_grad(galois_engine *eng, int32_t *G, float *g1);
+
+/* Of the last forward: Lambda_b = sum_c U_c (= L_b + m; the unsat count of the sample
+ * in ST mode), host b_loc floats. */
+int galois_engine_get_loss(galois_engine *eng, float *lambda);
+
+/* The sample bits X_{t+1} the next forward will use and the rounding R_t of the last
+ * update, host [b_loc][n] bytes 0/1 each (NULL to skip). */
+int galois_engine_get_bits(galois_engine *eng, uint8_t *x_next, uint8_t *r);
+
+/* Kernel times accumulated since the last call (profiling mode): for kernel class
+ * k in {0 forward, 1 update, 2 check, 3 best/extract, 4 hub-partial, 5 init}:
+ * ms[k] total milliseconds and launches[k] count (arrays of GALOIS_NUM_KERNEL_CLASSES). */
+#define GALOIS_NUM_KERNEL_CLASSES 6
+int galois_engine_kernel_times(galois_engine *eng, double *ms, int64_t *launches);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GALOIS_H */

@@ -1,0 +1,922 @@
+// engine.cu — the C ABI (include/galois.h) and the engine orchestration.
+//
+// One engine = one rank's slice of the batch on one GPU. Each step enqueues, on the
+// engine's stream:
+//   memset Lambda | forward (a5) | hub partials (a6) | fused update (a6+a7)
+//   and at check points: memset unsat | check (a8) | best | [NCCL MIN (a9) | finalize] | extract
+// Every kernel reads the device control block first and returns immediately once the
+// best member satisfies the CNF, so the host only polls an 8-byte flag per chunk.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/galois.h"
+#include "comm.h"
+#include "galois_internal.h"
+
+namespace galois {
+namespace launch {
+void init(const StepParams &p, float *z, float *m, float *v, uint32_t *X, uint32_t *R, cudaStream_t st);
+void resample(const StepParams &p, const float *z, uint32_t *X, uint32_t *R, int32_t t_next, cudaStream_t st);
+void forward_st(const DevCnf &c, int32_t W, int32_t b_pad, const uint32_t *X, uint32_t *E, int32_t *lam,
+                Ctrl *ctrl, cudaStream_t st);
+void check(const DevCnf &c, int32_t W, int32_t b_pad, const uint32_t *R, int32_t *unsat, Ctrl *ctrl,
+           cudaStream_t st);
+void hub_partial(const DevCnf &c, int32_t W, int32_t b_pad, const uint32_t *E, int4 *partial,
+                 const Ctrl *ctrl, cudaStream_t st);
+void update_st(const DevCnf &c, const StepParams &p, float *z, float *m, float *v, uint32_t *X, uint32_t *R,
+               const uint32_t *E, const int4 *partial, Ctrl *ctrl, int32_t *dbg_G, float *dbg_g1,
+               cudaStream_t st);
+void best(const int32_t *unsat, int32_t b_loc, int64_t b0, Ctrl *ctrl, bool finalize, cudaStream_t st);
+void finalize(Ctrl *ctrl, int64_t b0, int32_t b_loc, cudaStream_t st);
+void extract(const uint32_t *R, int32_t n, int32_t W, int64_t b0, const Ctrl *ctrl, uint8_t *best_bits,
+             cudaStream_t st);
+// SOFT mode (soft_kernels.cu)
+void forward_soft(const DevCnf &c, const StepParams &p, const float *z, float *P, float *Es, float *lam,
+                  Ctrl *ctrl, cudaStream_t st);
+void update_soft(const DevCnf &c, const StepParams &p, float *z, float *m, float *v, uint32_t *X, uint32_t *R,
+                 const float *Es, Ctrl *ctrl, float *dbg_G, float *dbg_g1, cudaStream_t st);
+int soft_chunks();
+}  // namespace launch
+}  // namespace galois
+
+using namespace galois;
+
+// ------------------------------------------------------------------------ errors
+static thread_local std::string g_last_error;
+
+static int fail(int code, const std::string &msg)
+{
+    g_last_error = msg;
+    return code;
+}
+
+#define CUDA_TRY(expr)                                                                         \
+    do {                                                                                       \
+        cudaError_t _e = (expr);                                                               \
+        if (_e != cudaSuccess) {                                                               \
+            return fail(_e == cudaErrorMemoryAllocation ? GALOIS_E_OOM : GALOIS_E_CUDA,        \
+                        std::string(#expr) + ": " + cudaGetErrorString(_e));                   \
+        }                                                                                      \
+    } while (0)
+
+static int check_device(int *dev)
+{
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0)
+        return fail(GALOIS_E_CUDA, std::string("no CUDA device: ") +
+                                       (e != cudaSuccess ? cudaGetErrorString(e) : "device count is 0"));
+    CUDA_TRY(cudaGetDevice(dev));
+    return GALOIS_OK;
+}
+
+// ------------------------------------------------------------------------ CNF
+struct galois_cnf {
+    std::atomic<int> refs{1};
+    int device = 0;
+    int32_t n = 0;
+    int64_t m = 0;
+    int64_t L = 0;
+    int32_t max_width = 0;
+    int32_t max_degree = 0;
+    int32_t *clause_off = nullptr;
+    int2 *slot_info = nullptr;
+    int32_t *code_off = nullptr;
+    int32_t *occ_slot = nullptr;
+    int32_t *hub_of_var = nullptr;
+    int32_t *hub_chunk_off = nullptr;
+    int2 *hub_chunk = nullptr;
+    int32_t num_hubs = 0;
+    int32_t num_hub_chunks = 0;
+
+    DevCnf view() const
+    {
+        DevCnf d;
+        d.n = n;
+        d.m = (int32_t)m;
+        d.L = (int32_t)L;
+        d.clause_off = clause_off;
+        d.slot_info = slot_info;
+        d.code_off = code_off;
+        d.occ_slot = occ_slot;
+        d.num_hubs = num_hubs;
+        d.num_hub_chunks = num_hub_chunks;
+        d.hub_of_var = hub_of_var;
+        d.hub_chunk_off = hub_chunk_off;
+        d.hub_chunk = hub_chunk;
+        return d;
+    }
+    ~galois_cnf()
+    {
+        int cur = 0;
+        cudaGetDevice(&cur);
+        cudaSetDevice(device);
+        cudaFree(clause_off);
+        cudaFree(slot_info);
+        cudaFree(code_off);
+        cudaFree(occ_slot);
+        cudaFree(hub_of_var);
+        cudaFree(hub_chunk_off);
+        cudaFree(hub_chunk);
+        cudaSetDevice(cur);
+    }
+};
+
+static void cnf_release(galois_cnf *c)
+{
+    if (c && c->refs.fetch_sub(1) == 1) delete c;
+}
+
+template <typename T>
+static cudaError_t dmalloc(T **p, size_t count)
+{
+    *p = nullptr;
+    if (count == 0) count = 1;
+    return cudaMalloc((void **)p, count * sizeof(T));
+}
+
+extern "C" int galois_cnf_load(int32_t num_vars, int64_t num_clauses, const int64_t *clause_offsets,
+                               const int32_t *literals, galois_cnf **out)
+{
+    if (!out) return fail(GALOIS_E_ARG, "out is NULL");
+    *out = nullptr;
+    if (num_vars < 1 || num_vars >= (1 << 30)) return fail(GALOIS_E_ARG, "num_vars must be in [1, 2^30)");
+    if (num_clauses < 0 || num_clauses >= INT32_MAX) return fail(GALOIS_E_ARG, "num_clauses must be in [0, 2^31-1)");
+    if (!clause_offsets) return fail(GALOIS_E_ARG, "clause_offsets is NULL");
+    const int64_t L = clause_offsets[num_clauses];
+    if (clause_offsets[0] != 0) return fail(GALOIS_E_OFFSETS, "clause_offsets[0] != 0");
+    if (L < 0 || L >= INT32_MAX) return fail(GALOIS_E_OFFSETS, "literal count L must be in [0, 2^31-1)");
+    if (L > 0 && !literals) return fail(GALOIS_E_ARG, "literals is NULL");
+    int dev = 0;
+    if (int rc = check_device(&dev)) return rc;
+
+    galois_cnf *c = new galois_cnf();
+    c->device = dev;
+    c->n = num_vars;
+    c->m = num_clauses;
+    c->L = L;
+    const int64_t m = num_clauses;
+    int64_t *d_off64 = nullptr;
+    int32_t *d_lits = nullptr, *d_err = nullptr;
+    void *d_scratch = nullptr;
+    cudaStream_t st = nullptr;
+    auto cleanup = [&]() {
+        cudaFree(d_off64);
+        cudaFree(d_lits);
+        cudaFree(d_err);
+        cudaFree(d_scratch);
+        if (st) cudaStreamDestroy(st);
+    };
+    auto bail = [&](int code, const std::string &msg) {
+        cleanup();
+        cnf_release(c);
+        return fail(code, msg);
+    };
+#define LOAD_TRY(expr)                                                                                   \
+    do {                                                                                                 \
+        cudaError_t _e = (expr);                                                                         \
+        if (_e != cudaSuccess)                                                                           \
+            return bail(_e == cudaErrorMemoryAllocation ? GALOIS_E_OOM : GALOIS_E_CUDA,                  \
+                        std::string(#expr) + ": " + cudaGetErrorString(_e));                             \
+    } while (0)
+
+    LOAD_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    LOAD_TRY(dmalloc(&d_off64, (size_t)m + 1));
+    LOAD_TRY(dmalloc(&d_lits, (size_t)L));
+    LOAD_TRY(dmalloc(&d_err, 8));
+    LOAD_TRY(dmalloc(&c->clause_off, (size_t)m + 1));
+    LOAD_TRY(dmalloc(&c->slot_info, (size_t)L));
+    LOAD_TRY(dmalloc(&c->code_off, 2 * (size_t)num_vars + 1));
+    LOAD_TRY(dmalloc(&c->occ_slot, (size_t)L));
+    const size_t scratch = build_cnf_scratch_bytes(num_vars, L);
+    LOAD_TRY(cudaMalloc(&d_scratch, scratch));
+    LOAD_TRY(cudaMemcpyAsync(d_off64, clause_offsets, sizeof(int64_t) * (size_t)(m + 1), cudaMemcpyHostToDevice, st));
+    if (L > 0)
+        LOAD_TRY(cudaMemcpyAsync(d_lits, literals, sizeof(int32_t) * (size_t)L, cudaMemcpyHostToDevice, st));
+    const int32_t h_err_init[8] = {0, INT32_MAX, INT32_MAX, INT32_MAX, 0, 0, 0, 0};
+    LOAD_TRY(cudaMemcpyAsync(d_err, h_err_init, sizeof(h_err_init), cudaMemcpyHostToDevice, st));
+    LOAD_TRY(launch_build_cnf(num_vars, m, L, d_off64, d_lits, c->clause_off, c->slot_info, c->code_off,
+                              c->occ_slot, d_err, d_err + 4, d_scratch, scratch, st));
+    int32_t h_err[8];
+    LOAD_TRY(cudaMemcpyAsync(h_err, d_err, sizeof(h_err), cudaMemcpyDeviceToHost, st));
+    LOAD_TRY(cudaStreamSynchronize(st));
+    if (h_err[0] & 1) {
+        char buf[160];
+        snprintf(buf, sizeof buf, "clause offsets are not a valid CSR (first bad clause %d)", h_err[1]);
+        return bail(GALOIS_E_OFFSETS, buf);
+    }
+    if (h_err[0] & 4) {
+        char buf[160];
+        snprintf(buf, sizeof buf, "clause %d is empty: the CNF is trivially UNSAT", h_err[2]);
+        return bail(GALOIS_E_EMPTY_CLAUSE, buf);
+    }
+    if (h_err[0] & 2) {
+        char buf[160];
+        snprintf(buf, sizeof buf, "literal at slot %d is 0 or exceeds num_vars=%d", h_err[3], num_vars);
+        return bail(GALOIS_E_VAR_RANGE, buf);
+    }
+    c->max_width = h_err[4];
+
+    // hub table: variables with more than kHubDegree occurrences are reduced in chunks
+    std::vector<int32_t> code_off(2 * (size_t)num_vars + 1);
+    LOAD_TRY(cudaMemcpy(code_off.data(), c->code_off, code_off.size() * 4, cudaMemcpyDeviceToHost));
+    std::vector<int32_t> hub_of_var(num_vars, -1), hub_chunk_off(1, 0);
+    std::vector<int2> hub_chunk;
+    for (int32_t v = 0; v < num_vars; ++v) {
+        const int32_t a = code_off[2 * (size_t)v], e = code_off[2 * (size_t)v + 2];
+        const int32_t deg = e - a;
+        c->max_degree = std::max(c->max_degree, deg);
+        if (deg > kHubDegree) {
+            hub_of_var[v] = c->num_hubs++;
+            for (int32_t k = a; k < e; k += kHubChunk) hub_chunk.push_back(make_int2(v, k));
+            hub_chunk_off.push_back((int32_t)hub_chunk.size());
+        }
+    }
+    c->num_hub_chunks = (int32_t)hub_chunk.size();
+    if (c->num_hubs > 0) {
+        LOAD_TRY(dmalloc(&c->hub_of_var, (size_t)num_vars));
+        LOAD_TRY(dmalloc(&c->hub_chunk_off, hub_chunk_off.size()));
+        LOAD_TRY(dmalloc(&c->hub_chunk, hub_chunk.size()));
+        LOAD_TRY(cudaMemcpy(c->hub_of_var, hub_of_var.data(), hub_of_var.size() * 4, cudaMemcpyHostToDevice));
+        LOAD_TRY(cudaMemcpy(c->hub_chunk_off, hub_chunk_off.data(), hub_chunk_off.size() * 4, cudaMemcpyHostToDevice));
+        LOAD_TRY(cudaMemcpy(c->hub_chunk, hub_chunk.data(), hub_chunk.size() * sizeof(int2), cudaMemcpyHostToDevice));
+    }
+#undef LOAD_TRY
+    cleanup();
+    *out = c;
+    return GALOIS_OK;
+}
+
+extern "C" int galois_cnf_info(const galois_cnf *c, int32_t *n, int64_t *m, int64_t *L, int32_t *max_width,
+                               int32_t *max_degree, int32_t *num_hubs)
+{
+    if (!c) return fail(GALOIS_E_ARG, "cnf is NULL");
+    if (n) *n = c->n;
+    if (m) *m = c->m;
+    if (L) *L = c->L;
+    if (max_width) *max_width = c->max_width;
+    if (max_degree) *max_degree = c->max_degree;
+    if (num_hubs) *num_hubs = c->num_hubs;
+    return GALOIS_OK;
+}
+
+extern "C" int galois_cnf_get_csc(const galois_cnf *c, int32_t *code_off, int32_t *occ_slot)
+{
+    if (!c) return fail(GALOIS_E_ARG, "cnf is NULL");
+    CUDA_TRY(cudaSetDevice(c->device));
+    if (code_off) CUDA_TRY(cudaMemcpy(code_off, c->code_off, (2 * (size_t)c->n + 1) * 4, cudaMemcpyDeviceToHost));
+    if (occ_slot && c->L > 0) CUDA_TRY(cudaMemcpy(occ_slot, c->occ_slot, (size_t)c->L * 4, cudaMemcpyDeviceToHost));
+    return GALOIS_OK;
+}
+
+extern "C" void galois_cnf_free(galois_cnf *c) { cnf_release(c); }
+
+// ------------------------------------------------------------------------ engine
+struct galois_engine {
+    galois_cnf *cnf = nullptr;
+    int device = 0;
+    // configuration
+    int64_t B = 0;
+    int32_t T = 0;
+    double lr = 0.5, tau = 1.0, beta1 = 0.9, beta2 = 0.999, eps = 1e-8;
+    int32_t optimizer = 0, mode = 0, K = 1;
+    uint64_t seed = 0;
+    std::vector<int32_t> pins;   // 0-based, ascending
+    int32_t rank = 0, world = 1;
+    unsigned char nccl_id[128] = {0};
+    bool debug = false, profiling = false;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    // state
+    bool prepared = false, poisoned = false;
+    int32_t steps_enqueued = 0;
+    int64_t b_per = 0, b0 = 0;
+    int32_t b_loc = 0, b_pad = 0, W = 0;
+    Comm comm;
+    // device buffers
+    float *z = nullptr, *m = nullptr, *v = nullptr;
+    uint32_t *X = nullptr, *R = nullptr, *E = nullptr;
+    int4 *partial = nullptr;
+    int32_t *lam = nullptr, *unsat = nullptr;
+    Ctrl *ctrl = nullptr;
+    uint8_t *best_bits = nullptr;
+    int8_t *pin_rank = nullptr;
+    float2 *adam_consts = nullptr;
+    int32_t *dbg_G = nullptr;
+    float *dbg_g1 = nullptr;
+    float *P = nullptr, *Es = nullptr, *lam_f = nullptr, *dbg_Gf = nullptr;   // SOFT mode
+    Ctrl *h_ctrl = nullptr;     // pinned mirror (2 slots)
+    cudaEvent_t poll_ev[2] = {nullptr, nullptr};
+    // profiling
+    struct Rec {
+        int cls;
+        cudaEvent_t a, b;
+    };
+    std::vector<Rec> recs;
+    std::vector<cudaEvent_t> ev_pool;
+
+    StepParams params() const
+    {
+        StepParams p;
+        p.n = cnf->n;
+        p.b_pad = b_pad;
+        p.W = W;
+        p.b_loc = b_loc;
+        p.b0 = b0;
+        p.seed = seed;
+        p.tau = (float)tau;
+        p.inv_tau = (float)(1.0 / tau);
+        p.beta1 = (float)beta1;
+        p.beta2 = (float)beta2;
+        p.eps = (float)eps;
+        p.omb1 = (float)(1.0 - beta1);
+        p.omb2 = (float)(1.0 - beta2);
+        p.optimizer = optimizer;
+        p.lr = (float)lr;
+        p.adam_consts = adam_consts;
+        p.num_pins = (int32_t)pins.size();
+        p.pin_rank = pins.empty() ? nullptr : pin_rank;
+        return p;
+    }
+
+    cudaEvent_t take_event()
+    {
+        if (!ev_pool.empty()) {
+            cudaEvent_t e = ev_pool.back();
+            ev_pool.pop_back();
+            return e;
+        }
+        cudaEvent_t e = nullptr;
+        cudaEventCreate(&e);
+        return e;
+    }
+    template <typename F>
+    void timed(int cls, F &&f)
+    {
+        if (!profiling) {
+            f();
+            return;
+        }
+        Rec r{cls, take_event(), take_event()};
+        cudaEventRecord(r.a, stream);
+        f();
+        cudaEventRecord(r.b, stream);
+        recs.push_back(r);
+    }
+};
+
+static void engine_free_buffers(galois_engine *e)
+{
+    cudaFree(e->z); cudaFree(e->m); cudaFree(e->v);
+    cudaFree(e->X); cudaFree(e->R); cudaFree(e->E);
+    cudaFree(e->partial); cudaFree(e->lam); cudaFree(e->unsat);
+    cudaFree(e->ctrl); cudaFree(e->best_bits); cudaFree(e->pin_rank);
+    cudaFree(e->adam_consts); cudaFree(e->dbg_G); cudaFree(e->dbg_g1);
+    cudaFree(e->P); cudaFree(e->Es); cudaFree(e->lam_f); cudaFree(e->dbg_Gf);
+    if (e->h_ctrl) cudaFreeHost(e->h_ctrl);
+    e->z = e->m = e->v = nullptr;
+}
+
+extern "C" int galois_engine_create(const galois_cnf *cnf, int64_t batch, int32_t steps, float lr, uint64_t seed,
+                                    galois_engine **out)
+{
+    if (!out) return fail(GALOIS_E_ARG, "out is NULL");
+    *out = nullptr;
+    if (!cnf) return fail(GALOIS_E_ARG, "cnf is NULL");
+    if (batch < 1 || batch > (int64_t(1) << 32)) return fail(GALOIS_E_ARG, "batch must be in [1, 2^32]");
+    if (steps < 0 || steps > (1 << 30)) return fail(GALOIS_E_ARG, "steps must be in [0, 2^30]");
+    if (!(lr > 0.0f) || !std::isfinite(lr)) return fail(GALOIS_E_ARG, "lr must be a positive finite number");
+    galois_engine *e = new galois_engine();
+    const_cast<galois_cnf *>(cnf)->refs.fetch_add(1);
+    e->cnf = const_cast<galois_cnf *>(cnf);
+    e->device = cnf->device;
+    e->B = batch;
+    e->T = steps;
+    e->lr = lr;
+    e->seed = seed;
+    *out = e;
+    return GALOIS_OK;
+}
+
+#define ENGINE_ENTRY(e)                                                                        \
+    do {                                                                                       \
+        if (!(e)) return fail(GALOIS_E_ARG, "engine is NULL");                                 \
+        if ((e)->poisoned) return fail(GALOIS_E_STATE, "engine is poisoned by an earlier error"); \
+    } while (0)
+
+#define SETTER_ENTRY(e)                                                                        \
+    do {                                                                                       \
+        ENGINE_ENTRY(e);                                                                       \
+        if ((e)->prepared) return fail(GALOIS_E_STATE, "setters are valid only before the first step"); \
+    } while (0)
+
+extern "C" int galois_engine_set_mode(galois_engine *e, int32_t mode)
+{
+    SETTER_ENTRY(e);
+    if (mode != GALOIS_MODE_ST && mode != GALOIS_MODE_SOFT) return fail(GALOIS_E_ARG, "mode must be 0 or 1");
+    e->mode = mode;
+    return GALOIS_OK;
+}
+
+extern "C" int galois_engine_set_hparams(galois_engine *e, float tau, float beta1, float beta2, float eps,
+                                         int32_t optimizer)
+{
+    SETTER_ENTRY(e);
+    if (!(tau > 0.0f) || !std::isfinite(tau)) return fail(GALOIS_E_ARG, "tau must be > 0");
+    if (!(beta1 >= 0.0f && beta1 < 1.0f) || !(beta2 >= 0.0f && beta2 < 1.0f))
+        return fail(GALOIS_E_ARG, "betas must be in [0, 1)");
+    if (!(eps > 0.0f) || !std::isfinite(eps)) return fail(GALOIS_E_ARG, "eps must be > 0");
+    if (optimizer != GALOIS_ADAM && optimizer != GALOIS_SGD) return fail(GALOIS_E_ARG, "optimizer must be 0 or 1");
+    e->tau = tau;
+    e->beta1 = beta1;
+    e->beta2 = beta2;
+    e->eps = eps;
+    e->optimizer = optimizer;
+    return GALOIS_OK;
+}
+
+extern "C" int galois_engine_set_check_interval(galois_engine *e, int32_t k)
+{
+    SETTER_ENTRY(e);
+    if (k < 1) return fail(GALOIS_E_ARG, "check interval must be >= 1");
+    e->K = k;
+    return GALOIS_OK;
+}
+
+extern "C" int galois_engine_set_cubes(galois_engine *e, int32_t d, const int32_t *vars)
+{
+    SETTER_ENTRY(e);
+    if (d < 0 || d > 30) return fail(GALOIS_E_ARG, "d must be in [0, 30]");
+    if (d > 0 && !vars) return fail(GALOIS_E_ARG, "vars is NULL");
+    std::vector<int32_t> p(vars, vars + d);
+    for (int32_t &x : p) {
+        if (x < 1 || x > e->cnf->n) return fail(GALOIS_E_VAR_RANGE, "cube variable out of range");
+        x -= 1;
+    }
+    std::sort(p.begin(), p.end());
+    if (std::adjacent_find(p.begin(), p.end()) != p.end()) return fail(GALOIS_E_ARG, "cube variables must be distinct");
+    e->pins = p;
+    return GALOIS_OK;
+}
+
+extern "C" int galois_engine_set_comm(galois_engine *e, int32_t rank, int32_t world, const void *id)
+{
+    SETTER_ENTRY(e);
+    if (world < 1 || rank < 0 || rank >= world) return fail(GALOIS_E_ARG, "need 0 <= rank < world");
+    if (world > 1 && !id) return fail(GALOIS_E_ARG, "nccl_unique_id is NULL");
+    e->rank = rank;
+    e->world = world;
+    if (id) memcpy(e->nccl_id, id, 128);
+    return GALOIS_OK;
+}
+
+extern "C" int galois_engine_set_stream(galois_engine *e, void *s)
+{
+    SETTER_ENTRY(e);
+    e->stream = (cudaStream_t)s;
+    e->own_stream = false;
+    return GALOIS_OK;
+}
+
+extern "C" int galois_engine_set_debug(galois_engine *e, int32_t enable)
+{
+    SETTER_ENTRY(e);
+    e->debug = enable != 0;
+    return GALOIS_OK;
+}
+
+extern "C" int galois_engine_set_profiling(galois_engine *e, int32_t enable)
+{
+    ENGINE_ENTRY(e);
+    e->profiling = enable != 0;
+    return GALOIS_OK;
+}
+
+extern "C" int galois_comm_unique_id(void *out128)
+{
+    if (!out128) return fail(GALOIS_E_ARG, "out is NULL");
+    std::string why;
+    if (!nccl_unique_id(out128, &why)) return fail(GALOIS_E_NCCL, why);
+    return GALOIS_OK;
+}
+
+static int poison(galois_engine *e, int code, const std::string &msg)
+{
+    e->poisoned = true;
+    return fail(code, msg);
+}
+
+#define ENG_CUDA(e, expr)                                                                      \
+    do {                                                                                       \
+        cudaError_t _e = (expr);                                                               \
+        if (_e != cudaSuccess)                                                                 \
+            return poison((e), _e == cudaErrorMemoryAllocation ? GALOIS_E_OOM : GALOIS_E_CUDA, \
+                          std::string(#expr) + ": " + cudaGetErrorString(_e));                 \
+    } while (0)
+
+static bool is_check_step(const galois_engine *e, int32_t s) { return (s % e->K) == 0 || s == e->T; }
+
+// Enqueue the check of the rounding currently in R (steps done = ctrl->t).
+static int enqueue_check(galois_engine *e)
+{
+    const DevCnf c = e->cnf->view();
+    ENG_CUDA(e, cudaMemsetAsync(e->unsat, 0, sizeof(int32_t) * (size_t)e->b_pad, e->stream));
+    e->timed(2, [&] { launch::check(c, e->W, e->b_pad, e->R, e->unsat, e->ctrl, e->stream); });
+    e->timed(3, [&] {
+        launch::best(e->unsat, e->b_loc, e->b0, e->ctrl, e->world == 1, e->stream);
+        if (e->world > 1) {
+            std::string why;
+            if (!e->comm.allreduce_min_u64(&e->ctrl->key_local, &e->ctrl->key_global, e->stream, &why)) {
+                e->poisoned = true;
+                g_last_error = why;
+                return;
+            }
+            launch::finalize(e->ctrl, e->b0, e->b_loc, e->stream);
+        }
+        launch::extract(e->R, e->cnf->n, e->W, e->b0, e->ctrl, e->best_bits, e->stream);
+    });
+    if (e->poisoned) return GALOIS_E_NCCL;
+    ENG_CUDA(e, cudaGetLastError());
+    return GALOIS_OK;
+}
+
+static int enqueue_step(galois_engine *e)
+{
+    const DevCnf c = e->cnf->view();
+    const StepParams p = e->params();
+    const int32_t s = e->steps_enqueued + 1;
+    if (e->mode == GALOIS_MODE_ST) {
+        ENG_CUDA(e, cudaMemsetAsync(e->lam, 0, sizeof(int32_t) * (size_t)e->b_pad, e->stream));
+        e->timed(0, [&] { launch::forward_st(c, e->W, e->b_pad, e->X, e->E, e->lam, e->ctrl, e->stream); });
+        if (c.num_hub_chunks > 0)
+            e->timed(4, [&] { launch::hub_partial(c, e->W, e->b_pad, e->E, e->partial, e->ctrl, e->stream); });
+        e->timed(1, [&] {
+            launch::update_st(c, p, e->z, e->m, e->v, e->X, e->R, e->E, e->partial, e->ctrl,
+                              e->debug ? e->dbg_G : nullptr, e->debug ? e->dbg_g1 : nullptr, e->stream);
+        });
+    } else {
+        ENG_CUDA(e, cudaMemsetAsync(e->lam_f, 0, sizeof(float) * (size_t)e->b_pad, e->stream));
+        e->timed(0, [&] { launch::forward_soft(c, p, e->z, e->P, e->Es, e->lam_f, e->ctrl, e->stream); });
+        e->timed(1, [&] {
+            launch::update_soft(c, p, e->z, e->m, e->v, e->X, e->R, e->Es, e->ctrl,
+                                e->debug ? e->dbg_Gf : nullptr, e->debug ? e->dbg_g1 : nullptr, e->stream);
+        });
+    }
+    ENG_CUDA(e, cudaGetLastError());
+    e->steps_enqueued = s;
+    if (is_check_step(e, s)) return enqueue_check(e);
+    return GALOIS_OK;
+}
+
+static int prepare(galois_engine *e)
+{
+    if (e->prepared) return GALOIS_OK;
+    ENG_CUDA(e, cudaSetDevice(e->device));
+    galois_cnf *c = e->cnf;
+    const int32_t n = c->n;
+    // batch slice: b_per = roundup(ceil(B / world), 32); pad the local slice to 32
+    int64_t per = (e->B + e->world - 1) / e->world;
+    per = (per + 31) / 32 * 32;
+    e->b_per = per;
+    e->b0 = per * e->rank;
+    const int64_t left = e->B - e->b0;
+    e->b_loc = (int32_t)std::max<int64_t>(0, std::min<int64_t>(per, left));
+    e->b_pad = std::max<int32_t>(32, (e->b_loc + 31) / 32 * 32);
+    e->W = e->b_pad / 32;
+    if ((uint64_t)n * (uint64_t)e->b_pad / 4 >= (1ull << 40))
+        return poison(e, GALOIS_E_ARG, "n * local batch too large");
+    if (!e->stream) {
+        ENG_CUDA(e, cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
+        e->own_stream = true;
+    }
+    const size_t nb = (size_t)n * (size_t)e->b_pad;
+    ENG_CUDA(e, dmalloc(&e->z, nb));
+    ENG_CUDA(e, dmalloc(&e->m, nb));
+    ENG_CUDA(e, dmalloc(&e->v, nb));
+    ENG_CUDA(e, dmalloc(&e->X, (size_t)n * e->W));
+    ENG_CUDA(e, dmalloc(&e->R, (size_t)n * e->W));
+    ENG_CUDA(e, dmalloc(&e->unsat, (size_t)e->b_pad));
+    ENG_CUDA(e, dmalloc(&e->ctrl, 1));
+    ENG_CUDA(e, dmalloc(&e->best_bits, (size_t)n));
+    ENG_CUDA(e, cudaMemsetAsync(e->best_bits, 0, (size_t)n, e->stream));
+    if (e->mode == GALOIS_MODE_ST) {
+        ENG_CUDA(e, dmalloc(&e->E, (size_t)c->L * e->W));
+        ENG_CUDA(e, dmalloc(&e->lam, (size_t)e->b_pad));
+        if (c->num_hub_chunks > 0) ENG_CUDA(e, dmalloc(&e->partial, (size_t)c->num_hub_chunks * (e->b_pad / 4)));
+        if (e->debug) {
+            ENG_CUDA(e, dmalloc(&e->dbg_G, nb));
+            ENG_CUDA(e, dmalloc(&e->dbg_g1, nb));
+        }
+    } else {
+        ENG_CUDA(e, dmalloc(&e->P, nb));
+        ENG_CUDA(e, dmalloc(&e->Es, (size_t)c->L * e->b_pad));
+        ENG_CUDA(e, dmalloc(&e->lam_f, (size_t)e->b_pad * (1 + launch::soft_chunks())));
+        if (e->debug) {
+            ENG_CUDA(e, dmalloc(&e->dbg_Gf, nb));
+            ENG_CUDA(e, dmalloc(&e->dbg_g1, nb));
+        }
+    }
+    // Adam step constants in fp64, per step index: lr / (1 - beta1^t), 1 / sqrt(1 - beta2^t)
+    std::vector<float2> consts((size_t)e->T + 2);
+    for (size_t t = 0; t < consts.size(); ++t) {
+        const double bc1 = 1.0 - std::pow(e->beta1, (double)t);
+        const double bc2 = 1.0 - std::pow(e->beta2, (double)t);
+        consts[t] = make_float2(t ? (float)(e->lr / bc1) : 0.f, t ? (float)(1.0 / std::sqrt(bc2)) : 0.f);
+    }
+    ENG_CUDA(e, dmalloc(&e->adam_consts, consts.size()));
+    ENG_CUDA(e, cudaMemcpyAsync(e->adam_consts, consts.data(), consts.size() * sizeof(float2), cudaMemcpyHostToDevice,
+                                e->stream));
+    if (!e->pins.empty()) {
+        std::vector<int8_t> pr((size_t)n, -1);
+        for (size_t r = 0; r < e->pins.size(); ++r) pr[e->pins[r]] = (int8_t)r;
+        ENG_CUDA(e, dmalloc(&e->pin_rank, (size_t)n));
+        ENG_CUDA(e, cudaMemcpyAsync(e->pin_rank, pr.data(), (size_t)n, cudaMemcpyHostToDevice, e->stream));
+    }
+    Ctrl h{};
+    h.t = 0;
+    h.stopped = 0;
+    h.best_u = INT32_MAX;
+    h.best_t = -1;
+    h.best_b = -1;
+    ENG_CUDA(e, cudaMallocHost((void **)&e->h_ctrl, 2 * sizeof(Ctrl)));
+    e->h_ctrl[0] = h;
+    ENG_CUDA(e, cudaMemcpyAsync(e->ctrl, &e->h_ctrl[0], sizeof(Ctrl), cudaMemcpyHostToDevice, e->stream));
+    ENG_CUDA(e, cudaStreamSynchronize(e->stream));   // h_ctrl[0] is reused below
+    for (auto &ev : e->poll_ev) ENG_CUDA(e, cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    if (e->world > 1) {
+        std::string why;
+        if (!e->comm.init(e->rank, e->world, e->nccl_id, &why)) return poison(e, GALOIS_E_NCCL, why);
+    }
+    e->prepared = true;
+    // a3: initial logits, first sample, and the check at t = 0
+    const StepParams p = e->params();
+    e->timed(5, [&] { launch::init(p, e->z, e->m, e->v, e->X, e->R, e->stream); });
+    ENG_CUDA(e, cudaGetLastError());
+    if (int rc = enqueue_check(e)) return rc;
+    return GALOIS_OK;
+}
+
+static int read_ctrl(galois_engine *e, Ctrl *out)
+{
+    ENG_CUDA(e, cudaMemcpyAsync(&e->h_ctrl[0], e->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, e->stream));
+    ENG_CUDA(e, cudaStreamSynchronize(e->stream));
+    *out = e->h_ctrl[0];
+    if (out->nonfinite) return poison(e, GALOIS_E_NONFINITE, "an iterate became NaN/Inf");
+    return GALOIS_OK;
+}
+
+extern "C" int galois_engine_step(galois_engine *e)
+{
+    ENGINE_ENTRY(e);
+    if (int rc = prepare(e)) return rc;
+    Ctrl h;
+    if (int rc = read_ctrl(e, &h)) return rc;
+    if (h.stopped) return GALOIS_SAT;
+    if (e->steps_enqueued >= e->T) return GALOIS_BUDGET;
+    if (int rc = enqueue_step(e)) return rc;
+    if (int rc = read_ctrl(e, &h)) return rc;
+    return h.stopped ? GALOIS_SAT : GALOIS_OK;
+}
+
+extern "C" int galois_engine_enqueue(galois_engine *e, int32_t max_steps)
+{
+    ENGINE_ENTRY(e);
+    if (int rc = prepare(e)) return rc;
+    if (e->steps_enqueued >= e->T) return GALOIS_BUDGET;
+    for (int32_t i = 0; i < max_steps && e->steps_enqueued < e->T; ++i)
+        if (int rc = enqueue_step(e)) return rc;
+    return GALOIS_OK;
+}
+
+extern "C" int galois_engine_run(galois_engine *e)
+{
+    ENGINE_ENTRY(e);
+    if (int rc = prepare(e)) return rc;
+    // chunks of steps; poll the stop flag of chunk i-1 while chunk i is queued
+    const int32_t chunk = std::max<int32_t>(1, std::min<int32_t>(16, e->K * 4));
+    int iter = 0;
+    while (e->steps_enqueued < e->T) {
+        for (int32_t i = 0; i < chunk && e->steps_enqueued < e->T; ++i)
+            if (int rc = enqueue_step(e)) return rc;
+        Ctrl *slot = &e->h_ctrl[iter & 1];
+        ENG_CUDA(e, cudaMemcpyAsync(slot, e->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, e->stream));
+        ENG_CUDA(e, cudaEventRecord(e->poll_ev[iter & 1], e->stream));
+        if (iter >= 1) {
+            ENG_CUDA(e, cudaEventSynchronize(e->poll_ev[(iter - 1) & 1]));
+            if (e->h_ctrl[(iter - 1) & 1].stopped) break;
+        }
+        ++iter;
+    }
+    Ctrl h;
+    if (int rc = read_ctrl(e, &h)) return rc;
+    return h.stopped ? GALOIS_SAT : GALOIS_BUDGET;
+}
+
+extern "C" int galois_engine_info(galois_engine *e, int64_t *local_batch, int64_t *first_global_b,
+                                  int32_t *steps_done, int32_t *stopped)
+{
+    ENGINE_ENTRY(e);
+    if (int rc = prepare(e)) return rc;
+    Ctrl h;
+    if (int rc = read_ctrl(e, &h)) return rc;
+    if (local_batch) *local_batch = e->b_loc;
+    if (first_global_b) *first_global_b = e->b0;
+    if (steps_done) *steps_done = h.t;
+    if (stopped) *stopped = h.stopped;
+    return GALOIS_OK;
+}
+
+extern "C" int galois_best_assignment(galois_engine *e, uint8_t *values, int32_t *unsat, int64_t *global_b,
+                                      int32_t *step)
+{
+    ENGINE_ENTRY(e);
+    if (int rc = prepare(e)) return rc;
+    Ctrl h;
+    if (int rc = read_ctrl(e, &h)) return rc;
+    if (e->world > 1 && h.best_b >= 0) {
+        const int root = (int)(h.best_b / e->b_per);
+        std::string why;
+        if (!e->comm.broadcast_bytes(e->best_bits, (size_t)e->cnf->n, root, e->stream, &why))
+            return poison(e, GALOIS_E_NCCL, why);
+    }
+    if (values) ENG_CUDA(e, cudaMemcpyAsync(values, e->best_bits, (size_t)e->cnf->n, cudaMemcpyDeviceToHost, e->stream));
+    ENG_CUDA(e, cudaStreamSynchronize(e->stream));
+    if (unsat) *unsat = h.best_u;
+    if (global_b) *global_b = h.best_b;
+    if (step) *step = h.best_t;
+    return GALOIS_OK;
+}
+
+extern "C" int galois_unsat_counts(galois_engine *e, int32_t *counts, int64_t *first_global_b)
+{
+    ENGINE_ENTRY(e);
+    if (int rc = prepare(e)) return rc;
+    if (counts && e->b_loc > 0)
+        ENG_CUDA(e, cudaMemcpyAsync(counts, e->unsat, sizeof(int32_t) * (size_t)e->b_loc, cudaMemcpyDeviceToHost,
+                                    e->stream));
+    ENG_CUDA(e, cudaStreamSynchronize(e->stream));
+    if (first_global_b) *first_global_b = e->b0;
+    return GALOIS_OK;
+}
+
+// [n][b_pad] device -> [b_loc][n] host
+template <typename T>
+static int copy_transposed_out(galois_engine *e, const T *dev, T *host)
+{
+    const int32_t n = e->cnf->n;
+    std::vector<T> tmp((size_t)n * e->b_pad);
+    ENG_CUDA(e, cudaMemcpyAsync(tmp.data(), dev, tmp.size() * sizeof(T), cudaMemcpyDeviceToHost, e->stream));
+    ENG_CUDA(e, cudaStreamSynchronize(e->stream));
+    for (int32_t b = 0; b < e->b_loc; ++b)
+        for (int32_t v = 0; v < n; ++v) host[(size_t)b * n + v] = tmp[(size_t)v * e->b_pad + b];
+    return GALOIS_OK;
+}
+
+extern "C" int galois_engine_get_iterate(galois_engine *e, float *z, float *m, float *v, int32_t *t)
+{
+    ENGINE_ENTRY(e);
+    if (int rc = prepare(e)) return rc;
+    if (z) if (int rc = copy_transposed_out(e, e->z, z)) return rc;
+    if (m) if (int rc = copy_transposed_out(e, e->m, m)) return rc;
+    if (v) if (int rc = copy_transposed_out(e, e->v, v)) return rc;
+    if (t) {
+        Ctrl h;
+        if (int rc = read_ctrl(e, &h)) return rc;
+        *t = h.t;
+    }
+    return GALOIS_OK;
+}
+
+extern "C" int galois_engine_set_iterate(galois_engine *e, const float *z, const float *m, const float *v, int32_t t)
+{
+    ENGINE_ENTRY(e);
+    if (!z || !m || !v) return fail(GALOIS_E_ARG, "z, m and v are required");
+    if (t < 0 || t > e->T) return fail(GALOIS_E_ARG, "t must be in [0, steps]");
+    if (int rc = prepare(e)) return rc;
+    const int32_t n = e->cnf->n;
+    const float *src[3] = {z, m, v};
+    float *dst[3] = {e->z, e->m, e->v};
+    std::vector<float> tmp((size_t)n * e->b_pad);
+    ENG_CUDA(e, cudaStreamSynchronize(e->stream));
+    for (int a = 0; a < 3; ++a) {
+        ENG_CUDA(e, cudaMemcpy(tmp.data(), dst[a], tmp.size() * 4, cudaMemcpyDeviceToHost));  // keep padding
+        for (int32_t b = 0; b < e->b_loc; ++b)
+            for (int32_t x = 0; x < n; ++x) tmp[(size_t)x * e->b_pad + b] = src[a][(size_t)b * n + x];
+        ENG_CUDA(e, cudaMemcpy(dst[a], tmp.data(), tmp.size() * 4, cudaMemcpyHostToDevice));
+    }
+    Ctrl h;
+    if (int rc = read_ctrl(e, &h)) return rc;
+    h.t = t;
+    h.stopped = 0;
+    h.nonfinite = 0;
+    e->h_ctrl[0] = h;
+    ENG_CUDA(e, cudaMemcpyAsync(e->ctrl, &e->h_ctrl[0], sizeof(Ctrl), cudaMemcpyHostToDevice, e->stream));
+    launch::resample(e->params(), e->z, e->X, e->R, t + 1, e->stream);
+    ENG_CUDA(e, cudaGetLastError());
+    ENG_CUDA(e, cudaStreamSynchronize(e->stream));
+    e->steps_enqueued = t;
+    return GALOIS_OK;
+}
+
+extern "C" int galois_engine_get_grad(galois_engine *e, int32_t *G, float *g1)
+{
+    ENGINE_ENTRY(e);
+    if (!e->debug) return fail(GALOIS_E_STATE, "get_grad needs set_debug(1) before the first step");
+    if (int rc = prepare(e)) return rc;
+    if (G) {
+        if (e->mode == GALOIS_MODE_ST) {
+            if (int rc = copy_transposed_out(e, e->dbg_G, G)) return rc;
+        } else {
+            std::vector<float> tmp((size_t)e->b_loc * e->cnf->n);
+            if (int rc = copy_transposed_out(e, e->dbg_Gf, tmp.data())) return rc;
+            for (size_t i = 0; i < tmp.size(); ++i) G[i] = (int32_t)lrintf(tmp[i]);
+        }
+    }
+    if (g1) if (int rc = copy_transposed_out(e, e->dbg_g1, g1)) return rc;
+    return GALOIS_OK;
+}
+
+extern "C" int galois_engine_get_loss(galois_engine *e, float *lambda)
+{
+    ENGINE_ENTRY(e);
+    if (!lambda) return fail(GALOIS_E_ARG, "lambda is NULL");
+    if (int rc = prepare(e)) return rc;
+    if (e->mode == GALOIS_MODE_ST) {
+        std::vector<int32_t> tmp((size_t)e->b_pad);
+        ENG_CUDA(e, cudaMemcpyAsync(tmp.data(), e->lam, tmp.size() * 4, cudaMemcpyDeviceToHost, e->stream));
+        ENG_CUDA(e, cudaStreamSynchronize(e->stream));
+        for (int32_t b = 0; b < e->b_loc; ++b) lambda[b] = (float)tmp[b];
+    } else {
+        ENG_CUDA(e, cudaMemcpyAsync(lambda, e->lam_f, (size_t)e->b_loc * 4, cudaMemcpyDeviceToHost, e->stream));
+        ENG_CUDA(e, cudaStreamSynchronize(e->stream));
+    }
+    return GALOIS_OK;
+}
+
+extern "C" int galois_engine_get_bits(galois_engine *e, uint8_t *x_next, uint8_t *r)
+{
+    ENGINE_ENTRY(e);
+    if (int rc = prepare(e)) return rc;
+    const int32_t n = e->cnf->n;
+    std::vector<uint32_t> tmp((size_t)n * e->W);
+    uint8_t *outs[2] = {x_next, r};
+    uint32_t *srcs[2] = {e->X, e->R};
+    for (int a = 0; a < 2; ++a) {
+        if (!outs[a]) continue;
+        ENG_CUDA(e, cudaMemcpyAsync(tmp.data(), srcs[a], tmp.size() * 4, cudaMemcpyDeviceToHost, e->stream));
+        ENG_CUDA(e, cudaStreamSynchronize(e->stream));
+        for (int32_t b = 0; b < e->b_loc; ++b)
+            for (int32_t v = 0; v < n; ++v)
+                outs[a][(size_t)b * n + v] = (uint8_t)((tmp[(size_t)v * e->W + (b >> 5)] >> (b & 31)) & 1u);
+    }
+    return GALOIS_OK;
+}
+
+extern "C" int galois_engine_kernel_times(galois_engine *e, double *ms, int64_t *launches)
+{
+    ENGINE_ENTRY(e);
+    if (ms) std::fill(ms, ms + GALOIS_NUM_KERNEL_CLASSES, 0.0);
+    if (launches) std::fill(launches, launches + GALOIS_NUM_KERNEL_CLASSES, 0);
+    if (e->stream) ENG_CUDA(e, cudaStreamSynchronize(e->stream));
+    for (auto &r : e->recs) {
+        float t = 0.f;
+        ENG_CUDA(e, cudaEventElapsedTime(&t, r.a, r.b));
+        if (ms) ms[r.cls] += t;
+        if (launches) launches[r.cls] += 1;
+        e->ev_pool.push_back(r.a);
+        e->ev_pool.push_back(r.b);
+    }
+    e->recs.clear();
+    return GALOIS_OK;
+}
+
+extern "C" void galois_engine_free(galois_engine *e)
+{
+    if (!e) return;
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(e->device);
+    if (e->stream) cudaStreamSynchronize(e->stream);
+    e->comm.destroy(e->poisoned);
+    engine_free_buffers(e);
+    for (auto &r : e->recs) {
+        cudaEventDestroy(r.a);
+        cudaEventDestroy(r.b);
+    }
+    for (auto ev : e->ev_pool) cudaEventDestroy(ev);
+    for (auto ev : e->poll_ev)
+        if (ev) cudaEventDestroy(ev);
+    if (e->own_stream && e->stream) cudaStreamDestroy(e->stream);
+    cnf_release(e->cnf);
+    cudaSetDevice(cur);
+    delete e;
+}
+
+extern "C" const char *galois_last_error(void) { return g_last_error.c_str(); }

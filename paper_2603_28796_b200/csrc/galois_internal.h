@@ -1,0 +1,77 @@
+// galois_internal.h — device data layout shared by the CUDA sources of libgalois.
+//
+// HBM layout. n variables, m clauses, L literal slots, a rank's
+// b_pad members (b_loc valid, padded to a multiple of 32), W = b_pad / 32 words:
+//   CSR  clause_off[m+1] int32, slot_info[L] int2 = {lit code (v<<1)|neg, CSC position}
+//   CSC  code_off[2n+1] int32: occurrences of literal code c are CSC positions
+//        [code_off[c], code_off[c+1]), ascending slot order (stable counting sort)
+//   state z, m, v float [n][b_pad]  (reduced iterate z = theta_1 - theta_0)
+//   bits  X, R uint32 [n][W]        (bit j of word w = member 32w + j)
+//   E     uint32 [L][W] in CSC order (exclusive products of each occurrence)
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace galois {
+
+constexpr int kHubDegree = 1024;     // variables with more occurrences use the hub path
+constexpr int kHubChunk = 512;       // occurrences per hub partial item
+
+// Device-side control block (one per engine, device memory).
+struct Ctrl {
+    int32_t t;            // steps done (incremented by the forward of each step)
+    int32_t stopped;      // 1 once the best member satisfies the CNF
+    int32_t best_u;       // best unsat count so far (INT32_MAX = none)
+    int32_t best_t;       // step of the best
+    int64_t best_b;       // global member index of the best
+    int32_t improved;     // last finalize improved the best AND this rank owns it
+    int32_t nonfinite;    // sticky: an iterate became NaN/Inf
+    unsigned long long key_local;   // (u << 32) | global b, min over local members
+    unsigned long long key_global;  // same, min over ranks (NCCL MIN)
+    int32_t last_check_t; // step of the last check
+    int32_t pad;
+};
+
+struct DevCnf {
+    int32_t n;
+    int32_t m;
+    int32_t L;
+    const int32_t *clause_off;   // [m+1]
+    const int2 *slot_info;       // [L] {code, csc position}
+    const int32_t *code_off;     // [2n+1]
+    const int32_t *occ_slot;     // [L]
+    // hub path
+    int32_t num_hubs;
+    int32_t num_hub_chunks;
+    const int32_t *hub_of_var;   // [n] hub index or -1
+    const int32_t *hub_chunk_off;// [num_hubs+1] first chunk of each hub
+    const int2 *hub_chunk;       // [num_hub_chunks] {var, first CSC position}
+};
+
+struct StepParams {
+    int32_t n;
+    int32_t b_pad;
+    int32_t W;
+    int32_t b_loc;
+    int64_t b0;               // global index of local member 0
+    uint64_t seed;
+    float tau, inv_tau;
+    float beta1, beta2, eps;
+    float omb1, omb2;         // 1 - beta1, 1 - beta2 (rounded from fp64)
+    int32_t optimizer;        // 0 Adam, 1 SGD
+    float lr;
+    const float2 *adam_consts;// [steps+2] {lr / (1 - beta1^t), 1 / sqrt(1 - beta2^t)}
+    int32_t num_pins;
+    const int8_t *pin_rank;   // [n] r or -1 (NULL if no pins)
+};
+
+// kernels (launch wrappers in kernels.cu)
+cudaError_t launch_build_cnf(int32_t n, int64_t m, int64_t L, const int64_t *d_offsets64,
+                             const int32_t *d_lits, int32_t *d_clause_off, int2 *d_slot_info,
+                             int32_t *d_code_off, int32_t *d_occ_slot, int32_t *d_err,
+                             int32_t *d_max_width, void *d_scratch, size_t scratch_bytes,
+                             cudaStream_t st);
+size_t build_cnf_scratch_bytes(int32_t n, int64_t L);
+
+}  // namespace galois

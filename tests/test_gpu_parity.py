@@ -1,0 +1,223 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle (-m gpu)."""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2603_28796_b200 import instances as I
+from tests import parity
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def G():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_2603_28796_b200 import galois
+    galois.lib()
+    return galois
+
+
+# --------------------------------------------------------------------------- a1 / a2
+def test_cnf_load_device_validation(G):
+    with pytest.raises(G.GaloisError) as e:
+        G.Cnf(3, np.array([0, 2, 1, 3], np.int64), np.array([1, 2, 3], np.int32))
+    assert e.value.code == G.E_OFFSETS
+    with pytest.raises(G.GaloisError) as e:
+        G.Cnf(3, np.array([0, 2, 3], np.int64), np.array([1, 4, 3], np.int32))
+    assert e.value.code == G.E_VAR_RANGE
+    with pytest.raises(G.GaloisError) as e:
+        G.Cnf(3, np.array([0, 2, 3], np.int64), np.array([1, 0, 3], np.int32))
+    assert e.value.code == G.E_VAR_RANGE
+    with pytest.raises(G.GaloisError) as e:
+        G.Cnf(3, np.array([0, 2, 2, 3], np.int64), np.array([1, -2, 3], np.int32))
+    assert e.value.code == G.E_EMPTY_CLAUSE
+    c = G.Cnf(3, np.array([0], np.int64), np.zeros(0, np.int32))       # zero clauses is fine
+    assert c.info()["m"] == 0
+
+
+@pytest.mark.parametrize("which", ["small", "3sat", "industrial", "wide_n"])
+def test_csc_is_stable_counting_sort(G, which):
+    """a2: the device transpose equals numpy's stable argsort of the literal codes
+    (variable, sign, slot order) — bit-exact, including several radix passes."""
+    inst = {"small": lambda: I.from_clauses("t", 5, [[1, -2, 5], [-5, 3, 4], [-1, 3, 3]]),
+            "3sat": lambda: I.random_ksat(3000, 12000, 3, 1),
+            "industrial": lambda: I.industrial(40_000, 160_000, 3),
+            "wide_n": lambda: I.random_ksat(200_000, 300_000, 4, 2)}[which]()
+    c = G.Cnf.from_instance(inst)
+    code_off, occ = c.csc()
+    lits = inst.lits.astype(np.int64)
+    code = (np.abs(lits) - 1) * 2 + (lits < 0)
+    np.testing.assert_array_equal(occ, np.argsort(code, kind="stable"))
+    np.testing.assert_array_equal(code_off, np.concatenate([[0], np.cumsum(np.bincount(code, minlength=2 * inst.n))]))
+    info = c.info()
+    deg = I.degrees(inst)
+    assert info["max_degree"] == deg.max()
+    assert info["max_width"] == np.diff(inst.offsets).max()
+    assert info["num_hubs"] == int((deg > 1024).sum())
+
+
+# --------------------------------------------------------------------------- a3-a8
+@pytest.mark.parametrize("batch", [32, 64, 100, 256])
+def test_init_and_t0_check(G, batch):
+    """a3 + a8 at t = 0: z0 = theta_1 - theta_0 from the same Philox counters, R_0, the
+    exact unsat counts and the best at t = 0."""
+    inst = I.random_ksat(50, 213, 3, 0)
+    rep = parity.run_trajectory(G, inst, batch, steps=0)
+    assert rep.best_gpu == rep.best_oracle
+
+
+@pytest.mark.parametrize("t", [0, 1, 7, 40])
+@pytest.mark.parametrize("which", ["3sat", "mixed", "dups"])
+def test_one_step_identical_iterate(G, which, t):
+    """a4-a8 from identical iterates: X, R bit-exact (outside the tie zone), Lambda and G
+    exact, g1 within relative 1e-5, z/m/v within 1e-5."""
+    inst = {"3sat": lambda: I.random_ksat(60, 255, 3, 3),
+            "mixed": lambda: I.industrial(300, 1500, 4),
+            "dups": lambda: I.from_clauses("dups", 6, [[1, 1, -2], [2, -3, 3], [4, 5, 6, -1, 2, 3, 4, 5, 6, -6],
+                                                        [-4], [5, -5], [1, 2, 3, 4, 5, 6, -1, -2, -3, -4]])}[which]()
+    res = parity.one_step(G, inst, 96, t)
+    assert res["tie_x"] + res["tie_r"] <= 2
+
+
+def test_trajectory_50_steps(G):
+    """North star: per-step trajectories within 1e-4 for 50 steps on small instances."""
+    inst = I.random_ksat(50, 213, 3, 5)
+    rep = parity.run_trajectory(G, inst, 128, 50, seed=3, stop_on_sat=False)
+    assert rep.steps == 50
+    assert len(rep.resyncs) <= 3, rep.resyncs
+    assert rep.best_gpu == rep.best_oracle
+
+
+def test_trajectory_mixed_widths_check_interval(G):
+    inst = I.industrial(400, 1800, 7)
+    rep = parity.run_trajectory(G, inst, 64, 30, seed=11, check_interval=4, stop_on_sat=False)
+    assert rep.best_gpu == rep.best_oracle
+
+
+def test_first_sat_matches_oracle_C1(G):
+    """configs[0]: 3-SAT n=50, m=213, B=1024, 100 steps: the first satisfying member and
+    step found by the engine are the oracle's."""
+    inst = I.random_ksat(50, 213, 3, 0)
+    rep = parity.run_trajectory(G, inst, 1024, 100, seed=0)
+    assert rep.best_gpu == rep.best_oracle, rep
+
+
+def test_run_equals_stepwise(G):
+    """galois_engine_run (chunked, device stop flag) gives the same best and step count
+    as stepping one call at a time; a SAT stop freezes the engine."""
+    inst = I.random_ksat(40, 160, 3, 2, planted=True)
+    out = []
+    for mode in ("run", "step"):
+        cnf = G.Cnf.from_instance(inst)
+        eng = G.Engine(cnf, 512, 60, 0.5, 4)
+        if mode == "run":
+            rc = eng.run()
+        else:
+            rc = G.OK
+            while rc == G.OK:
+                rc = eng.step()
+        best = eng.best_assignment()
+        info = eng.info()
+        out.append((rc, best["unsat"], best["step"], best["global_b"], info["steps_done"], info["stopped"]))
+        f = O.Cnf(inst.n, inst.offsets, inst.lits)
+        assert O.unsat_count(f, best["values"]) == best["unsat"]
+        eng.free()
+    assert out[0] == out[1]
+    if out[0][0] == G.SAT:
+        assert out[0][1] == 0 and out[0][4] == out[0][2]
+
+
+def test_batch_independence_and_determinism(G):
+    """Member b's trajectory does not depend on B (global RNG counters) and repeats are
+    bit-identical."""
+    inst = I.random_ksat(80, 336, 3, 6)
+    states = []
+    for B in (64, 64, 160):
+        cnf = G.Cnf.from_instance(inst)
+        eng = G.Engine(cnf, B, 12, 0.5, 9)
+        for _ in range(12):
+            eng.step()
+        z, m, v, t = eng.get_iterate()
+        x, r = eng.get_bits()
+        states.append((z[:64], m[:64], v[:64], x[:64], r[:64]))
+        eng.free()
+    for a, b in zip(states[0], states[1]):
+        np.testing.assert_array_equal(a, b)
+    for a, b in zip(states[0], states[2]):
+        np.testing.assert_array_equal(a, b)
+
+
+def test_cubes(G):
+    """Lemma 1 cube pins: pinned variables follow alpha = b mod 2^d, never move, and the
+    engine matches the oracle with pins."""
+    inst = I.random_ksat(60, 250, 3, 8)
+    cubes = I.top_degree_vars(inst, 5)
+    rep = parity.run_trajectory(G, inst, 64, 15, seed=2, cubes=cubes, stop_on_sat=False)
+    assert rep.best_gpu == rep.best_oracle
+    cnf = G.Cnf.from_instance(inst)
+    eng = G.Engine(cnf, 64, 5, 0.5, 2, cubes=cubes)
+    z0 = eng.get_iterate()[0]
+    for _ in range(5):
+        eng.step()
+    z, _, _, _ = eng.get_iterate()
+    x, r = eng.get_bits()
+    idx = np.array(cubes) - 1
+    np.testing.assert_array_equal(z[:, idx], z0[:, idx])
+    for b in range(64):
+        expect = [(b >> k) & 1 for k in range(5)]
+        assert list(r[b, idx]) == expect and list(x[b, idx]) == expect
+
+
+def test_sgd_and_tau(G):
+    inst = I.random_ksat(50, 200, 3, 9)
+    parity.one_step(G, inst, 64, 3, optimizer=1, lr=0.2)
+    parity.one_step(G, inst, 64, 3, tau=0.5)
+    rep = parity.run_trajectory(G, inst, 64, 20, seed=1, tau=1.7, stop_on_sat=False)
+    assert rep.best_gpu == rep.best_oracle
+
+
+@pytest.mark.parametrize("t", [0, 5])
+def test_soft_mode_one_step(G, t):
+    """SOFT mode: fp32 relaxed forward/backward vs the fp64 oracle."""
+    inst = I.industrial(200, 900, 5)
+    parity.one_step(G, inst, 64, t, mode=1)
+
+
+def test_hub_path_exact(G):
+    """Variables with > 1024 occurrences are reduced through deterministic chunked
+    partials; their signal G must still equal the oracle's exactly."""
+    inst = I.industrial(3000, 60_000, 12, occ_exp=1.0)
+    deg = I.degrees(inst)
+    assert (deg > 1024).sum() >= 2
+    res = parity.one_step(G, inst, 64, 2)
+    assert res["tie_x"] + res["tie_r"] <= 2
+
+
+def test_full_size_sampled_C2(G):
+    """configs[1] at full size in the bench launch configuration (B = 4096): one step, then
+    the sampled members' Lambda, unsat counts and bits against the oracle computed for
+    those members only (global RNG counters make members independent)."""
+    inst = I.random_ksat(10_000, 42_000, 3, 0)
+    f = O.Cnf(inst.n, inst.offsets, inst.lits)
+    cnf = G.Cnf.from_instance(inst)
+    eng = G.Engine(cnf, 4096, 50, 0.5, 0, debug=True)
+    eng.step()
+    lam = eng.get_loss()
+    u, _ = eng.unsat_counts()
+    x, r = eng.get_bits()
+    Gg, _ = eng.get_grad()
+    for b in (0, 1, 31, 32, 1000, 2047, 4095):
+        st = O.State.init(inst.n, b, 1, 0)
+        out = O.step(f, parity.oracle_cfg(0), st)
+        ties = np.abs(out["a"][0]) <= 1e-5 * (1 + np.abs(st.reduced()[0][0]))
+        if not ties.any():
+            assert lam[b] == out["lam"][0]
+            np.testing.assert_array_equal(Gg[b], out["G"][0].astype(np.int32))
+        zo = st.reduced()[0][0]
+        safe = np.abs(zo) > 1e-4 * np.maximum(1, np.abs(zo))
+        np.testing.assert_array_equal(r[b][safe], out["r"][0][safe])
+        if safe.all() and not ties.any():
+            assert u[b] == out["unsat"][0]
+    eng.free()
