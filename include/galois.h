@@ -91,7 +91,7 @@ void galois_cnf_free(galois_cnf *cnf);
  * rate lr > 0 (paper 0.5) and RNG seed. Defaults: ST mode, tau = 1, Adam (0.9, 0.999,
  * 1e-8), check interval 1, no cubes, world = 1. Device memory is allocated and the
  * logits initialised lazily at the first step/run/get (so setters may follow create). */
-int galois_engine_create(const galois_cnf *cnf, int64_t batch, int32_t steps, float lr,
+int galois_engine_create(const galois_cnf *cnf, int64_t batch, int32_t steps, double lr,
                          uint64_t seed, galois_engine **out);
 
 /* One optimiser step t -> t+1 (sample, clause forward, straight-through gradient,
@@ -139,7 +139,7 @@ int galois_engine_set_mode(galois_engine *eng, int32_t mode);
 
 /* tau > 0 (Eq.3; paper 1.0), Adam beta1, beta2 in [0,1), eps > 0, optimizer
  * 0 = Adam (App. A), 1 = plain gradient step theta -= lr g. */
-int galois_engine_set_hparams(galois_engine *eng, float tau, float beta1, float beta2, float eps,
+int galois_engine_set_hparams(galois_engine *eng, double tau, double beta1, double beta2, double eps,
                               int32_t optimizer);
 
 /* Check (round + exact count + best update) at t = 0, every k >= 1 steps, and at the

@@ -384,7 +384,7 @@ static void engine_free_buffers(galois_engine *e)
     e->z = e->m = e->v = nullptr;
 }
 
-extern "C" int galois_engine_create(const galois_cnf *cnf, int64_t batch, int32_t steps, float lr, uint64_t seed,
+extern "C" int galois_engine_create(const galois_cnf *cnf, int64_t batch, int32_t steps, double lr, uint64_t seed,
                                     galois_engine **out)
 {
     if (!out) return fail(GALOIS_E_ARG, "out is NULL");
@@ -425,7 +425,7 @@ extern "C" int galois_engine_set_mode(galois_engine *e, int32_t mode)
     return GALOIS_OK;
 }
 
-extern "C" int galois_engine_set_hparams(galois_engine *e, float tau, float beta1, float beta2, float eps,
+extern "C" int galois_engine_set_hparams(galois_engine *e, double tau, double beta1, double beta2, double eps,
                                          int32_t optimizer)
 {
     SETTER_ENTRY(e);

@@ -57,7 +57,7 @@ def lib() -> ctypes.CDLL:
             raise RuntimeError(f"{LIB_PATH} is missing: run `python -m paper_2603_28796_b200.build` "
                                "(there is no CPU fallback)")
         L = ctypes.CDLL(LIB_PATH)
-        P, I32, I64, U64, F = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_float
+        P, I32, I64, U64, F = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_double
         sig = {
             "galois_cnf_load": [I32, I64, P, P, P],
             "galois_cnf_info": [P, P, P, P, P, P, P],

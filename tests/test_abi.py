@@ -73,7 +73,7 @@ def test_host_argument_checks(G):
     assert lib.galois_cnf_load(2, -1, off.ctypes.data, lits.ctypes.data, ctypes.byref(h)) == G.E_ARG
     assert lib.galois_cnf_load(2, 2, off.ctypes.data, None, ctypes.byref(h)) == G.E_ARG
     e = ctypes.c_void_p()
-    assert lib.galois_engine_create(None, 4, 1, ctypes.c_float(0.5), 0, ctypes.byref(e)) == G.E_ARG
+    assert lib.galois_engine_create(None, 4, 1, ctypes.c_double(0.5), 0, ctypes.byref(e)) == G.E_ARG
     assert lib.galois_engine_step(None) == G.E_ARG
     assert lib.galois_engine_run(None) == G.E_ARG
     assert lib.galois_best_assignment(None, None, None, None, None) == G.E_ARG
