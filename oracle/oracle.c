@@ -66,18 +66,18 @@ void oracle_philox4x32_10(const uint32_t ctr_in[4], const uint32_t key_in[2], ui
     out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
 }
 
-/* Open-interval uniform from the top 23 bits of a 32-bit word (reading R2):
- * u = (k + 1/2) 2^-23 with k = w >> 9, so u and 1-u are both exact binary
+/* Open-interval uniform from the low 23 bits of a 32-bit word (reading R2):
+ * u = (k + 1/2) 2^-23 with k = w mod 2^23, so u and 1-u are both exact binary
  * fractions with 24 significant bits. */
 double oracle_uniform(uint32_t w)
 {
-    uint32_t k = w >> 9;
+    uint32_t k = w & 0x7FFFFFu;
     return ((double)k + 0.5) / 8388608.0;
 }
 
 double oracle_uniform_complement(uint32_t w)
 {
-    uint32_t k = w >> 9;
+    uint32_t k = w & 0x7FFFFFu;
     return ((double)(8388607u - k) + 0.5) / 8388608.0;
 }
 

@@ -17,7 +17,7 @@ LIB = os.path.join(PKG, "libgalois.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O2,-Wall", "-Xptxas", "-v",
+FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-ftz=true", "-Xcompiler", "-fPIC,-O2,-Wall", "-Xptxas", "-v",
          "--expt-relaxed-constexpr", f"-I{os.path.join(ROOT, 'include')}", f"-I{CSRC}"]
 SOURCES = ["cnf_build.cu", "step_kernels.cu", "soft_kernels.cu", "engine.cu", "comm.cpp"]
 HEADERS = ["galois_internal.h", "philox.cuh", "comm.h"]

@@ -28,10 +28,10 @@ void forward_st(const DevCnf &c, int32_t W, int32_t b_pad, const uint32_t *X, ui
                 Ctrl *ctrl, cudaStream_t st);
 void check(const DevCnf &c, int32_t W, int32_t b_pad, const uint32_t *R, int32_t *unsat, Ctrl *ctrl,
            cudaStream_t st);
-void hub_partial(const DevCnf &c, int32_t W, int32_t b_pad, const uint32_t *E, int4 *partial,
+void hub_partial(const DevCnf &c, int32_t W, int32_t b_pad, const uint32_t *E, short4 *partial,
                  const Ctrl *ctrl, cudaStream_t st);
 void update_st(const DevCnf &c, const StepParams &p, float *z, float *m, float *v, uint32_t *X, uint32_t *R,
-               const uint32_t *E, const int4 *partial, Ctrl *ctrl, int32_t *dbg_G, float *dbg_g1,
+               const uint32_t *E, const short4 *partial, Ctrl *ctrl, int32_t *dbg_G, float *dbg_g1,
                cudaStream_t st);
 void best(const int32_t *unsat, int32_t b_loc, int64_t b0, Ctrl *ctrl, bool finalize, cudaStream_t st);
 void finalize(Ctrl *ctrl, int64_t b0, int32_t b_loc, cudaStream_t st);
@@ -303,7 +303,7 @@ struct galois_engine {
     // device buffers
     float *z = nullptr, *m = nullptr, *v = nullptr;
     uint32_t *X = nullptr, *R = nullptr, *E = nullptr;
-    int4 *partial = nullptr;
+    short4 *partial = nullptr;
     int32_t *lam = nullptr, *unsat = nullptr;
     Ctrl *ctrl = nullptr;
     uint8_t *best_bits = nullptr;
@@ -343,6 +343,7 @@ struct galois_engine {
         p.adam_consts = adam_consts;
         p.num_pins = (int32_t)pins.size();
         p.pin_rank = pins.empty() ? nullptr : pin_rank;
+        p.keys = philox_round_keys(seed);
         return p;
     }
 
@@ -529,20 +530,15 @@ static int enqueue_check(galois_engine *e)
     const DevCnf c = e->cnf->view();
     ENG_CUDA(e, cudaMemsetAsync(e->unsat, 0, sizeof(int32_t) * (size_t)e->b_pad, e->stream));
     e->timed(2, [&] { launch::check(c, e->W, e->b_pad, e->R, e->unsat, e->ctrl, e->stream); });
-    e->timed(3, [&] {
-        launch::best(e->unsat, e->b_loc, e->b0, e->ctrl, e->world == 1, e->stream);
-        if (e->world > 1) {
-            std::string why;
-            if (!e->comm.allreduce_min_u64(&e->ctrl->key_local, &e->ctrl->key_global, e->stream, &why)) {
-                e->poisoned = true;
-                g_last_error = why;
-                return;
-            }
-            launch::finalize(e->ctrl, e->b0, e->b_loc, e->stream);
-        }
-        launch::extract(e->R, e->cnf->n, e->W, e->b0, e->ctrl, e->best_bits, e->stream);
-    });
-    if (e->poisoned) return GALOIS_E_NCCL;
+    // one record per kernel, so the launch counts of galois_engine_kernel_times are exact
+    e->timed(3, [&] { launch::best(e->unsat, e->b_loc, e->b0, e->ctrl, e->world == 1, e->stream); });
+    if (e->world > 1) {
+        std::string why;
+        if (!e->comm.allreduce_min_u64(&e->ctrl->key_local, &e->ctrl->key_global, e->stream, &why))
+            return poison(e, GALOIS_E_NCCL, why);
+        e->timed(3, [&] { launch::finalize(e->ctrl, e->b0, e->b_loc, e->stream); });
+    }
+    e->timed(3, [&] { launch::extract(e->R, e->cnf->n, e->W, e->b0, e->ctrl, e->best_bits, e->stream); });
     ENG_CUDA(e, cudaGetLastError());
     return GALOIS_OK;
 }
@@ -623,12 +619,13 @@ static int prepare(galois_engine *e)
             ENG_CUDA(e, dmalloc(&e->dbg_g1, nb));
         }
     }
-    // Adam step constants in fp64, per step index: lr / (1 - beta1^t), 1 / sqrt(1 - beta2^t)
+    // Adam step constants in fp64, per step index: 2 lr / (1 - beta1^t), 1 / sqrt(1 - beta2^t)
+    // (the factor 2: z = theta_1 - theta_0 moves by twice the per-logit step)
     std::vector<float2> consts((size_t)e->T + 2);
     for (size_t t = 0; t < consts.size(); ++t) {
         const double bc1 = 1.0 - std::pow(e->beta1, (double)t);
         const double bc2 = 1.0 - std::pow(e->beta2, (double)t);
-        consts[t] = make_float2(t ? (float)(e->lr / bc1) : 0.f, t ? (float)(1.0 / std::sqrt(bc2)) : 0.f);
+        consts[t] = make_float2(t ? (float)(2.0 * e->lr / bc1) : 0.f, t ? (float)(1.0 / std::sqrt(bc2)) : 0.f);
     }
     ENG_CUDA(e, dmalloc(&e->adam_consts, consts.size()));
     ENG_CUDA(e, cudaMemcpyAsync(e->adam_consts, consts.data(), consts.size() * sizeof(float2), cudaMemcpyHostToDevice,

@@ -13,10 +13,12 @@
 
 #include <cstdint>
 
+#include "philox.cuh"
+
 namespace galois {
 
-constexpr int kHubDegree = 1024;     // variables with more occurrences use the hub path
-constexpr int kHubChunk = 512;       // occurrences per hub partial item
+constexpr int kHubDegree = 256;      // variables with more occurrences use the hub path
+constexpr int kHubChunk = 128;       // occurrences per hub partial item (|partial| <= 128: int16)
 
 // Device-side control block (one per engine, device memory).
 struct Ctrl {
@@ -49,6 +51,19 @@ struct DevCnf {
     const int2 *hub_chunk;       // [num_hub_chunks] {var, first CSC position}
 };
 
+// Work layout of the per-variable kernels: one thread per QUAD (4 members) of a row; a
+// 256-thread CTA covers one 256-quad chunk of a row (QW >= 256) or R = 256 / QW whole
+// rows (QW < 256). Item i = (row group i / cpr, chunk i % cpr). No per-quad division.
+struct RowMap {
+    uint32_t QW;        // quads per row = b_pad / 4 (a multiple of 8)
+    uint32_t cpr;       // 256-quad chunks per row (1 when QW < 256)
+    uint32_t R;         // rows per item (1 when QW >= 256)
+    uint32_t rows;      // number of rows (variables, or hub chunks)
+    uint32_t items;     // ceil(rows / R) * cpr
+    uint32_t div_mul;   // fast division by cpr: q = (umulhi(x, mul) + x) >> shift
+    uint32_t div_shift;
+};
+
 struct StepParams {
     int32_t n;
     int32_t b_pad;
@@ -61,9 +76,10 @@ struct StepParams {
     float omb1, omb2;         // 1 - beta1, 1 - beta2 (rounded from fp64)
     int32_t optimizer;        // 0 Adam, 1 SGD
     float lr;
-    const float2 *adam_consts;// [steps+2] {lr / (1 - beta1^t), 1 / sqrt(1 - beta2^t)}
+    const float2 *adam_consts;// [steps+2] {2 lr / (1 - beta1^t), 1 / sqrt(1 - beta2^t)}
     int32_t num_pins;
     const int8_t *pin_rank;   // [n] r or -1 (NULL if no pins)
+    PhiloxKeys keys;          // round keys of the seed (philox.cuh)
 };
 
 // kernels (launch wrappers in kernels.cu)

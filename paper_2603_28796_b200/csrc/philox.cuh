@@ -13,31 +13,72 @@ __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k)
 {
 #pragma unroll
     for (int r = 0; r < 10; ++r) {
-        const uint32_t lo0 = 0xD2511F53u * c.x, hi0 = __umulhi(0xD2511F53u, c.x);
-        const uint32_t lo1 = 0xCD9E8D57u * c.z, hi1 = __umulhi(0xCD9E8D57u, c.z);
-        c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+        const uint64_t p0 = (uint64_t)0xD2511F53u * c.x;   // one IMAD.WIDE.U32 each
+        const uint64_t p1 = (uint64_t)0xCD9E8D57u * c.z;
+        c = make_uint4((uint32_t)(p1 >> 32) ^ c.y ^ k.x, (uint32_t)p1, (uint32_t)(p0 >> 32) ^ c.w ^ k.y, (uint32_t)p0);
         k.x += 0x9E3779B9u;
         k.y += 0xBB67AE85u;
     }
     return c;
 }
 
-// Logistic(0,1) draw ell = ln u - ln(1 - u) = g_1 - g_0 (Eq.3) from the top
-// 23 bits k of a word: u = (2k+1) 2^-24 and 1 - u = (2^24 - 1 - 2k) 2^-24 are exact in
-// binary32. lg2.approx has absolute error <= 2^-22.6 for arguments in [0.5, 2] and
-// relative error 2^-22 elsewhere, so |d ell| <~ 2.3e-7 + 2.4e-7 |ell|.
-__device__ __forceinline__ float logistic_from_word(uint32_t w)
+// Same generator with the 10 round keys precomputed on the host (key + r * W for
+// r = 0..9) and passed as kernel parameters: each round is then two IMAD.WIDE and two
+// LOP3 whose key operand comes straight from the constant bank.
+struct PhiloxKeys {
+    uint32_t k0[10];
+    uint32_t k1[10];
+};
+
+inline PhiloxKeys philox_round_keys(uint64_t seed)
 {
-    const uint32_t k2 = (w >> 9) << 1;
-    const float u = __uint2float_rn(k2 + 1u) * 5.9604644775390625e-8f;       // (2k+1) 2^-24
-    const float ub = __uint2float_rn(16777215u - k2) * 5.9604644775390625e-8f; // 1 - u, exact
-    return (__log2f(u) - __log2f(ub)) * 0.69314718055994531f;
+    PhiloxKeys pk;
+    uint32_t a = (uint32_t)seed, b = (uint32_t)(seed >> 32);
+    for (int r = 0; r < 10; ++r) {
+        pk.k0[r] = a;
+        pk.k1[r] = b;
+        a += 0x9E3779B9u;
+        b += 0xBB67AE85u;
+    }
+    return pk;
 }
 
-// Same draw in fp64 (init path only).
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, const PhiloxKeys &pk)
+{
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const uint64_t p0 = (uint64_t)0xD2511F53u * c.x;
+        const uint64_t p1 = (uint64_t)0xCD9E8D57u * c.z;
+        c = make_uint4((uint32_t)(p1 >> 32) ^ c.y ^ pk.k0[r], (uint32_t)p1, (uint32_t)(p0 >> 32) ^ c.w ^ pk.k1[r],
+                       (uint32_t)p0);
+    }
+    return c;
+}
+
+// Open-interval uniform pair (u, 1 - u) from the low 23 bits k of a word (reading R2):
+// f = 1 + k 2^-23 is built by OR-ing k into the mantissa of 1.0f, and
+// u = f - (1 - 2^-24) = (2k+1) 2^-24, 1 - u = (2^24 - 1 - 2k) 2^-24 are both exact in
+// binary32 (24 significant bits; Sterbenz), so the pair costs one LOP3 and two FADDs.
+__device__ __forceinline__ float2 unif_pair(uint32_t w)
+{
+    const float f = __uint_as_float(0x3F800000u | (w & 0x7FFFFFu));
+    const float u = f - 0.999999940395355224609375f;
+    return make_float2(u, 1.0f - u);
+}
+
+// Logistic(0,1) draw ell = ln u - ln(1 - u) = g_1 - g_0 (Eq.3).
+// lg2.approx has absolute error <= 2^-22.6 for arguments in [0.5, 2] and relative error
+// 2^-22 elsewhere, so |d ell| <~ 2.3e-7 + 2.4e-7 |ell|.
+__device__ __forceinline__ float logistic_from_word(uint32_t w)
+{
+    const float2 uu = unif_pair(w);
+    return (__log2f(uu.x) - __log2f(uu.y)) * 0.69314718055994531f;
+}
+
+// Same uniform in fp64 (init path only).
 __device__ __forceinline__ double uniform_f64(uint32_t w)
 {
-    return (double)(((w >> 9) << 1) | 1u) * (1.0 / 16777216.0);  // (2k+1) 2^-24
+    return (double)(((w & 0x7FFFFFu) << 1) | 1u) * (1.0 / 16777216.0);  // (2k+1) 2^-24
 }
 
 }  // namespace galois

@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(256) k_update_soft(DevCnf c, StepParams p, flo
             if (p.optimizer == 0) {
                 mm = p.beta1 * mm + p.omb1 * g1;
                 w2 = p.beta2 * w2 + p.omb2 * g1 * g1;
-                zz = zz - 2.0f * ac.x * __fdividef(mm, sqrtf(w2) * ac.y + p.eps);
+                zz = zz - ac.x * __fdividef(mm, sqrtf(w2) * ac.y + p.eps);   // ac.x = 2 lr / bc1
             } else {
                 zz = zz - 2.0f * p.lr * g1;
             }

@@ -46,10 +46,10 @@ def test_philox_known_answers():
 
 
 def test_uniform_is_open_and_complement_exact():
-    """u = (k + 1/2) 2^-23 from the top 23 bits; u + (1-u) == 1 exactly (reading R2)."""
-    for w in [0, 1, 511, 512, 0x7FFFFFFF, 0x80000000, 0xFFFFFE00, 0xFFFFFFFF, 0x12345678]:
+    """u = (k + 1/2) 2^-23 from the low 23 bits; u + (1-u) == 1 exactly (reading R2)."""
+    for w in [0, 1, 511, 512, 0x7FFFFF, 0x800000, 0x7FFFFFFF, 0x80000000, 0xFFFFFE00, 0xFFFFFFFF, 0x12345678]:
         u, ub = O.uniform(w), O.uniform_complement(w)
-        k = w >> 9
+        k = w & 0x7FFFFF
         assert u == (k + 0.5) / 2 ** 23
         assert u + ub == 1.0
         assert 0.0 < u < 1.0 and 0.0 < ub < 1.0
@@ -75,7 +75,7 @@ def test_logistic_noise_closed_form():
     """ell(k) = ln((2k+1) / (2^24 - 2k - 1)) for the 23-bit k of the selected word."""
     seed, v, b, t = 12345, 3, 9, 5
     w = O.philox4x32_10([v, b >> 2, t, 1], [seed & 0xFFFFFFFF, seed >> 32])
-    k = int(w[b & 3]) >> 9
+    k = int(w[b & 3]) & 0x7FFFFF
     expect = math.log((2 * k + 1) / (2 ** 24 - 2 * k - 1))
     assert abs(O.lib().oracle_logistic_noise(v, b, t, seed) - expect) < 1e-12
 
