@@ -1,0 +1,95 @@
+// device_utils.cuh — small device helpers shared by the CUDA sources of libgalois.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "galois_internal.h"
+
+namespace galois {
+
+__device__ __forceinline__ uint32_t group8_mask(int lane) { return 0xFFu << (lane & 24); }
+
+// OR the 4-bit nibbles of the 8 lanes that share one 32-bit word of packed bits.
+__device__ __forceinline__ uint32_t gather_word(uint32_t nib, int lane)
+{
+    const uint32_t mask = group8_mask(lane);
+    uint32_t w = nib << (4 * (lane & 7));
+    w |= __shfl_xor_sync(mask, w, 1);
+    w |= __shfl_xor_sync(mask, w, 2);
+    w |= __shfl_xor_sync(mask, w, 4);
+    return w;
+}
+
+// 4 bits -> four 8-bit counters (bit i -> byte i).
+__device__ __forceinline__ uint32_t spread4(uint32_t nib) { return (nib * 0x00204081u) & 0x01010101u; }
+
+__device__ __forceinline__ int pinned_bit(const StepParams &p, int32_t v, int64_t b_global)
+{
+    if (p.pin_rank == nullptr) return -1;
+    const int r = p.pin_rank[v];
+    return r < 0 ? -1 : (int)((b_global >> r) & 1);
+}
+
+__device__ __forceinline__ float exp_neg_abs(float z)            // exp(-|z|), one MUFU.EX2
+{
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(-1.4426950408889634f * fabsf(z)));
+    return y;
+}
+
+__device__ __forceinline__ float sqrt_approx(float x)            // MUFU.SQRT, rel err ~2^-23
+{
+    float y;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// --------------------------------------------------------------- mbarrier + TMA bulk copy
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void fence_mbar_init()
+{
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase)
+{
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+
+// 1-D TMA bulk copy global -> shared (cp.async.bulk; SASS UBLKCP), completion counted in
+// bytes on the mbarrier. dst/src 16-B aligned, bytes a multiple of 16.
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar)
+{
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// Order this thread's earlier generic-proxy smem accesses before later async-proxy ones.
+__device__ __forceinline__ void fence_proxy_async_smem()
+{
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+}  // namespace galois

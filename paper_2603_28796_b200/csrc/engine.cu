@@ -584,7 +584,9 @@ static int prepare(galois_engine *e)
     e->b0 = per * e->rank;
     const int64_t left = e->B - e->b0;
     e->b_loc = (int32_t)std::max<int64_t>(0, std::min<int64_t>(per, left));
-    e->b_pad = std::max<int32_t>(32, (e->b_loc + 31) / 32 * 32);
+    // pad to 32 members (one bit word) up to 1024, then to whole 1024-member chunks, so that
+    // W <= 32 or W % 32 == 0 (chunk-major E, TMA-staged update)
+    e->b_pad = e->b_loc <= 1024 ? std::max<int32_t>(32, (e->b_loc + 31) / 32 * 32) : (e->b_loc + 1023) / 1024 * 1024;
     e->W = e->b_pad / 32;
     if ((uint64_t)n * (uint64_t)e->b_pad / 4 >= (1ull << 40))
         return poison(e, GALOIS_E_ARG, "n * local batch too large");

@@ -20,37 +20,11 @@
 
 #include <cstdint>
 
+#include "device_utils.cuh"
 #include "galois_internal.h"
 #include "philox.cuh"
 
 namespace galois {
-
-namespace {
-
-__device__ __forceinline__ uint32_t group8_mask(int lane) { return 0xFFu << (lane & 24); }
-
-// OR the 4-bit nibbles of the 8 lanes that share one 32-bit word.
-__device__ __forceinline__ uint32_t gather_word(uint32_t nib, int lane)
-{
-    const uint32_t mask = group8_mask(lane);
-    uint32_t w = nib << (4 * (lane & 7));
-    w |= __shfl_xor_sync(mask, w, 1);
-    w |= __shfl_xor_sync(mask, w, 2);
-    w |= __shfl_xor_sync(mask, w, 4);
-    return w;
-}
-
-// 4 bits -> four 8-bit counters (bit i -> byte i).
-__device__ __forceinline__ uint32_t spread4(uint32_t nib) { return (nib * 0x00204081u) & 0x01010101u; }
-
-__device__ __forceinline__ int pinned_bit(const StepParams &p, int32_t v, int64_t b_global)
-{
-    if (p.pin_rank == nullptr) return -1;
-    const int r = p.pin_rank[v];
-    return r < 0 ? -1 : (int)((b_global >> r) & 1);
-}
-
-}  // namespace
 
 // --------------------------------------------------------------------------- a3: init
 __global__ void __launch_bounds__(256) k_init(StepParams p, float4 *__restrict__ z4, float4 *__restrict__ m4,
@@ -187,17 +161,18 @@ __global__ void __launch_bounds__(256) k_clauses_st(DevCnf c, int32_t W, int32_t
         }
         if (kForward) {
             // E_i = prod_{j != i} (1 - s_j): all other literals false <=> none true, or
-            // exactly one true and it is i.
+            // exactly one true and it is i. Chunk-major layout E[chunk][csc position][LW].
+            uint32_t *Ec = E + (size_t)blockIdx.y * c.L * LW + wl;
 #pragma unroll
             for (int i = 0; i < 8; ++i)
                 if (i < width) {
                     const int2 si = c.slot_info[lo + i];
-                    E[(size_t)si.y * W + word] = ~any | (S[i] & ~two);
+                    Ec[(size_t)si.y * LW] = ~any | (S[i] & ~two);
                 }
             for (int i = 8; i < width; ++i) {
                 const int2 si = c.slot_info[lo + i];
                 const uint32_t s = bits[(size_t)(si.x >> 1) * W + word] ^ (0u - (uint32_t)(si.x & 1));
-                E[(size_t)si.y * W + word] = ~any | (s & ~two);
+                Ec[(size_t)si.y * LW] = ~any | (s & ~two);
             }
         }
         uint32_t U = ~any;                  // U = prod_i (1 - s_i): clause unsatisfied
@@ -213,225 +188,6 @@ __global__ void __launch_bounds__(256) k_clauses_st(DevCnf c, int32_t W, int32_t
         const int32_t v = s_cnt[i];
         if (v != 0 && base + i < b_pad) atomicAdd(&cnt[base + i], v);
     }
-}
-
-// ------------------------------------------------ per-variable kernels: shared pieces
-namespace {
-
-constexpr int kBatch = 8;   // independent E loads in flight per thread
-
-// Count the E bits of one quad (4 members: bits sh..sh+3 of word column `col`) over the
-// occurrences [k0, k1), into four counters. Loads are issued kBatch at a time
-// (predicated, independent) so one memory round trip covers a whole batch; four 8-bit
-// counters live in one register (spread4) and are flushed before they can overflow.
-__device__ __forceinline__ void count_bits(const uint32_t *__restrict__ col, int32_t W, int32_t k0, int32_t k1,
-                                           int sh, int32_t sign, int32_t G[4])
-{
-    const uint32_t *ptr = col + (size_t)k0 * W;
-    int32_t left = k1 - k0;
-    while (left > 0) {
-        int32_t blk = min(left, 248);              // 8-bit counters: <= 255 adds per flush
-        left -= blk;
-        uint32_t acc = 0;
-        for (; blk >= kBatch; blk -= kBatch) {     // full batches: no predication
-            uint32_t e[kBatch];
-#pragma unroll
-            for (int i = 0; i < kBatch; ++i) e[i] = __ldg(ptr + i * W);
-            ptr += kBatch * W;
-#pragma unroll
-            for (int i = 0; i < kBatch; ++i) acc += spread4((e[i] >> sh) & 15u);
-        }
-        if (blk > 0) {                             // remainder, predicated
-            uint32_t e[kBatch - 1];
-#pragma unroll
-            for (int i = 0; i < kBatch - 1; ++i) e[i] = i < blk ? __ldg(ptr + i * W) : 0u;
-            ptr += blk * W;
-#pragma unroll
-            for (int i = 0; i < kBatch - 1; ++i) acc += spread4((e[i] >> sh) & 15u);
-        }
-#pragma unroll
-        for (int j = 0; j < 4; ++j) G[j] += sign * (int32_t)((acc >> (8 * j)) & 255u);
-    }
-}
-
-struct ItemPos {
-    uint32_t row;    // variable (or hub chunk)
-    uint32_t q;      // quad within the row
-    bool valid;
-};
-
-__device__ __forceinline__ ItemPos item_pos(const RowMap &rm, uint32_t item, uint32_t r_t, uint32_t q_t)
-{
-    const uint32_t grp = (uint32_t)(((uint64_t)__umulhi(item, rm.div_mul) + item) >> rm.div_shift);
-    const uint32_t chunk = item - grp * rm.cpr;
-    ItemPos ip;
-    ip.row = grp * rm.R + r_t;
-    ip.q = chunk * 256u + q_t;
-    ip.valid = r_t < rm.R && ip.row < rm.rows && ip.q < rm.QW;
-    return ip;
-}
-
-// Helpers of the tau = 1 path: with (u, ub = 1 - u) from unif_pair and e = exp(-|z|),
-// sigma(z + logit(u)) sigma(-(z + logit(u))) = u ub e / (A + B e)^2 where
-// (A, B) = (u, ub) if z >= 0 else (ub, u); and [z + logit(u) >= 0] <=> A >= B e (z >= 0)
-// or B e >= A (z < 0). Exact rewrites of Eq.3 at tau = 1 with no logarithm.
-__device__ __forceinline__ bool sample_bit_tau1(float z, float2 uu, float e)
-{
-    return z >= 0.0f ? (uu.x >= uu.y * e) : (uu.x * e >= uu.y);
-}
-
-__device__ __forceinline__ float exp_neg_abs(float z)            // exp(-|z|), one MUFU.EX2
-{
-    float y;
-    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(-1.4426950408889634f * fabsf(z)));
-    return y;
-}
-
-__device__ __forceinline__ float sqrt_approx(float x)            // MUFU.SQRT, rel err ~2^-23
-{
-    float y;
-    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-    return y;
-}
-
-}  // namespace
-
-// --------------------------------------------------------------- a6: hub partial sums
-// Row = hub chunk of <= kHubChunk occurrences of one variable; per quad, the signed count
-// of E bits over the chunk (|value| <= 128 -> int16). Fixed chunk order = deterministic.
-__global__ void __launch_bounds__(256) k_hub_partial(DevCnf c, int32_t W, RowMap rm, const uint32_t *__restrict__ E,
-                                                     short4 *__restrict__ partial, const Ctrl *__restrict__ ctrl)
-{
-    if (ctrl->stopped) return;
-    const uint32_t r_t = rm.QW >= 256 ? 0u : threadIdx.x / rm.QW;
-    const uint32_t q_t = rm.QW >= 256 ? threadIdx.x : threadIdx.x - r_t * rm.QW;
-    for (uint32_t item = blockIdx.x; item < rm.items; item += gridDim.x) {
-        const ItemPos ip = item_pos(rm, item, r_t, q_t);
-        if (!ip.valid) continue;
-        const int2 info = c.hub_chunk[ip.row];                 // {variable, first CSC position}
-        const int32_t split = c.code_off[2 * info.x + 1], end = c.code_off[2 * info.x + 2];
-        const int32_t k1 = min(info.y + kHubChunk, end);
-        const uint32_t *col = E + (ip.q >> 3);
-        const int sh = 4 * (ip.q & 7);
-        int32_t G[4] = {0, 0, 0, 0};
-        count_bits(col, W, info.y, min(split, k1), sh, 1, G);
-        count_bits(col, W, max(split, info.y), k1, sh, -1, G);
-        partial[(size_t)ip.row * rm.QW + ip.q] = make_short4((short)G[0], (short)G[1], (short)G[2], (short)G[3]);
-    }
-}
-
-// ------------------------------------------------------------ a6 + a7: fused update
-// Per quad: G = sum over occurrences of sigma * E (CSC: positive codes, then negative),
-// g1 = -G p q / tau (straight-through), Adam on the reduced iterate
-// z = theta_1 - theta_0, rounding R_t = [z >= 0], next sample X_{t+1}.
-template <bool kDebug, bool kTau1, bool kAdam, bool kPins>
-__global__ void __launch_bounds__(256) k_update_st(DevCnf c, StepParams p, RowMap rm, float4 *__restrict__ z4,
-                                                   float4 *__restrict__ m4, float4 *__restrict__ v4,
-                                                   uint32_t *__restrict__ X, uint32_t *__restrict__ R,
-                                                   const uint32_t *__restrict__ E,
-                                                   const short4 *__restrict__ partial, Ctrl *__restrict__ ctrl,
-                                                   int4 *__restrict__ dbg_G, float4 *__restrict__ dbg_g1)
-{
-    if (ctrl->stopped) return;
-    const int32_t s = ctrl->t;                       // this step's index (t-1 -> t)
-    const float2 ac = p.adam_consts[s];              // {2 lr / bc1, 1 / sqrt(bc2)}
-    const int lane = threadIdx.x & 31;
-    const uint32_t r_t = rm.QW >= 256 ? 0u : threadIdx.x / rm.QW;
-    const uint32_t q_t = rm.QW >= 256 ? threadIdx.x : threadIdx.x - r_t * rm.QW;
-    bool bad = false;
-    for (uint32_t item = blockIdx.x; item < rm.items; item += gridDim.x) {
-        const ItemPos ip = item_pos(rm, item, r_t, q_t);
-        const int32_t v = (int32_t)ip.row;
-        const uint32_t q = ip.q;
-        uint32_t xn = 0, rn = 0;
-        if (ip.valid) {
-            const int64_t bq = p.b0 + 4 * (int64_t)q;
-            const size_t idx = (size_t)v * rm.QW + q;
-            const float4 z = z4[idx], m = m4[idx], vv = v4[idx];
-
-            // --- a6: signal G of the 4 members
-            int32_t G[4] = {0, 0, 0, 0};
-            const int32_t hub = c.num_hubs > 0 ? c.hub_of_var[v] : -1;
-            if (hub >= 0) {
-                const int32_t c0 = c.hub_chunk_off[hub], c1 = c.hub_chunk_off[hub + 1];
-                for (int32_t ch = c0; ch < c1; ++ch) {
-                    const short4 pp = partial[(size_t)ch * rm.QW + q];
-                    G[0] += pp.x; G[1] += pp.y; G[2] += pp.z; G[3] += pp.w;
-                }
-            } else {
-                const int32_t k0 = c.code_off[2 * v], k1 = c.code_off[2 * v + 1], k2 = c.code_off[2 * v + 2];
-                const uint32_t *col = E + (q >> 3);
-                const int sh = 4 * (q & 7);
-                count_bits(col, p.W, k0, k1, sh, 1, G);
-                count_bits(col, p.W, k1, k2, sh, -1, G);
-            }
-
-            // --- a7: straight-through gradient, optimiser, rounding, next sample
-            const uint4 wn4 = philox4x32_10(make_uint4((uint32_t)v, (uint32_t)(bq >> 2), (uint32_t)s, 1u), p.keys);
-            const uint4 wx4 = philox4x32_10(make_uint4((uint32_t)v, (uint32_t)(bq >> 2), (uint32_t)(s + 1), 1u), p.keys);
-            const uint32_t wn[4] = {wn4.x, wn4.y, wn4.z, wn4.w};
-            const uint32_t wx[4] = {wx4.x, wx4.y, wx4.z, wx4.w};
-            float zz[4] = {z.x, z.y, z.z, z.w}, mm[4] = {m.x, m.y, m.z, m.w}, ww[4] = {vv.x, vv.y, vv.z, vv.w};
-            float g1o[4];
-            const int pin_r = kPins ? (int)p.pin_rank[v] : -1;   // cube pin of this variable
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                float g1;
-                if (kTau1) {
-                    const float2 uu = unif_pair(wn[j]);
-                    const float e = exp_neg_abs(zz[j]);
-                    const bool pos = zz[j] >= 0.0f;
-                    const float d = pos ? fmaf(uu.y, e, uu.x) : fmaf(uu.x, e, uu.y);
-                    const float pq = __fdividef(uu.x * uu.y * e, d * d);   // sigma(a) sigma(-a)
-                    g1 = -(float)G[j] * pq;                // dL/dtheta_1 (straight-through), tau = 1
-                } else {
-                    const float a = (zz[j] + logistic_from_word(wn[j])) * p.inv_tau;
-                    const float e = exp_neg_abs(a);
-                    const float d = 1.0f + e;
-                    g1 = -(float)G[j] * __fdividef(e, d * d) * p.inv_tau;
-                }
-                if (kPins && pin_r >= 0) g1 = 0.0f;
-                float zn;
-                if (kAdam) {
-                    const float mn = fmaf(p.beta1, mm[j], p.omb1 * g1);
-                    const float wv = fmaf(p.beta2, ww[j], p.omb2 * g1 * g1);
-                    zn = zz[j] - ac.x * __fdividef(mn, fmaf(sqrt_approx(wv), ac.y, p.eps));
-                    if (!kPins || pin_r < 0) { mm[j] = mn; ww[j] = wv; }
-                } else {
-                    zn = zz[j] - 2.0f * p.lr * g1;
-                }
-                if (!kPins || pin_r < 0) zz[j] = zn;
-                bad |= !isfinite(zz[j]);
-                g1o[j] = g1;
-                uint32_t xb, rb;
-                if (kPins && pin_r >= 0) {
-                    xb = rb = (uint32_t)((bq + j) >> pin_r) & 1u;
-                } else {
-                    rb = zz[j] >= 0.0f ? 1u : 0u;
-                    if (kTau1)
-                        xb = sample_bit_tau1(zz[j], unif_pair(wx[j]), exp_neg_abs(zz[j])) ? 1u : 0u;
-                    else
-                        xb = zz[j] + logistic_from_word(wx[j]) >= 0.0f ? 1u : 0u;
-                }
-                rn |= rb << j;
-                xn |= xb << j;
-            }
-            z4[idx] = make_float4(zz[0], zz[1], zz[2], zz[3]);
-            m4[idx] = make_float4(mm[0], mm[1], mm[2], mm[3]);
-            v4[idx] = make_float4(ww[0], ww[1], ww[2], ww[3]);
-            if (kDebug) {
-                dbg_G[idx] = make_int4(G[0], G[1], G[2], G[3]);
-                dbg_g1[idx] = make_float4(g1o[0], g1o[1], g1o[2], g1o[3]);
-            }
-        }
-        // 8 lanes = one 32-bit word; validity is uniform within each group of 8 lanes
-        const uint32_t xw = gather_word(xn, lane), rw = gather_word(rn, lane);
-        if (ip.valid && (lane & 7) == 0) {
-            X[(size_t)v * p.W + (q >> 3)] = xw;
-            R[(size_t)v * p.W + (q >> 3)] = rw;
-        }
-    }
-    if (bad) atomicOr(&ctrl->nonfinite, 1);
 }
 
 // ------------------------------------------------------------------- a8/a9: best
@@ -537,67 +293,6 @@ void check(const DevCnf &c, int32_t W, int32_t b_pad, const uint32_t *R, int32_t
            cudaStream_t st)
 {
     k_clauses_st<false><<<clause_grid(c, W), 256, 0, st>>>(c, W, b_pad, R, nullptr, unsat, ctrl);
-}
-
-RowMap make_rowmap(uint32_t rows, uint32_t b_pad)
-{
-    RowMap rm;
-    rm.QW = b_pad / 4u;
-    rm.rows = rows;
-    if (rm.QW >= 256) {
-        rm.cpr = (rm.QW + 255u) / 256u;
-        rm.R = 1;
-    } else {
-        rm.cpr = 1;
-        rm.R = 256u / rm.QW;
-    }
-    rm.items = (rows + rm.R - 1) / rm.R * rm.cpr;
-    // q = (umulhi(x, mul) + x) >> shift == x / cpr for all 32-bit x (64-bit add)
-    uint32_t l = 0;
-    while ((1ull << l) < rm.cpr) ++l;
-    rm.div_shift = l;
-    rm.div_mul = (uint32_t)((((1ull << l) - rm.cpr) << 32) / rm.cpr + 1ull);
-    if (rm.cpr == 1) rm.div_mul = 0;
-    return rm;
-}
-
-static unsigned item_grid(const RowMap &rm, unsigned ctas_per_sm)
-{
-    unsigned g = 148u * ctas_per_sm;
-    if (rm.items < g) g = rm.items;
-    return g < 1 ? 1 : g;
-}
-
-void hub_partial(const DevCnf &c, int32_t W, int32_t b_pad, const uint32_t *E, short4 *partial,
-                 const Ctrl *ctrl, cudaStream_t st)
-{
-    if (c.num_hub_chunks == 0) return;
-    const RowMap rm = make_rowmap((uint32_t)c.num_hub_chunks, (uint32_t)b_pad);
-    k_hub_partial<<<item_grid(rm, 8), 256, 0, st>>>(c, W, rm, E, partial, ctrl);
-}
-
-void update_st(const DevCnf &c, const StepParams &p, float *z, float *m, float *v, uint32_t *X, uint32_t *R,
-               const uint32_t *E, const short4 *partial, Ctrl *ctrl, int32_t *dbg_G, float *dbg_g1,
-               cudaStream_t st)
-{
-    const RowMap rm = make_rowmap((uint32_t)p.n, (uint32_t)p.b_pad);
-    const unsigned grid = item_grid(rm, 8);
-    const int variant = (dbg_G ? 8 : 0) | (p.inv_tau == 1.0f ? 4 : 0) | (p.optimizer == 0 ? 2 : 0) |
-                        (p.pin_rank ? 1 : 0);
-    using K = void (*)(DevCnf, StepParams, RowMap, float4 *, float4 *, float4 *, uint32_t *, uint32_t *,
-                       const uint32_t *, const short4 *, Ctrl *, int4 *, float4 *);
-    static const K table[16] = {
-        k_update_st<false, false, false, false>, k_update_st<false, false, false, true>,
-        k_update_st<false, false, true, false>,  k_update_st<false, false, true, true>,
-        k_update_st<false, true, false, false>,  k_update_st<false, true, false, true>,
-        k_update_st<false, true, true, false>,   k_update_st<false, true, true, true>,
-        k_update_st<true, false, false, false>,  k_update_st<true, false, false, true>,
-        k_update_st<true, false, true, false>,   k_update_st<true, false, true, true>,
-        k_update_st<true, true, false, false>,   k_update_st<true, true, false, true>,
-        k_update_st<true, true, true, false>,    k_update_st<true, true, true, true>,
-    };
-    table[variant]<<<grid, 256, 0, st>>>(c, p, rm, (float4 *)z, (float4 *)m, (float4 *)v, X, R, E, partial, ctrl,
-                                          (int4 *)dbg_G, (float4 *)dbg_g1);
 }
 
 void best(const int32_t *unsat, int32_t b_loc, int64_t b0, Ctrl *ctrl, bool finalize, cudaStream_t st)

@@ -1,0 +1,461 @@
+// update_kernels.cu — rows a6 + a7 of SURVEY §8: the fused backward + update.
+//
+// For every variable v and member b (one thread per QUAD of 4 members):
+//   a6  G_v,b = sum over the occurrences of v of sigma * E   (segmented, CSC order:
+//       positive codes, then negative; integer, no atomics -> deterministic)
+//   a7  g1 = -G p q / tau (straight-through, Eq.4 text P:160; p q = sigma(a) sigma(-a)),
+//       Adam (App. A) on the reduced iterate z = theta_1 - theta_0, rounding
+//       R_t = [z >= 0], next sample X_{t+1} = [z + ell_{t+1} >= 0] (Eq.3-4).
+// E layout: chunk-major E[chunk][csc position][CW], CW = min(W, 32) words, so the
+// occurrences of one variable within one 1024-member chunk are ONE contiguous block of
+// deg * 128 B — one TMA bulk copy (k_update_tma). Hub variables (degree > kHubDegree)
+// are first reduced in fixed-size chunks by k_hub_partial (deterministic int16 partials).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "device_utils.cuh"
+#include "galois_internal.h"
+#include "philox.cuh"
+
+namespace galois {
+
+namespace {
+
+constexpr int kBatch = 8;             // independent E loads in flight per thread (global path)
+constexpr int kStages = 3;            // TMA pipeline depth
+constexpr int kStageRows = 64;        // E rows staged per item (variables with degree <= 64)
+constexpr int kStageE = kStageRows * 128;
+constexpr int kStageBytes = kStageE + 3 * 4096;   // E rows + z, m, v of 256 quads
+constexpr int kTmaSmem = kStages * kStageBytes;
+
+// Count the E bits of one quad (bits sh..sh+3 of column `col`, row stride CW words) over
+// occurrences [k0, k1): kBatch independent predicated loads per round trip; four 8-bit
+// counters in one register (spread4), flushed before they can overflow.
+__device__ __forceinline__ void count_bits(const uint32_t *__restrict__ col, int32_t CW, int32_t k0, int32_t k1,
+                                           int sh, int32_t sign, int32_t G[4])
+{
+    const uint32_t *ptr = col + (size_t)k0 * CW;
+    int32_t left = k1 - k0;
+    while (left > 0) {
+        int32_t blk = min(left, 248);
+        left -= blk;
+        uint32_t acc = 0;
+        for (; blk >= kBatch; blk -= kBatch) {
+            uint32_t e[kBatch];
+#pragma unroll
+            for (int i = 0; i < kBatch; ++i) e[i] = __ldg(ptr + i * CW);
+            ptr += kBatch * CW;
+#pragma unroll
+            for (int i = 0; i < kBatch; ++i) acc += spread4((e[i] >> sh) & 15u);
+        }
+        if (blk > 0) {
+            uint32_t e[kBatch - 1];
+#pragma unroll
+            for (int i = 0; i < kBatch - 1; ++i) e[i] = i < blk ? __ldg(ptr + i * CW) : 0u;
+            ptr += blk * CW;
+#pragma unroll
+            for (int i = 0; i < kBatch - 1; ++i) acc += spread4((e[i] >> sh) & 15u);
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) G[j] += sign * (int32_t)((acc >> (8 * j)) & 255u);
+    }
+}
+
+// Same count over rows staged in shared memory (row = 32 words = 128 B).
+__device__ __forceinline__ void count_bits_smem(const uint32_t *srow, int32_t n, int sh, int32_t sign, int32_t G[4])
+{
+    uint32_t acc = 0;                     // n <= kStageRows < 256: no overflow
+#pragma unroll 8
+    for (int32_t k = 0; k < n; ++k) acc += spread4((srow[k * 32] >> sh) & 15u);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) G[j] += sign * (int32_t)((acc >> (8 * j)) & 255u);
+}
+
+struct ItemPos {
+    uint32_t row;    // variable (or hub chunk)
+    uint32_t q;      // quad within the row
+    bool valid;
+};
+
+__device__ __forceinline__ uint32_t div_cpr(const RowMap &rm, uint32_t x)
+{
+    return (uint32_t)(((uint64_t)__umulhi(x, rm.div_mul) + x) >> rm.div_shift);
+}
+
+__device__ __forceinline__ ItemPos item_pos(const RowMap &rm, uint32_t item, uint32_t r_t, uint32_t q_t)
+{
+    const uint32_t grp = div_cpr(rm, item);
+    const uint32_t chunk = item - grp * rm.cpr;
+    ItemPos ip;
+    ip.row = grp * rm.R + r_t;
+    ip.q = chunk * 256u + q_t;
+    ip.valid = r_t < rm.R && ip.row < rm.rows && ip.q < rm.QW;
+    return ip;
+}
+
+// Column of quad q in the chunk-major E: chunk q/256 (when CW = 32), word (q/8) mod CW.
+__device__ __forceinline__ const uint32_t *e_column(const uint32_t *E, int32_t L, int32_t CW, uint32_t q)
+{
+    const uint32_t w = q >> 3;
+    const uint32_t ch = w / (uint32_t)CW, wi = w - ch * (uint32_t)CW;
+    return E + (size_t)ch * L * CW + wi;
+}
+
+// tau = 1 rewrites of Eq.3 with no logarithm: with (u, ub = 1 - u) and e = exp(-|z|),
+// sigma(z + logit u) sigma(-(z + logit u)) = u ub e / d^2 with d = u + ub e (z >= 0) or
+// ub + u e (z < 0); and [z + logit u >= 0] <=> u >= ub e (z >= 0) or u e >= ub (z < 0).
+__device__ __forceinline__ bool sample_bit_tau1(float z, float2 uu, float e)
+{
+    return z >= 0.0f ? (uu.x >= uu.y * e) : (uu.x * e >= uu.y);
+}
+
+// a7 for one quad: gradient, optimiser, rounding, next sample. Returns the nibbles.
+template <bool kTau1, bool kAdam, bool kPins>
+__device__ __forceinline__ void quad_update(const StepParams &p, float2 ac, int32_t v, int64_t bq, int32_t s,
+                                            const int32_t G[4], float4 &z, float4 &m, float4 &vv, uint32_t &xn,
+                                            uint32_t &rn, float g1o[4], bool &bad)
+{
+    const uint4 wn4 = philox4x32_10(make_uint4((uint32_t)v, (uint32_t)(bq >> 2), (uint32_t)s, 1u), p.keys);
+    const uint4 wx4 = philox4x32_10(make_uint4((uint32_t)v, (uint32_t)(bq >> 2), (uint32_t)(s + 1), 1u), p.keys);
+    const uint32_t wn[4] = {wn4.x, wn4.y, wn4.z, wn4.w};
+    const uint32_t wx[4] = {wx4.x, wx4.y, wx4.z, wx4.w};
+    float zz[4] = {z.x, z.y, z.z, z.w}, mm[4] = {m.x, m.y, m.z, m.w}, ww[4] = {vv.x, vv.y, vv.z, vv.w};
+    const int pin_r = kPins ? (int)p.pin_rank[v] : -1;       // cube pin of this variable
+    xn = rn = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        float g1;
+        if (kTau1) {
+            const float2 uu = unif_pair(wn[j]);
+            const float e = exp_neg_abs(zz[j]);
+            const float d = zz[j] >= 0.0f ? fmaf(uu.y, e, uu.x) : fmaf(uu.x, e, uu.y);
+            g1 = -(float)G[j] * __fdividef(uu.x * uu.y * e, d * d);   // -G sigma(a) sigma(-a)
+        } else {
+            const float a = (zz[j] + logistic_from_word(wn[j])) * p.inv_tau;
+            const float e = exp_neg_abs(a);
+            const float d = 1.0f + e;
+            g1 = -(float)G[j] * __fdividef(e, d * d) * p.inv_tau;
+        }
+        if (kPins && pin_r >= 0) g1 = 0.0f;
+        float zn;
+        if (kAdam) {
+            const float mn = fmaf(p.beta1, mm[j], p.omb1 * g1);
+            const float wv = fmaf(p.beta2, ww[j], p.omb2 * g1 * g1);
+            zn = zz[j] - ac.x * __fdividef(mn, fmaf(sqrt_approx(wv), ac.y, p.eps));
+            if (!kPins || pin_r < 0) { mm[j] = mn; ww[j] = wv; }
+        } else {
+            zn = zz[j] - 2.0f * p.lr * g1;
+        }
+        if (!kPins || pin_r < 0) zz[j] = zn;
+        bad |= !isfinite(zz[j]);
+        g1o[j] = g1;
+        uint32_t xb, rb;
+        if (kPins && pin_r >= 0) {
+            xb = rb = (uint32_t)((bq + j) >> pin_r) & 1u;
+        } else {
+            rb = zz[j] >= 0.0f ? 1u : 0u;
+            if (kTau1)
+                xb = sample_bit_tau1(zz[j], unif_pair(wx[j]), exp_neg_abs(zz[j])) ? 1u : 0u;
+            else
+                xb = zz[j] + logistic_from_word(wx[j]) >= 0.0f ? 1u : 0u;
+        }
+        rn |= rb << j;
+        xn |= xb << j;
+    }
+    z = make_float4(zz[0], zz[1], zz[2], zz[3]);
+    m = make_float4(mm[0], mm[1], mm[2], mm[3]);
+    vv = make_float4(ww[0], ww[1], ww[2], ww[3]);
+}
+
+__device__ __forceinline__ void hub_signal(const DevCnf &c, const short4 *__restrict__ partial, uint32_t QW,
+                                           int32_t hub, uint32_t q, int32_t G[4])
+{
+    const int32_t c0 = c.hub_chunk_off[hub], c1 = c.hub_chunk_off[hub + 1];
+    for (int32_t ch = c0; ch < c1; ++ch) {
+        const short4 pp = partial[(size_t)ch * QW + q];
+        G[0] += pp.x; G[1] += pp.y; G[2] += pp.z; G[3] += pp.w;
+    }
+}
+
+}  // namespace
+
+// --------------------------------------------------------------- a6: hub partial sums
+// Row = hub chunk of <= kHubChunk occurrences of one variable; per quad, the signed count
+// of E bits over the chunk (|value| <= 128 -> int16). Fixed chunk order = deterministic.
+__global__ void __launch_bounds__(256) k_hub_partial(DevCnf c, int32_t CW, RowMap rm, const uint32_t *__restrict__ E,
+                                                     short4 *__restrict__ partial, const Ctrl *__restrict__ ctrl)
+{
+    if (ctrl->stopped) return;
+    const uint32_t r_t = rm.QW >= 256 ? 0u : threadIdx.x / rm.QW;
+    const uint32_t q_t = rm.QW >= 256 ? threadIdx.x : threadIdx.x - r_t * rm.QW;
+    for (uint32_t item = blockIdx.x; item < rm.items; item += gridDim.x) {
+        const ItemPos ip = item_pos(rm, item, r_t, q_t);
+        if (!ip.valid) continue;
+        const int2 info = c.hub_chunk[ip.row];                 // {variable, first CSC position}
+        const int32_t split = c.code_off[2 * info.x + 1], end = c.code_off[2 * info.x + 2];
+        const int32_t k1 = min(info.y + kHubChunk, end);
+        const uint32_t *col = e_column(E, c.L, CW, ip.q);
+        const int sh = 4 * (ip.q & 7);
+        int32_t G[4] = {0, 0, 0, 0};
+        count_bits(col, CW, info.y, min(split, k1), sh, 1, G);
+        count_bits(col, CW, max(split, info.y), k1, sh, -1, G);
+        partial[(size_t)ip.row * rm.QW + ip.q] = make_short4((short)G[0], (short)G[1], (short)G[2], (short)G[3]);
+    }
+}
+
+// ------------------------------------------------- a6 + a7: fused update, generic layout
+template <bool kDebug, bool kTau1, bool kAdam, bool kPins>
+__global__ void __launch_bounds__(256) k_update_st(DevCnf c, StepParams p, RowMap rm, float4 *__restrict__ z4,
+                                                   float4 *__restrict__ m4, float4 *__restrict__ v4,
+                                                   uint32_t *__restrict__ X, uint32_t *__restrict__ R,
+                                                   const uint32_t *__restrict__ E,
+                                                   const short4 *__restrict__ partial, Ctrl *__restrict__ ctrl,
+                                                   int4 *__restrict__ dbg_G, float4 *__restrict__ dbg_g1)
+{
+    if (ctrl->stopped) return;
+    const int32_t s = ctrl->t;                       // this step's index (t-1 -> t)
+    const float2 ac = p.adam_consts[s];              // {2 lr / bc1, 1 / sqrt(bc2)}
+    const int lane = threadIdx.x & 31;
+    const int32_t CW = p.W < 32 ? p.W : 32;
+    const uint32_t r_t = rm.QW >= 256 ? 0u : threadIdx.x / rm.QW;
+    const uint32_t q_t = rm.QW >= 256 ? threadIdx.x : threadIdx.x - r_t * rm.QW;
+    bool bad = false;
+    for (uint32_t item = blockIdx.x; item < rm.items; item += gridDim.x) {
+        const ItemPos ip = item_pos(rm, item, r_t, q_t);
+        const int32_t v = (int32_t)ip.row;
+        const uint32_t q = ip.q;
+        uint32_t xn = 0, rn = 0;
+        if (ip.valid) {
+            const int64_t bq = p.b0 + 4 * (int64_t)q;
+            const size_t idx = (size_t)v * rm.QW + q;
+            float4 z = z4[idx], m = m4[idx], vv = v4[idx];
+            int32_t G[4] = {0, 0, 0, 0};
+            const int32_t hub = c.num_hubs > 0 ? c.hub_of_var[v] : -1;
+            if (hub >= 0) {
+                hub_signal(c, partial, rm.QW, hub, q, G);
+            } else {
+                const int32_t k0 = c.code_off[2 * v], k1 = c.code_off[2 * v + 1], k2 = c.code_off[2 * v + 2];
+                const uint32_t *col = e_column(E, c.L, CW, q);
+                const int sh = 4 * (q & 7);
+                count_bits(col, CW, k0, k1, sh, 1, G);
+                count_bits(col, CW, k1, k2, sh, -1, G);
+            }
+            float g1o[4];
+            quad_update<kTau1, kAdam, kPins>(p, ac, v, bq, s, G, z, m, vv, xn, rn, g1o, bad);
+            z4[idx] = z;
+            m4[idx] = m;
+            v4[idx] = vv;
+            if (kDebug) {
+                dbg_G[idx] = make_int4(G[0], G[1], G[2], G[3]);
+                dbg_g1[idx] = make_float4(g1o[0], g1o[1], g1o[2], g1o[3]);
+            }
+        }
+        // 8 lanes = one 32-bit word; validity is uniform within each group of 8 lanes
+        const uint32_t xw = gather_word(xn, lane), rw = gather_word(rn, lane);
+        if (ip.valid && (lane & 7) == 0) {
+            X[(size_t)v * p.W + (q >> 3)] = xw;
+            R[(size_t)v * p.W + (q >> 3)] = rw;
+        }
+    }
+    if (bad) atomicOr(&ctrl->nonfinite, 1);
+}
+
+// -------------------------------- a6 + a7: fused update, TMA-pipelined (W % 32 == 0)
+// Persistent CTAs; item = (variable, 1024-member chunk), one quad per thread. Thread 0 is
+// the producer: kStages items ahead it issues 1-D TMA bulk copies (cp.async.bulk) of the
+// item's z, m, v rows (3 x 4 KB) and, for variables of degree <= kStageRows, of its
+// contiguous E block (deg x 128 B) into a shared-memory stage, completing on an mbarrier.
+// The memory system sees several items in flight per CTA with no register cost.
+template <bool kDebug, bool kTau1, bool kAdam, bool kPins>
+__global__ void __launch_bounds__(256) k_update_tma(DevCnf c, StepParams p, RowMap rm, float4 *__restrict__ z4,
+                                                    float4 *__restrict__ m4, float4 *__restrict__ v4,
+                                                    uint32_t *__restrict__ X, uint32_t *__restrict__ R,
+                                                    const uint32_t *__restrict__ E,
+                                                    const short4 *__restrict__ partial, Ctrl *__restrict__ ctrl,
+                                                    int4 *__restrict__ dbg_G, float4 *__restrict__ dbg_g1)
+{
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ uint64_t full[kStages];
+    __shared__ int4 hdr[kStages];          // {v, k0, k1, k2}
+    __shared__ int32_t hmode[kStages];     // 1 = E staged, 2 = hub, 0 = E from global
+    if (ctrl->stopped) return;
+    const int32_t s = ctrl->t;
+    const float2 ac = p.adam_consts[s];
+    const int tid = threadIdx.x, lane = tid & 31;
+    const uint32_t QW = rm.QW;
+
+    if (tid == 0) {
+        for (int i = 0; i < kStages; ++i) mbar_init(&full[i], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    auto issue = [&](uint32_t j) {         // producer (thread 0): item j of this CTA
+        const uint32_t item = blockIdx.x + j * gridDim.x;
+        if (item >= rm.items) return;
+        const int st = (int)(j % kStages);
+        const uint32_t v = div_cpr(rm, item), ch = item - v * rm.cpr;
+        const int32_t k0 = c.code_off[2 * v], k1 = c.code_off[2 * v + 1], k2 = c.code_off[2 * v + 2];
+        const int32_t hub = c.num_hubs > 0 ? c.hub_of_var[v] : -1;
+        const bool staged = hub < 0 && (k2 - k0) <= kStageRows;
+        hdr[st] = make_int4((int32_t)v, k0, k1, k2);
+        hmode[st] = hub >= 0 ? 2 : (staged ? 1 : 0);
+        uint8_t *sb = smem + st * kStageBytes;
+        const uint32_t ebytes = staged ? (uint32_t)(k2 - k0) * 128u : 0u;
+        mbar_arrive_expect_tx(&full[st], 3u * 4096u + ebytes);
+        const size_t off = (size_t)v * QW + (size_t)ch * 256u;
+        bulk_g2s(sb + kStageE, z4 + off, 4096u, &full[st]);
+        bulk_g2s(sb + kStageE + 4096, m4 + off, 4096u, &full[st]);
+        bulk_g2s(sb + kStageE + 8192, v4 + off, 4096u, &full[st]);
+        if (ebytes) bulk_g2s(sb, E + ((size_t)ch * c.L + k0) * 32u, ebytes, &full[st]);
+    };
+    if (tid == 0)
+        for (uint32_t j = 0; j < (uint32_t)kStages; ++j) issue(j);
+
+    bool bad = false;
+    for (uint32_t j = 0;; ++j) {
+        const uint32_t item = blockIdx.x + j * gridDim.x;
+        if (item >= rm.items) break;
+        const int st = (int)(j % kStages);
+        mbar_wait(&full[st], (j / kStages) & 1u);
+        const int4 h = hdr[st];
+        const int mode = hmode[st];
+        const int32_t v = h.x;
+        const uint32_t ch = item - (uint32_t)v * rm.cpr;
+        const uint32_t q = ch * 256u + (uint32_t)tid;
+        const uint8_t *sb = smem + st * kStageBytes;
+        float4 z = reinterpret_cast<const float4 *>(sb + kStageE)[tid];
+        float4 m = reinterpret_cast<const float4 *>(sb + kStageE + 4096)[tid];
+        float4 vv = reinterpret_cast<const float4 *>(sb + kStageE + 8192)[tid];
+        const int sh = 4 * (tid & 7);
+        int32_t G[4] = {0, 0, 0, 0};
+        if (mode == 1) {
+            const uint32_t *srow = reinterpret_cast<const uint32_t *>(sb) + (tid >> 3);
+            count_bits_smem(srow, h.z - h.y, sh, 1, G);
+            count_bits_smem(srow + (h.z - h.y) * 32, h.w - h.z, sh, -1, G);
+        } else if (mode == 2) {
+            hub_signal(c, partial, QW, c.hub_of_var[v], q, G);
+        } else {
+            const uint32_t *col = E + (size_t)ch * c.L * 32u + (tid >> 3);
+            count_bits(col, 32, h.y, h.z, sh, 1, G);
+            count_bits(col, 32, h.z, h.w, sh, -1, G);
+        }
+        const int64_t bq = p.b0 + 4 * (int64_t)q;
+        uint32_t xn, rn;
+        float g1o[4];
+        quad_update<kTau1, kAdam, kPins>(p, ac, v, bq, s, G, z, m, vv, xn, rn, g1o, bad);
+        const size_t idx = (size_t)v * QW + q;
+        z4[idx] = z;
+        m4[idx] = m;
+        v4[idx] = vv;
+        if (kDebug) {
+            dbg_G[idx] = make_int4(G[0], G[1], G[2], G[3]);
+            dbg_g1[idx] = make_float4(g1o[0], g1o[1], g1o[2], g1o[3]);
+        }
+        const uint32_t xw = gather_word(xn, lane), rw = gather_word(rn, lane);
+        if ((lane & 7) == 0) {
+            X[(size_t)v * p.W + (q >> 3)] = xw;
+            R[(size_t)v * p.W + (q >> 3)] = rw;
+        }
+        __syncthreads();                   // every thread is done with stage st
+        if (tid == 0) {
+            fence_proxy_async_smem();      // generic reads of the stage before the TMA refill
+            issue(j + kStages);
+        }
+    }
+    if (bad) atomicOr(&ctrl->nonfinite, 1);
+}
+
+// ------------------------------------------------------------------ launch wrappers
+namespace launch {
+
+RowMap make_rowmap(uint32_t rows, uint32_t b_pad)
+{
+    RowMap rm;
+    rm.QW = b_pad / 4u;
+    rm.rows = rows;
+    if (rm.QW >= 256) {
+        rm.cpr = (rm.QW + 255u) / 256u;
+        rm.R = 1;
+    } else {
+        rm.cpr = 1;
+        rm.R = 256u / rm.QW;
+    }
+    rm.items = (rows + rm.R - 1) / rm.R * rm.cpr;
+    // x / cpr == (umulhi(x, mul) + x) >> shift for all 32-bit x (64-bit add)
+    uint32_t l = 0;
+    while ((1ull << l) < rm.cpr) ++l;
+    rm.div_shift = l;
+    rm.div_mul = rm.cpr == 1 ? 0u : (uint32_t)((((1ull << l) - rm.cpr) << 32) / rm.cpr + 1ull);
+    return rm;
+}
+
+static unsigned item_grid(const RowMap &rm, unsigned ctas_per_sm)
+{
+    unsigned g = 148u * ctas_per_sm;
+    if (rm.items < g) g = rm.items;
+    return g < 1 ? 1 : g;
+}
+
+void hub_partial(const DevCnf &c, int32_t W, int32_t b_pad, const uint32_t *E, short4 *partial,
+                 const Ctrl *ctrl, cudaStream_t st)
+{
+    if (c.num_hub_chunks == 0) return;
+    const RowMap rm = make_rowmap((uint32_t)c.num_hub_chunks, (uint32_t)b_pad);
+    k_hub_partial<<<item_grid(rm, 8), 256, 0, st>>>(c, W < 32 ? W : 32, rm, E, partial, ctrl);
+}
+
+using UpdKernel = void (*)(DevCnf, StepParams, RowMap, float4 *, float4 *, float4 *, uint32_t *, uint32_t *,
+                           const uint32_t *, const short4 *, Ctrl *, int4 *, float4 *);
+
+template <template <bool, bool, bool, bool> class Sel>
+static UpdKernel pick(int variant)
+{
+    static const UpdKernel table[16] = {
+        Sel<false, false, false, false>::k, Sel<false, false, false, true>::k, Sel<false, false, true, false>::k,
+        Sel<false, false, true, true>::k,   Sel<false, true, false, false>::k,  Sel<false, true, false, true>::k,
+        Sel<false, true, true, false>::k,   Sel<false, true, true, true>::k,    Sel<true, false, false, false>::k,
+        Sel<true, false, false, true>::k,   Sel<true, false, true, false>::k,   Sel<true, false, true, true>::k,
+        Sel<true, true, false, false>::k,   Sel<true, true, false, true>::k,    Sel<true, true, true, false>::k,
+        Sel<true, true, true, true>::k,
+    };
+    return table[variant];
+}
+
+template <bool a, bool b, bool c, bool d>
+struct SelGeneric {
+    static constexpr UpdKernel k = k_update_st<a, b, c, d>;
+};
+template <bool a, bool b, bool c, bool d>
+struct SelTma {
+    static constexpr UpdKernel k = k_update_tma<a, b, c, d>;
+};
+
+bool use_tma_update(int32_t W) { return W % 32 == 0; }
+
+void update_st(const DevCnf &c, const StepParams &p, float *z, float *m, float *v, uint32_t *X, uint32_t *R,
+               const uint32_t *E, const short4 *partial, Ctrl *ctrl, int32_t *dbg_G, float *dbg_g1,
+               cudaStream_t st)
+{
+    const RowMap rm = make_rowmap((uint32_t)p.n, (uint32_t)p.b_pad);
+    const int variant = (dbg_G ? 8 : 0) | (p.inv_tau == 1.0f ? 4 : 0) | (p.optimizer == 0 ? 2 : 0) |
+                        (p.pin_rank ? 1 : 0);
+    if (use_tma_update(p.W)) {
+        static bool configured[16] = {false};
+        const UpdKernel k = pick<SelTma>(variant);
+        if (!configured[variant]) {
+            cudaFuncSetAttribute((const void *)k, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
+            configured[variant] = true;
+        }
+        k<<<item_grid(rm, 3), 256, kTmaSmem, st>>>(c, p, rm, (float4 *)z, (float4 *)m, (float4 *)v, X, R, E,
+                                                   partial, ctrl, (int4 *)dbg_G, (float4 *)dbg_g1);
+    } else {
+        const UpdKernel k = pick<SelGeneric>(variant);
+        k<<<item_grid(rm, 8), 256, 0, st>>>(c, p, rm, (float4 *)z, (float4 *)m, (float4 *)v, X, R, E, partial,
+                                            ctrl, (int4 *)dbg_G, (float4 *)dbg_g1);
+    }
+}
+
+}  // namespace launch
+}  // namespace galois
