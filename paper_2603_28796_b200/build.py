@@ -19,7 +19,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-ftz=true", "-Xcompiler", "-fPIC,-O2,-Wall", "-Xptxas", "-v",
          "--expt-relaxed-constexpr", f"-I{os.path.join(ROOT, 'include')}", f"-I{CSRC}"]
-SOURCES = ["cnf_build.cu", "step_kernels.cu", "update_kernels.cu", "soft_kernels.cu", "engine.cu", "comm.cpp"]
+SOURCES = ["cnf_build.cu", "step_kernels.cu", "clause_kernels.cu", "update_kernels.cu", "soft_kernels.cu",
+           "engine.cu", "comm.cpp"]
 HEADERS = ["galois_internal.h", "philox.cuh", "device_utils.cuh", "comm.h"]
 
 

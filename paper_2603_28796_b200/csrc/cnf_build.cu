@@ -198,6 +198,16 @@ __global__ void k_radix_scatter(const uint32_t *__restrict__ keys_in, const int3
     }
 }
 
+__global__ void k_width_keys(int64_t m, const int32_t *__restrict__ clause_off, uint32_t *__restrict__ keys,
+                             int32_t *__restrict__ vals)
+{
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < m; c += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t w = clause_off[c + 1] - clause_off[c];
+        keys[c] = (uint32_t)(w < 0 ? 0 : (w > 255 ? 255 : w));
+        vals[c] = (int32_t)c;
+    }
+}
+
 __global__ void k_code_hist(const uint32_t *__restrict__ keys, int64_t L, int32_t *__restrict__ cnt)
 {
     for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < L;
@@ -241,16 +251,19 @@ size_t build_cnf_scratch_bytes(int32_t n, int64_t L)
 cudaError_t launch_build_cnf(int32_t n, int64_t m, int64_t L, const int64_t *d_off64,
                              const int32_t *d_lits, int32_t *d_clause_off, int2 *d_slot_info,
                              int32_t *d_code_off, int32_t *d_occ_slot, int32_t *d_err,
-                             int32_t *d_max_width, void *d_scratch, size_t scratch_bytes,
-                             cudaStream_t st)
+                             int32_t *d_max_width, int32_t *d_clause_perm, void *d_scratch,
+                             size_t scratch_bytes, cudaStream_t st)
 {
     (void)scratch_bytes;
+    // scratch is sized by build_cnf_scratch_bytes(n, max(L, m)): with empty clauses m > L
+    const int64_t NB = L > m ? L : m;
     const int64_t tiles = (L + kTile - 1) / kTile;
+    const int64_t tiles_nb = (NB + kTile - 1) / kTile;
     char *p = (char *)d_scratch;
-    uint32_t *keys_a = (uint32_t *)p; p += (size_t)L * 4;
-    uint32_t *keys_b = (uint32_t *)p; p += (size_t)L * 4;
-    int32_t *vals_b = (int32_t *)p;   p += (size_t)L * 4;
-    int32_t *hist = (int32_t *)p;     p += (size_t)256 * (tiles > 0 ? tiles : 1) * 4;
+    uint32_t *keys_a = (uint32_t *)p; p += (size_t)NB * 4;
+    uint32_t *keys_b = (uint32_t *)p; p += (size_t)NB * 4;
+    int32_t *vals_b = (int32_t *)p;   p += (size_t)NB * 4;
+    int32_t *hist = (int32_t *)p;     p += (size_t)256 * (tiles_nb > 0 ? tiles_nb : 1) * 4;
     int32_t *scan_scratch = (int32_t *)p;
     int32_t *vals_a = d_occ_slot;
 
@@ -280,6 +293,17 @@ cudaError_t launch_build_cnf(int32_t n, int64_t m, int64_t L, const int64_t *d_o
     if (L > 0) k_code_hist<<<grid_for(L), kThreads, 0, st>>>(kin, L, d_code_off);
     exclusive_scan(d_code_off, d_code_off, ncodes + 1, scan_scratch, st);
     if (L > 0) k_slot_info<<<grid_for(L), kThreads, 0, st>>>(kin, d_occ_slot, L, d_slot_info);
+
+    // clause processing order: stable sort of the clauses by width (one 8-bit radix pass;
+    // widths >= 255 share the last bucket) so that the clauses a warp handles together
+    // have similar widths — no divergence on mixed-width (industrial) CNFs
+    if (m > 0) {
+        const int64_t mt = (m + kTile - 1) / kTile;
+        k_width_keys<<<grid_for(m), kThreads, 0, st>>>(m, d_clause_off, keys_a, vals_b);
+        k_radix_hist<<<(unsigned)mt, kThreads, 0, st>>>(keys_a, m, 0, mt, hist);
+        exclusive_scan(hist, hist, 256 * mt, scan_scratch, st);
+        k_radix_scatter<<<(unsigned)mt, kThreads, 0, st>>>(keys_a, vals_b, keys_b, d_clause_perm, m, 0, mt, hist);
+    }
     return cudaGetLastError();
 }
 

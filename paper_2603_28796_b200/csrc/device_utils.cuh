@@ -75,6 +75,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase)
         : "memory");
 }
 
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
 // 1-D TMA bulk copy global -> shared (cp.async.bulk; SASS UBLKCP), completion counted in
 // bytes on the mbarrier. dst/src 16-B aligned, bytes a multiple of 16.
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar)

@@ -87,6 +87,7 @@ struct galois_cnf {
     int32_t max_width = 0;
     int32_t max_degree = 0;
     int32_t *clause_off = nullptr;
+    int32_t *clause_perm = nullptr;
     int2 *slot_info = nullptr;
     int32_t *code_off = nullptr;
     int32_t *occ_slot = nullptr;
@@ -103,6 +104,7 @@ struct galois_cnf {
         d.m = (int32_t)m;
         d.L = (int32_t)L;
         d.clause_off = clause_off;
+        d.clause_perm = clause_perm;
         d.slot_info = slot_info;
         d.code_off = code_off;
         d.occ_slot = occ_slot;
@@ -119,6 +121,7 @@ struct galois_cnf {
         cudaGetDevice(&cur);
         cudaSetDevice(device);
         cudaFree(clause_off);
+        cudaFree(clause_perm);
         cudaFree(slot_info);
         cudaFree(code_off);
         cudaFree(occ_slot);
@@ -192,10 +195,11 @@ extern "C" int galois_cnf_load(int32_t num_vars, int64_t num_clauses, const int6
     LOAD_TRY(dmalloc(&d_lits, (size_t)L));
     LOAD_TRY(dmalloc(&d_err, 8));
     LOAD_TRY(dmalloc(&c->clause_off, (size_t)m + 1));
+    LOAD_TRY(dmalloc(&c->clause_perm, (size_t)m));
     LOAD_TRY(dmalloc(&c->slot_info, (size_t)L));
     LOAD_TRY(dmalloc(&c->code_off, 2 * (size_t)num_vars + 1));
     LOAD_TRY(dmalloc(&c->occ_slot, (size_t)L));
-    const size_t scratch = build_cnf_scratch_bytes(num_vars, L);
+    const size_t scratch = build_cnf_scratch_bytes(num_vars, std::max<int64_t>(L, m));
     LOAD_TRY(cudaMalloc(&d_scratch, scratch));
     LOAD_TRY(cudaMemcpyAsync(d_off64, clause_offsets, sizeof(int64_t) * (size_t)(m + 1), cudaMemcpyHostToDevice, st));
     if (L > 0)
@@ -203,7 +207,7 @@ extern "C" int galois_cnf_load(int32_t num_vars, int64_t num_clauses, const int6
     const int32_t h_err_init[8] = {0, INT32_MAX, INT32_MAX, INT32_MAX, 0, 0, 0, 0};
     LOAD_TRY(cudaMemcpyAsync(d_err, h_err_init, sizeof(h_err_init), cudaMemcpyHostToDevice, st));
     LOAD_TRY(launch_build_cnf(num_vars, m, L, d_off64, d_lits, c->clause_off, c->slot_info, c->code_off,
-                              c->occ_slot, d_err, d_err + 4, d_scratch, scratch, st));
+                              c->occ_slot, d_err, d_err + 4, c->clause_perm, d_scratch, scratch, st));
     int32_t h_err[8];
     LOAD_TRY(cudaMemcpyAsync(h_err, d_err, sizeof(h_err), cudaMemcpyDeviceToHost, st));
     LOAD_TRY(cudaStreamSynchronize(st));

@@ -40,6 +40,7 @@ struct DevCnf {
     int32_t m;
     int32_t L;
     const int32_t *clause_off;   // [m+1]
+    const int32_t *clause_perm;  // [m] clauses in stable width order (warp-uniform widths)
     const int2 *slot_info;       // [L] {code, csc position}
     const int32_t *code_off;     // [2n+1]
     const int32_t *occ_slot;     // [L]
@@ -86,8 +87,8 @@ struct StepParams {
 cudaError_t launch_build_cnf(int32_t n, int64_t m, int64_t L, const int64_t *d_offsets64,
                              const int32_t *d_lits, int32_t *d_clause_off, int2 *d_slot_info,
                              int32_t *d_code_off, int32_t *d_occ_slot, int32_t *d_err,
-                             int32_t *d_max_width, void *d_scratch, size_t scratch_bytes,
-                             cudaStream_t st);
+                             int32_t *d_max_width, int32_t *d_clause_perm, void *d_scratch,
+                             size_t scratch_bytes, cudaStream_t st);
 size_t build_cnf_scratch_bytes(int32_t n, int64_t L);
 
 }  // namespace galois

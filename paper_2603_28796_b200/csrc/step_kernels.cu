@@ -137,8 +137,9 @@ __global__ void __launch_bounds__(256) k_clauses_st(DevCnf c, int32_t W, int32_t
     const int64_t ngroups = ((int64_t)c.m + CPW - 1) / CPW;
     const int64_t stride = (int64_t)gridDim.x * (blockDim.x >> 5);
     for (int64_t g = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; g < ngroups; g += stride) {
-        const int64_t cl = g * CPW + sub;
-        if (!lane_ok || cl >= c.m) continue;
+        const int64_t ci = g * CPW + sub;
+        if (!lane_ok || ci >= c.m) continue;
+        const int32_t cl = c.clause_perm[ci];     // width-sorted order
         const int32_t lo = c.clause_off[cl], width = c.clause_off[cl + 1] - lo;
         uint32_t any = 0, two = 0;       // per member bit: >= 1 / >= 2 literals true
         uint32_t S[8];
@@ -283,16 +284,28 @@ static dim3 clause_grid(const DevCnf &c, int32_t W)
     return dim3(bx, chunks);
 }
 
+bool use_v4_clauses(int32_t W);
+void forward_v4(const DevCnf &c, int32_t W, int32_t b_pad, const uint32_t *X, uint32_t *E, int32_t *lam,
+                Ctrl *ctrl, cudaStream_t st);
+void check_v4(const DevCnf &c, int32_t W, int32_t b_pad, const uint32_t *R, int32_t *unsat, Ctrl *ctrl,
+              cudaStream_t st);
+
 void forward_st(const DevCnf &c, int32_t W, int32_t b_pad, const uint32_t *X, uint32_t *E, int32_t *lam,
                 Ctrl *ctrl, cudaStream_t st)
 {
-    k_clauses_st<true><<<clause_grid(c, W), 256, 0, st>>>(c, W, b_pad, X, E, lam, ctrl);
+    if (use_v4_clauses(W))
+        forward_v4(c, W, b_pad, X, E, lam, ctrl, st);
+    else
+        k_clauses_st<true><<<clause_grid(c, W), 256, 0, st>>>(c, W, b_pad, X, E, lam, ctrl);
 }
 
 void check(const DevCnf &c, int32_t W, int32_t b_pad, const uint32_t *R, int32_t *unsat, Ctrl *ctrl,
            cudaStream_t st)
 {
-    k_clauses_st<false><<<clause_grid(c, W), 256, 0, st>>>(c, W, b_pad, R, nullptr, unsat, ctrl);
+    if (use_v4_clauses(W))
+        check_v4(c, W, b_pad, R, unsat, ctrl, st);
+    else
+        k_clauses_st<false><<<clause_grid(c, W), 256, 0, st>>>(c, W, b_pad, R, nullptr, unsat, ctrl);
 }
 
 void best(const int32_t *unsat, int32_t b_loc, int64_t b0, Ctrl *ctrl, bool finalize, cudaStream_t st)

@@ -24,7 +24,8 @@ namespace {
 
 constexpr int kBatch = 8;             // independent E loads in flight per thread (global path)
 constexpr int kStages = 3;            // TMA pipeline depth
-constexpr int kStageRows = 64;        // E rows staged per item (variables with degree <= 64)
+constexpr int kStageRows = 32;        // E rows staged per item (variables with degree <= 32)
+constexpr int kTmaCtasPerSm = 4;      // 4 x (3 x 16 KB) shared memory per SM
 constexpr int kStageE = kStageRows * 128;
 constexpr int kStageBytes = kStageE + 3 * 4096;   // E rows + z, m, v of 256 quads
 constexpr int kTmaSmem = kStages * kStageBytes;
@@ -148,21 +149,24 @@ __device__ __forceinline__ void quad_update(const StepParams &p, float2 ac, int3
             zn = zz[j] - 2.0f * p.lr * g1;
         }
         if (!kPins || pin_r < 0) zz[j] = zn;
-        bad |= !isfinite(zz[j]);
         g1o[j] = g1;
-        uint32_t xb, rb;
+        bool xb, rb;
         if (kPins && pin_r >= 0) {
-            xb = rb = (uint32_t)((bq + j) >> pin_r) & 1u;
+            xb = rb = (((bq + j) >> pin_r) & 1) != 0;
         } else {
-            rb = zz[j] >= 0.0f ? 1u : 0u;
-            if (kTau1)
-                xb = sample_bit_tau1(zz[j], unif_pair(wx[j]), exp_neg_abs(zz[j])) ? 1u : 0u;
-            else
-                xb = zz[j] + logistic_from_word(wx[j]) >= 0.0f ? 1u : 0u;
+            rb = zz[j] >= 0.0f;
+            if (kTau1) {
+                const float2 uu = unif_pair(wx[j]);
+                const float e = exp_neg_abs(zz[j]);
+                xb = (rb && uu.x >= uu.y * e) || (!rb && uu.x * e >= uu.y);
+            } else {
+                xb = zz[j] + logistic_from_word(wx[j]) >= 0.0f;
+            }
         }
-        rn |= rb << j;
-        xn |= xb << j;
+        rn |= rb ? (1u << j) : 0u;
+        xn |= xb ? (1u << j) : 0u;
     }
+    bad |= !isfinite((zz[0] + zz[1]) + (zz[2] + zz[3]));   // NaN/Inf in any lane survives the sum
     z = make_float4(zz[0], zz[1], zz[2], zz[3]);
     m = make_float4(mm[0], mm[1], mm[2], mm[3]);
     vv = make_float4(ww[0], ww[1], ww[2], ww[3]);
@@ -262,57 +266,72 @@ __global__ void __launch_bounds__(256) k_update_st(DevCnf c, StepParams p, RowMa
 }
 
 // -------------------------------- a6 + a7: fused update, TMA-pipelined (W % 32 == 0)
-// Persistent CTAs; item = (variable, 1024-member chunk), one quad per thread. Thread 0 is
-// the producer: kStages items ahead it issues 1-D TMA bulk copies (cp.async.bulk) of the
-// item's z, m, v rows (3 x 4 KB) and, for variables of degree <= kStageRows, of its
-// contiguous E block (deg x 128 B) into a shared-memory stage, completing on an mbarrier.
-// The memory system sees several items in flight per CTA with no register cost.
+// Persistent CTAs of 8 consumer warps (one quad per thread) + 1 producer warp; item =
+// (variable, 1024-member chunk). The producer's elected lane runs kStages items ahead:
+// per item it issues 1-D TMA bulk copies (cp.async.bulk) of the z, m, v rows (3 x 4 KB)
+// and, for variables of degree <= kStageRows, of their contiguous E block (deg x 128 B)
+// into a shared-memory stage completing on the stage's `full` mbarrier; consumer warps
+// release a stage through its `empty` mbarrier (one arrive per warp). No CTA-wide
+// barrier in the loop; the memory system sees kStages items per CTA in flight.
+constexpr int kConsumerWarps = 8;
+
 template <bool kDebug, bool kTau1, bool kAdam, bool kPins>
-__global__ void __launch_bounds__(256) k_update_tma(DevCnf c, StepParams p, RowMap rm, float4 *__restrict__ z4,
-                                                    float4 *__restrict__ m4, float4 *__restrict__ v4,
-                                                    uint32_t *__restrict__ X, uint32_t *__restrict__ R,
-                                                    const uint32_t *__restrict__ E,
-                                                    const short4 *__restrict__ partial, Ctrl *__restrict__ ctrl,
-                                                    int4 *__restrict__ dbg_G, float4 *__restrict__ dbg_g1)
+__global__ void __launch_bounds__(256 + 32) k_update_tma(DevCnf c, StepParams p, RowMap rm, float4 *__restrict__ z4,
+                                                         float4 *__restrict__ m4, float4 *__restrict__ v4,
+                                                         uint32_t *__restrict__ X, uint32_t *__restrict__ R,
+                                                         const uint32_t *__restrict__ E,
+                                                         const short4 *__restrict__ partial, Ctrl *__restrict__ ctrl,
+                                                         int4 *__restrict__ dbg_G, float4 *__restrict__ dbg_g1)
 {
     extern __shared__ __align__(128) uint8_t smem[];
-    __shared__ uint64_t full[kStages];
+    __shared__ uint64_t full[kStages], empty[kStages];
     __shared__ int4 hdr[kStages];          // {v, k0, k1, k2}
     __shared__ int32_t hmode[kStages];     // 1 = E staged, 2 = hub, 0 = E from global
     if (ctrl->stopped) return;
-    const int32_t s = ctrl->t;
-    const float2 ac = p.adam_consts[s];
-    const int tid = threadIdx.x, lane = tid & 31;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t QW = rm.QW;
 
     if (tid == 0) {
-        for (int i = 0; i < kStages; ++i) mbar_init(&full[i], 1);
+        for (int i = 0; i < kStages; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], kConsumerWarps);
+        }
         fence_mbar_init();
     }
     __syncthreads();
 
-    auto issue = [&](uint32_t j) {         // producer (thread 0): item j of this CTA
-        const uint32_t item = blockIdx.x + j * gridDim.x;
-        if (item >= rm.items) return;
-        const int st = (int)(j % kStages);
-        const uint32_t v = div_cpr(rm, item), ch = item - v * rm.cpr;
-        const int32_t k0 = c.code_off[2 * v], k1 = c.code_off[2 * v + 1], k2 = c.code_off[2 * v + 2];
-        const int32_t hub = c.num_hubs > 0 ? c.hub_of_var[v] : -1;
-        const bool staged = hub < 0 && (k2 - k0) <= kStageRows;
-        hdr[st] = make_int4((int32_t)v, k0, k1, k2);
-        hmode[st] = hub >= 0 ? 2 : (staged ? 1 : 0);
-        uint8_t *sb = smem + st * kStageBytes;
-        const uint32_t ebytes = staged ? (uint32_t)(k2 - k0) * 128u : 0u;
-        mbar_arrive_expect_tx(&full[st], 3u * 4096u + ebytes);
-        const size_t off = (size_t)v * QW + (size_t)ch * 256u;
-        bulk_g2s(sb + kStageE, z4 + off, 4096u, &full[st]);
-        bulk_g2s(sb + kStageE + 4096, m4 + off, 4096u, &full[st]);
-        bulk_g2s(sb + kStageE + 8192, v4 + off, 4096u, &full[st]);
-        if (ebytes) bulk_g2s(sb, E + ((size_t)ch * c.L + k0) * 32u, ebytes, &full[st]);
-    };
-    if (tid == 0)
-        for (uint32_t j = 0; j < (uint32_t)kStages; ++j) issue(j);
+    if (warp == kConsumerWarps) {          // ------------------------------ producer warp
+        if (lane == 0) {
+            for (uint32_t j = 0;; ++j) {
+                const uint32_t item = blockIdx.x + j * gridDim.x;
+                if (item >= rm.items) break;
+                const int st = (int)(j % kStages);
+                if (j >= (uint32_t)kStages) {
+                    mbar_wait(&empty[st], ((j / kStages) - 1u) & 1u);
+                    fence_proxy_async_smem();
+                }
+                const uint32_t v = div_cpr(rm, item), ch = item - v * rm.cpr;
+                const int32_t k0 = c.code_off[2 * v], k1 = c.code_off[2 * v + 1], k2 = c.code_off[2 * v + 2];
+                const int32_t hub = c.num_hubs > 0 ? c.hub_of_var[v] : -1;
+                const bool staged = hub < 0 && (k2 - k0) <= kStageRows;
+                hdr[st] = make_int4((int32_t)v, k0, k1, k2);
+                hmode[st] = hub >= 0 ? 2 : (staged ? 1 : 0);
+                uint8_t *sb = smem + st * kStageBytes;
+                const uint32_t ebytes = staged ? (uint32_t)(k2 - k0) * 128u : 0u;
+                mbar_arrive_expect_tx(&full[st], 3u * 4096u + ebytes);
+                const size_t off = (size_t)v * QW + (size_t)ch * 256u;
+                bulk_g2s(sb + kStageE, z4 + off, 4096u, &full[st]);
+                bulk_g2s(sb + kStageE + 4096, m4 + off, 4096u, &full[st]);
+                bulk_g2s(sb + kStageE + 8192, v4 + off, 4096u, &full[st]);
+                if (ebytes) bulk_g2s(sb, E + ((size_t)ch * c.L + k0) * 32u, ebytes, &full[st]);
+            }
+        }
+        return;
+    }
 
+    // ------------------------------------------------------------------ consumer warps
+    const int32_t s = ctrl->t;
+    const float2 ac = p.adam_consts[s];
     bool bad = false;
     for (uint32_t j = 0;; ++j) {
         const uint32_t item = blockIdx.x + j * gridDim.x;
@@ -341,6 +360,8 @@ __global__ void __launch_bounds__(256) k_update_tma(DevCnf c, StepParams p, RowM
             count_bits(col, 32, h.y, h.z, sh, 1, G);
             count_bits(col, 32, h.z, h.w, sh, -1, G);
         }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);   // this warp is done reading the stage
         const int64_t bq = p.b0 + 4 * (int64_t)q;
         uint32_t xn, rn;
         float g1o[4];
@@ -357,11 +378,6 @@ __global__ void __launch_bounds__(256) k_update_tma(DevCnf c, StepParams p, RowM
         if ((lane & 7) == 0) {
             X[(size_t)v * p.W + (q >> 3)] = xw;
             R[(size_t)v * p.W + (q >> 3)] = rw;
-        }
-        __syncthreads();                   // every thread is done with stage st
-        if (tid == 0) {
-            fence_proxy_async_smem();      // generic reads of the stage before the TMA refill
-            issue(j + kStages);
         }
     }
     if (bad) atomicOr(&ctrl->nonfinite, 1);
@@ -448,7 +464,7 @@ void update_st(const DevCnf &c, const StepParams &p, float *z, float *m, float *
             cudaFuncSetAttribute((const void *)k, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
             configured[variant] = true;
         }
-        k<<<item_grid(rm, 3), 256, kTmaSmem, st>>>(c, p, rm, (float4 *)z, (float4 *)m, (float4 *)v, X, R, E,
+        k<<<item_grid(rm, kTmaCtasPerSm), 256 + 32, kTmaSmem, st>>>(c, p, rm, (float4 *)z, (float4 *)m, (float4 *)v, X, R, E,
                                                    partial, ctrl, (int4 *)dbg_G, (float4 *)dbg_g1);
     } else {
         const UpdKernel k = pick<SelGeneric>(variant);
