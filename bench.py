@@ -269,7 +269,7 @@ def main():
                        "check_interval": 1, "lr": 0.5, "tau": 1.0, "optimizer": "adam",
                        "l2": f"inputs larger than L2 (fp32 state {3 * 4 * n * b_pad / 1e6:.0f} MB per GPU > 126 MB)",
                        "parallelism": f"dp{world} (batch sharding, NCCL MIN all-reduce of the best key per step)"},
-            "roofline": {"bound": "hbm", "kernel": "k_update_st (fused signal reduction + Adam + round + sample)",
+            "roofline": {"bound": "hbm", "kernel": "k_update_tma (fused signal reduction + Adam + round + sample)",
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": (achieved / peak) if achieved else None,
                          "traffic": ncu_traffic(args.workload), "algorithmic_bytes_per_launch": bytes_update,
