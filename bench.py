@@ -174,6 +174,8 @@ def main():
     ap.add_argument("--ref-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--tts", default=None, help="only measure time-to-first-SAT on this config's SAT set")
+    ap.add_argument("--tts-seeds", type=int, default=10)
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -189,6 +191,10 @@ def main():
         args.gpus = world if world > 1 else args.gpus
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    if args.tts:
+        print(json.dumps({"time_to_first_sat": time_to_sat(G, torch, dev, args.tts, range(args.tts_seeds))}),
+              flush=True)
+        return 0
     pg = None
     nccl_id = None
     if world > 1:
@@ -294,6 +300,41 @@ def main():
     if line is not None:
         print(json.dumps(line), flush=True)
     return 0
+
+
+def time_to_sat(G, torch, dev, which="C1", seeds=range(10), batch=None, steps=None):
+    """Time-to-first-SAT through the public API (galois_engine_run; host wall clock
+    bracketed by device syncs; CNF already loaded, engine create + init included),
+    per instance: SAT-set instances of the config's shape (C1: G1(50, 213, 3, seed);
+    C2: planted G2(10000, 42000, 3, seed); C4: planted G3)."""
+    from paper_2603_28796_b200 import instances as I
+    make = {"C1": lambda s: I.random_ksat(50, 213, 3, s),
+            "C2": lambda s: I.random_ksat(10_000, 42_000, 3, s, planted=True),
+            "C3a": lambda s: I.random_ksat(2_000, 42_000, 5, s, planted=True),
+            "C4": lambda s: I.industrial(1_000_000, 4_200_000, s, planted=True)}[which]
+    B = batch or WORKLOADS[which]["batch"]
+    T = steps or (100 if which == "C1" else 200)
+    out = []
+    for s in seeds:
+        inst = make(s)
+        cnf = G.Cnf.from_instance(inst)
+        for rep in range(2):               # the first repetition warms up
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            eng = G.Engine(cnf, B, T, 0.5, 0)
+            rc = eng.run()
+            best = eng.best_assignment()
+            torch.cuda.synchronize(dev)
+            el = time.perf_counter() - t0
+            eng.free()
+        out.append({"seed": s, "sat": rc == G.SAT, "seconds": el, "step": best["step"], "member": best["global_b"],
+                    "best_unsat": best["unsat"]})
+        cnf.free()
+    solved = [o for o in out if o["sat"]]
+    return {"instances": which, "batch": B, "steps_budget": T, "n": len(out), "solved": len(solved),
+            "median_seconds_solved": statistics.median(o["seconds"] for o in solved) if solved else None,
+            "median_step_solved": statistics.median(o["step"] for o in solved) if solved else None,
+            "per_instance": out}
 
 
 def run_e2e(G, inst, B, args, torch, dev):

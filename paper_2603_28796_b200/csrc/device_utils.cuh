@@ -45,6 +45,23 @@ __device__ __forceinline__ float sqrt_approx(float x)            // MUFU.SQRT, r
     return y;
 }
 
+// End of an update kernel: the last CTA to finish advances the step counter. Every CTA
+// read ctrl->t at its start, and the last CTA finishes after all of them started, so
+// no CTA can observe the new value. Call with the whole CTA (contains __syncthreads).
+__device__ __forceinline__ void last_cta_tick(Ctrl *ctrl)
+{
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const uint32_t total = gridDim.x * gridDim.y * gridDim.z;
+        if (atomicAdd(&ctrl->done_ctas, 1u) == total - 1u) {
+            ctrl->done_ctas = 0;
+            ctrl->t += 1;
+            __threadfence();
+        }
+    }
+}
+
 // --------------------------------------------------------------- mbarrier + TMA bulk copy
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 

@@ -1,11 +1,13 @@
 // engine.cu — the C ABI (include/galois.h) and the engine orchestration.
 //
-// One engine = one rank's slice of the batch on one GPU. Each step enqueues, on the
+// One engine = one rank's slice of the batch on one GPU. Step s enqueues, on the
 // engine's stream:
-//   memset Lambda | forward (a5) | hub partials (a6) | fused update (a6+a7)
-//   and at check points: memset unsat | check (a8) | best | [NCCL MIN (a9) | finalize] | extract
+//   clause sweep: forward of X_s (a5) [+ exact check of R_{s-1} if it is a check point (a8)]
+//   [best | NCCL MIN (a9) | finalize | extract]   (when R_{s-1} was checked)
+//   [hub partials (a6)] | fused update (a6+a7; its last CTA advances t)
+// A check left pending at the end (t = T, or before any result is read) runs alone.
 // Every kernel reads the device control block first and returns immediately once the
-// best member satisfies the CNF, so the host only polls an 8-byte flag per chunk.
+// best member satisfies the CNF, so the host only polls the control block per chunk.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -24,16 +26,15 @@ namespace galois {
 namespace launch {
 void init(const StepParams &p, float *z, float *m, float *v, uint32_t *X, uint32_t *R, cudaStream_t st);
 void resample(const StepParams &p, const float *z, uint32_t *X, uint32_t *R, int32_t t_next, cudaStream_t st);
-void forward_st(const DevCnf &c, int32_t W, int32_t b_pad, const uint32_t *X, uint32_t *E, int32_t *lam,
-                Ctrl *ctrl, cudaStream_t st);
-void check(const DevCnf &c, int32_t W, int32_t b_pad, const uint32_t *R, int32_t *unsat, Ctrl *ctrl,
-           cudaStream_t st);
+int clauses(const DevCnf &c, int32_t W, int32_t b_pad, const uint32_t *X, const uint32_t *R, uint32_t *E,
+            int32_t *lam, int32_t *unsat, Ctrl *ctrl, cudaStream_t st);
 void hub_partial(const DevCnf &c, int32_t W, int32_t b_pad, const uint32_t *E, short4 *partial,
                  const Ctrl *ctrl, cudaStream_t st);
 void update_st(const DevCnf &c, const StepParams &p, float *z, float *m, float *v, uint32_t *X, uint32_t *R,
                const uint32_t *E, const short4 *partial, Ctrl *ctrl, int32_t *dbg_G, float *dbg_g1,
                cudaStream_t st);
-void best(const int32_t *unsat, int32_t b_loc, int64_t b0, Ctrl *ctrl, bool finalize, cudaStream_t st);
+void best(const int32_t *unsat, int32_t *unsat_last, int32_t b_loc, int64_t b0, Ctrl *ctrl, bool finalize,
+          cudaStream_t st);
 void finalize(Ctrl *ctrl, int64_t b0, int32_t b_loc, cudaStream_t st);
 void extract(const uint32_t *R, int32_t n, int32_t W, int64_t b0, const Ctrl *ctrl, uint8_t *best_bits,
              cudaStream_t st);
@@ -300,6 +301,7 @@ struct galois_engine {
     bool own_stream = false;
     // state
     bool prepared = false, poisoned = false;
+    bool pending_check = false;  // the rounding in R still has to be checked
     int32_t steps_enqueued = 0;
     int64_t b_per = 0, b0 = 0;
     int32_t b_loc = 0, b_pad = 0, W = 0;
@@ -308,7 +310,7 @@ struct galois_engine {
     float *z = nullptr, *m = nullptr, *v = nullptr;
     uint32_t *X = nullptr, *R = nullptr, *E = nullptr;
     short4 *partial = nullptr;
-    int32_t *lam = nullptr, *unsat = nullptr;
+    int32_t *lam = nullptr, *unsat = nullptr, *unsat_last = nullptr;   // lam: 2 x b_pad (step parity)
     Ctrl *ctrl = nullptr;
     uint8_t *best_bits = nullptr;
     int8_t *pin_rank = nullptr;
@@ -348,6 +350,8 @@ struct galois_engine {
         p.num_pins = (int32_t)pins.size();
         p.pin_rank = pins.empty() ? nullptr : pin_rank;
         p.keys = philox_round_keys(seed);
+        p.clear_a = nullptr;
+        p.clear_b = nullptr;
         return p;
     }
 
@@ -381,7 +385,7 @@ static void engine_free_buffers(galois_engine *e)
 {
     cudaFree(e->z); cudaFree(e->m); cudaFree(e->v);
     cudaFree(e->X); cudaFree(e->R); cudaFree(e->E);
-    cudaFree(e->partial); cudaFree(e->lam); cudaFree(e->unsat);
+    cudaFree(e->partial); cudaFree(e->lam); cudaFree(e->unsat); cudaFree(e->unsat_last);
     cudaFree(e->ctrl); cudaFree(e->best_bits); cudaFree(e->pin_rank);
     cudaFree(e->adam_consts); cudaFree(e->dbg_G); cudaFree(e->dbg_g1);
     cudaFree(e->P); cudaFree(e->Es); cudaFree(e->lam_f); cudaFree(e->dbg_Gf);
@@ -528,14 +532,12 @@ static int poison(galois_engine *e, int code, const std::string &msg)
 
 static bool is_check_step(const galois_engine *e, int32_t s) { return (s % e->K) == 0 || s == e->T; }
 
-// Enqueue the check of the rounding currently in R (steps done = ctrl->t).
-static int enqueue_check(galois_engine *e)
+// Best tracking after the unsat counts of the rounding R_t are in e->unsat (t = ctrl->t):
+// local argmin, [NCCL MIN over ranks, finalize], winner's bits. One timing record per
+// kernel, so the launch counts of galois_engine_kernel_times are exact.
+static int enqueue_best(galois_engine *e)
 {
-    const DevCnf c = e->cnf->view();
-    ENG_CUDA(e, cudaMemsetAsync(e->unsat, 0, sizeof(int32_t) * (size_t)e->b_pad, e->stream));
-    e->timed(2, [&] { launch::check(c, e->W, e->b_pad, e->R, e->unsat, e->ctrl, e->stream); });
-    // one record per kernel, so the launch counts of galois_engine_kernel_times are exact
-    e->timed(3, [&] { launch::best(e->unsat, e->b_loc, e->b0, e->ctrl, e->world == 1, e->stream); });
+    e->timed(3, [&] { launch::best(e->unsat, e->unsat_last, e->b_loc, e->b0, e->ctrl, e->world == 1, e->stream); });
     if (e->world > 1) {
         std::string why;
         if (!e->comm.allreduce_min_u64(&e->ctrl->key_local, &e->ctrl->key_global, e->stream, &why))
@@ -547,14 +549,47 @@ static int enqueue_check(galois_engine *e)
     return GALOIS_OK;
 }
 
+// Check of the pending rounding alone (t = 0 after init, or the last step before results
+// are read): check-only sweep + best tracking.
+static int flush_check(galois_engine *e)
+{
+    if (!e->pending_check) return GALOIS_OK;
+    const DevCnf c = e->cnf->view();
+    ENG_CUDA(e, cudaMemsetAsync(e->unsat, 0, sizeof(int32_t) * (size_t)e->b_pad, e->stream));
+    e->timed(2, [&] {
+        launch::clauses(c, e->W, e->b_pad, nullptr, e->R, nullptr, nullptr, e->unsat, e->ctrl, e->stream);
+    });
+    e->pending_check = false;
+    if (int rc = enqueue_best(e)) return rc;
+    ENG_CUDA(e, cudaGetLastError());
+    return GALOIS_OK;
+}
+
+// Step s = steps_enqueued + 1. ST mode: one clause sweep does the forward of X_s and, if
+// the previous step was a check point, the exact check of R_{s-1}; then best tracking
+// for R_{s-1} (so a SAT rounding stops the engine before the update of step s), the hub
+// partials, and the fused update (which ticks t at its end).
 static int enqueue_step(galois_engine *e)
 {
     const DevCnf c = e->cnf->view();
-    const StepParams p = e->params();
+    StepParams p = e->params();
     const int32_t s = e->steps_enqueued + 1;
     if (e->mode == GALOIS_MODE_ST) {
-        ENG_CUDA(e, cudaMemsetAsync(e->lam, 0, sizeof(int32_t) * (size_t)e->b_pad, e->stream));
-        e->timed(0, [&] { launch::forward_st(c, e->W, e->b_pad, e->X, e->E, e->lam, e->ctrl, e->stream); });
+        const bool chk = e->pending_check;
+        // Lambda of step s goes to lam[s & 1]; the update of step s zeroes lam[(s+1) & 1]
+        // and unsat for the next sweep (and does nothing once the engine has stopped, so
+        // the counters of the deciding check survive)
+        int32_t *lam_s = e->lam + (size_t)(s & 1) * e->b_pad;
+        p.clear_a = e->lam + (size_t)((s + 1) & 1) * e->b_pad;
+        p.clear_b = e->unsat;
+        e->timed(0, [&] {
+            launch::clauses(c, e->W, e->b_pad, e->X, chk ? e->R : nullptr, e->E, lam_s, e->unsat, e->ctrl,
+                            e->stream);
+        });
+        if (chk) {
+            e->pending_check = false;
+            if (int rc = enqueue_best(e)) return rc;
+        }
         if (c.num_hub_chunks > 0)
             e->timed(4, [&] { launch::hub_partial(c, e->W, e->b_pad, e->E, e->partial, e->ctrl, e->stream); });
         e->timed(1, [&] {
@@ -562,6 +597,7 @@ static int enqueue_step(galois_engine *e)
                               e->debug ? e->dbg_G : nullptr, e->debug ? e->dbg_g1 : nullptr, e->stream);
         });
     } else {
+        if (int rc = flush_check(e)) return rc;
         ENG_CUDA(e, cudaMemsetAsync(e->lam_f, 0, sizeof(float) * (size_t)e->b_pad, e->stream));
         e->timed(0, [&] { launch::forward_soft(c, p, e->z, e->P, e->Es, e->lam_f, e->ctrl, e->stream); });
         e->timed(1, [&] {
@@ -571,7 +607,7 @@ static int enqueue_step(galois_engine *e)
     }
     ENG_CUDA(e, cudaGetLastError());
     e->steps_enqueued = s;
-    if (is_check_step(e, s)) return enqueue_check(e);
+    e->pending_check = is_check_step(e, s);
     return GALOIS_OK;
 }
 
@@ -605,12 +641,16 @@ static int prepare(galois_engine *e)
     ENG_CUDA(e, dmalloc(&e->X, (size_t)n * e->W));
     ENG_CUDA(e, dmalloc(&e->R, (size_t)n * e->W));
     ENG_CUDA(e, dmalloc(&e->unsat, (size_t)e->b_pad));
+    ENG_CUDA(e, dmalloc(&e->unsat_last, (size_t)e->b_pad));
+    ENG_CUDA(e, cudaMemsetAsync(e->unsat, 0, sizeof(int32_t) * (size_t)e->b_pad, e->stream));
+    ENG_CUDA(e, cudaMemsetAsync(e->unsat_last, 0, sizeof(int32_t) * (size_t)e->b_pad, e->stream));
     ENG_CUDA(e, dmalloc(&e->ctrl, 1));
     ENG_CUDA(e, dmalloc(&e->best_bits, (size_t)n));
     ENG_CUDA(e, cudaMemsetAsync(e->best_bits, 0, (size_t)n, e->stream));
     if (e->mode == GALOIS_MODE_ST) {
         ENG_CUDA(e, dmalloc(&e->E, (size_t)c->L * e->W));
-        ENG_CUDA(e, dmalloc(&e->lam, (size_t)e->b_pad));
+        ENG_CUDA(e, dmalloc(&e->lam, 2 * (size_t)e->b_pad));
+        ENG_CUDA(e, cudaMemsetAsync(e->lam, 0, 2 * sizeof(int32_t) * (size_t)e->b_pad, e->stream));
         if (c->num_hub_chunks > 0) ENG_CUDA(e, dmalloc(&e->partial, (size_t)c->num_hub_chunks * (e->b_pad / 4)));
         if (e->debug) {
             ENG_CUDA(e, dmalloc(&e->dbg_G, nb));
@@ -662,7 +702,7 @@ static int prepare(galois_engine *e)
     const StepParams p = e->params();
     e->timed(5, [&] { launch::init(p, e->z, e->m, e->v, e->X, e->R, e->stream); });
     ENG_CUDA(e, cudaGetLastError());
-    if (int rc = enqueue_check(e)) return rc;
+    e->pending_check = true;             // the t = 0 check runs with the first sweep
     return GALOIS_OK;
 }
 
@@ -675,6 +715,14 @@ static int read_ctrl(galois_engine *e, Ctrl *out)
     return GALOIS_OK;
 }
 
+// Run the pending check (if any) and read the control block: every result read goes
+// through here so the last rounding is always checked before it is reported.
+static int settle(galois_engine *e, Ctrl *out)
+{
+    if (int rc = flush_check(e)) return rc;
+    return read_ctrl(e, out);
+}
+
 extern "C" int galois_engine_step(galois_engine *e)
 {
     ENGINE_ENTRY(e);
@@ -684,7 +732,7 @@ extern "C" int galois_engine_step(galois_engine *e)
     if (h.stopped) return GALOIS_SAT;
     if (e->steps_enqueued >= e->T) return GALOIS_BUDGET;
     if (int rc = enqueue_step(e)) return rc;
-    if (int rc = read_ctrl(e, &h)) return rc;
+    if (int rc = settle(e, &h)) return rc;
     return h.stopped ? GALOIS_SAT : GALOIS_OK;
 }
 
@@ -718,7 +766,7 @@ extern "C" int galois_engine_run(galois_engine *e)
         ++iter;
     }
     Ctrl h;
-    if (int rc = read_ctrl(e, &h)) return rc;
+    if (int rc = settle(e, &h)) return rc;
     return h.stopped ? GALOIS_SAT : GALOIS_BUDGET;
 }
 
@@ -728,7 +776,7 @@ extern "C" int galois_engine_info(galois_engine *e, int64_t *local_batch, int64_
     ENGINE_ENTRY(e);
     if (int rc = prepare(e)) return rc;
     Ctrl h;
-    if (int rc = read_ctrl(e, &h)) return rc;
+    if (int rc = settle(e, &h)) return rc;
     if (local_batch) *local_batch = e->b_loc;
     if (first_global_b) *first_global_b = e->b0;
     if (steps_done) *steps_done = h.t;
@@ -742,7 +790,7 @@ extern "C" int galois_best_assignment(galois_engine *e, uint8_t *values, int32_t
     ENGINE_ENTRY(e);
     if (int rc = prepare(e)) return rc;
     Ctrl h;
-    if (int rc = read_ctrl(e, &h)) return rc;
+    if (int rc = settle(e, &h)) return rc;
     if (e->world > 1 && h.best_b >= 0) {
         const int root = (int)(h.best_b / e->b_per);
         std::string why;
@@ -761,9 +809,11 @@ extern "C" int galois_unsat_counts(galois_engine *e, int32_t *counts, int64_t *f
 {
     ENGINE_ENTRY(e);
     if (int rc = prepare(e)) return rc;
+    Ctrl h;
+    if (int rc = settle(e, &h)) return rc;
     if (counts && e->b_loc > 0)
-        ENG_CUDA(e, cudaMemcpyAsync(counts, e->unsat, sizeof(int32_t) * (size_t)e->b_loc, cudaMemcpyDeviceToHost,
-                                    e->stream));
+        ENG_CUDA(e, cudaMemcpyAsync(counts, e->unsat_last, sizeof(int32_t) * (size_t)e->b_loc,
+                                    cudaMemcpyDeviceToHost, e->stream));
     ENG_CUDA(e, cudaStreamSynchronize(e->stream));
     if (first_global_b) *first_global_b = e->b0;
     return GALOIS_OK;
@@ -823,8 +873,11 @@ extern "C" int galois_engine_set_iterate(galois_engine *e, const float *z, const
     ENG_CUDA(e, cudaMemcpyAsync(e->ctrl, &e->h_ctrl[0], sizeof(Ctrl), cudaMemcpyHostToDevice, e->stream));
     launch::resample(e->params(), e->z, e->X, e->R, t + 1, e->stream);
     ENG_CUDA(e, cudaGetLastError());
+    if (e->lam) ENG_CUDA(e, cudaMemsetAsync(e->lam, 0, 2 * sizeof(int32_t) * (size_t)e->b_pad, e->stream));
+    ENG_CUDA(e, cudaMemsetAsync(e->unsat, 0, sizeof(int32_t) * (size_t)e->b_pad, e->stream));
     ENG_CUDA(e, cudaStreamSynchronize(e->stream));
     e->steps_enqueued = t;
+    e->pending_check = false;            // the injected iterate is not a check point
     return GALOIS_OK;
 }
 
@@ -852,8 +905,12 @@ extern "C" int galois_engine_get_loss(galois_engine *e, float *lambda)
     if (!lambda) return fail(GALOIS_E_ARG, "lambda is NULL");
     if (int rc = prepare(e)) return rc;
     if (e->mode == GALOIS_MODE_ST) {
+        // Lambda of the last completed step t lives in lam[t & 1] (see enqueue_step)
+        Ctrl h;
+        if (int rc = read_ctrl(e, &h)) return rc;
         std::vector<int32_t> tmp((size_t)e->b_pad);
-        ENG_CUDA(e, cudaMemcpyAsync(tmp.data(), e->lam, tmp.size() * 4, cudaMemcpyDeviceToHost, e->stream));
+        ENG_CUDA(e, cudaMemcpyAsync(tmp.data(), e->lam + (size_t)(h.t & 1) * e->b_pad, tmp.size() * 4,
+                                    cudaMemcpyDeviceToHost, e->stream));
         ENG_CUDA(e, cudaStreamSynchronize(e->stream));
         for (int32_t b = 0; b < e->b_loc; ++b) lambda[b] = (float)tmp[b];
     } else {

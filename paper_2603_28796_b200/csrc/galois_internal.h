@@ -22,7 +22,7 @@ constexpr int kHubChunk = 128;       // occurrences per hub partial item (|parti
 
 // Device-side control block (one per engine, device memory).
 struct Ctrl {
-    int32_t t;            // steps done (incremented by the forward of each step)
+    int32_t t;            // steps done (incremented by the last CTA of each update kernel)
     int32_t stopped;      // 1 once the best member satisfies the CNF
     int32_t best_u;       // best unsat count so far (INT32_MAX = none)
     int32_t best_t;       // step of the best
@@ -32,7 +32,7 @@ struct Ctrl {
     unsigned long long key_local;   // (u << 32) | global b, min over local members
     unsigned long long key_global;  // same, min over ranks (NCCL MIN)
     int32_t last_check_t; // step of the last check
-    int32_t pad;
+    uint32_t done_ctas;   // CTAs of the running update kernel that finished (last one ticks t)
 };
 
 struct DevCnf {
@@ -81,7 +81,21 @@ struct StepParams {
     int32_t num_pins;
     const int8_t *pin_rank;   // [n] r or -1 (NULL if no pins)
     PhiloxKeys keys;          // round keys of the seed (philox.cuh)
+    // counters the update kernel zeroes for the next clause sweep (b_pad ints each, may be
+    // null); an update that returns early (engine stopped) leaves them untouched
+    int32_t *clear_a;
+    int32_t *clear_b;
 };
+
+// Zero the next sweep's counters (grid-stride over the CTAs of an update kernel).
+__device__ __forceinline__ void clear_counters(const StepParams &p)
+{
+    const int32_t stride = gridDim.x * blockDim.x;
+    for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < p.b_pad; i += stride) {
+        if (p.clear_a) p.clear_a[i] = 0;
+        if (p.clear_b) p.clear_b[i] = 0;
+    }
+}
 
 // kernels (launch wrappers in kernels.cu)
 cudaError_t launch_build_cnf(int32_t n, int64_t m, int64_t L, const int64_t *d_offsets64,

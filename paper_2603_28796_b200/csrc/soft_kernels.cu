@@ -10,6 +10,7 @@
 
 #include <cstdint>
 
+#include "device_utils.cuh"
 #include "galois_internal.h"
 #include "philox.cuh"
 
@@ -47,10 +48,6 @@ __global__ void __launch_bounds__(256) k_soft_sample(StepParams p, const float *
     }
 }
 
-__global__ void k_soft_tick(Ctrl *__restrict__ ctrl)
-{
-    if (!ctrl->stopped) ctrl->t += 1;
-}
 
 // Clause chunk blockIdx.y, member b: E (prefix then suffix products, as Eq.2 in slot
 // order) written to Es[csc position][b]; partial Lambda of the chunk to lam_part.
@@ -106,7 +103,7 @@ __global__ void __launch_bounds__(256) k_update_soft(DevCnf c, StepParams p, flo
                                                      float *__restrict__ dbg_G, float *__restrict__ dbg_g1)
 {
     if (ctrl->stopped) return;
-    const int32_t s = ctrl->t;
+    const int32_t s = ctrl->t + 1;                   // this step's index (t -> t+1)
     const float2 ac = p.adam_consts[s];
     const int lane = threadIdx.x & 31;
     const uint64_t total = (uint64_t)p.n * p.b_pad;
@@ -157,6 +154,7 @@ __global__ void __launch_bounds__(256) k_update_soft(DevCnf c, StepParams p, flo
         }
     }
     if (bad) atomicOr(&ctrl->nonfinite, 1);
+    last_cta_tick(ctrl);
 }
 
 namespace launch {
@@ -178,7 +176,6 @@ void forward_soft(const DevCnf &c, const StepParams &p, const float *z, float *P
     dim3 grid((unsigned)((p.b_pad + 255) / 256), kSoftChunks);
     k_soft_clauses<<<grid, 256, 0, st>>>(c, p.b_pad, P, Es, lam_part, ctrl);
     k_soft_lam<<<(unsigned)((p.b_pad + 255) / 256), 256, 0, st>>>(p.b_pad, kSoftChunks, lam_part, lam, ctrl);
-    k_soft_tick<<<1, 1, 0, st>>>(ctrl);
 }
 
 void update_soft(const DevCnf &c, const StepParams &p, float *z, float *m, float *v, uint32_t *X, uint32_t *R,

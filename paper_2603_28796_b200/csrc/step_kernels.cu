@@ -124,7 +124,6 @@ __global__ void __launch_bounds__(256) k_clauses_st(DevCnf c, int32_t W, int32_t
 {
     __shared__ int32_t s_cnt[1024];
     if (ctrl->stopped) return;
-    if (kForward && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) ctrl->t += 1;
     for (int i = threadIdx.x; i < 1024; i += blockDim.x) s_cnt[i] = 0;
     __syncthreads();
 
@@ -208,14 +207,16 @@ __device__ void finalize_best(Ctrl *ctrl, unsigned long long key, int64_t b0, in
     if (ctrl->best_u == 0) ctrl->stopped = 1;
 }
 
-__global__ void __launch_bounds__(1024) k_best(const int32_t *__restrict__ unsat, int32_t b_loc, int64_t b0,
-                                               Ctrl *__restrict__ ctrl, int32_t finalize)
+__global__ void __launch_bounds__(1024) k_best(const int32_t *__restrict__ unsat, int32_t *__restrict__ unsat_last,
+                                               int32_t b_loc, int64_t b0, Ctrl *__restrict__ ctrl, int32_t finalize)
 {
     __shared__ unsigned long long s_min[32];
     if (ctrl->stopped) return;
     unsigned long long best = ~0ull;
     for (int32_t i = threadIdx.x; i < b_loc; i += blockDim.x) {
-        const unsigned long long key = ((unsigned long long)(uint32_t)unsat[i] << 32) | (unsigned long long)(b0 + i);
+        const int32_t u = unsat[i];
+        unsat_last[i] = u;                 // counts of the last check (the live buffer is reused)
+        const unsigned long long key = ((unsigned long long)(uint32_t)u << 32) | (unsigned long long)(b0 + i);
         best = key < best ? key : best;
     }
 #pragma unroll
@@ -285,32 +286,28 @@ static dim3 clause_grid(const DevCnf &c, int32_t W)
 }
 
 bool use_v4_clauses(int32_t W);
-void forward_v4(const DevCnf &c, int32_t W, int32_t b_pad, const uint32_t *X, uint32_t *E, int32_t *lam,
-                Ctrl *ctrl, cudaStream_t st);
-void check_v4(const DevCnf &c, int32_t W, int32_t b_pad, const uint32_t *R, int32_t *unsat, Ctrl *ctrl,
-              cudaStream_t st);
+void clauses_v4(const DevCnf &c, int32_t W, int32_t b_pad, const uint32_t *X, const uint32_t *R, uint32_t *E,
+                int32_t *lam, int32_t *unsat, Ctrl *ctrl, cudaStream_t st);
 
-void forward_st(const DevCnf &c, int32_t W, int32_t b_pad, const uint32_t *X, uint32_t *E, int32_t *lam,
-                Ctrl *ctrl, cudaStream_t st)
+// One sweep over the clauses: forward of the sample X (E, Lambda) when X != null and the
+// exact check of the rounding R (unsat counts) when R != null. Returns kernels launched.
+int clauses(const DevCnf &c, int32_t W, int32_t b_pad, const uint32_t *X, const uint32_t *R, uint32_t *E,
+            int32_t *lam, int32_t *unsat, Ctrl *ctrl, cudaStream_t st)
 {
-    if (use_v4_clauses(W))
-        forward_v4(c, W, b_pad, X, E, lam, ctrl, st);
-    else
-        k_clauses_st<true><<<clause_grid(c, W), 256, 0, st>>>(c, W, b_pad, X, E, lam, ctrl);
+    if (use_v4_clauses(W)) {
+        clauses_v4(c, W, b_pad, X, R, E, lam, unsat, ctrl, st);
+        return (X || R) ? 1 : 0;
+    }
+    int k = 0;
+    if (X) { k_clauses_st<true><<<clause_grid(c, W), 256, 0, st>>>(c, W, b_pad, X, E, lam, ctrl); ++k; }
+    if (R) { k_clauses_st<false><<<clause_grid(c, W), 256, 0, st>>>(c, W, b_pad, R, nullptr, unsat, ctrl); ++k; }
+    return k;
 }
 
-void check(const DevCnf &c, int32_t W, int32_t b_pad, const uint32_t *R, int32_t *unsat, Ctrl *ctrl,
-           cudaStream_t st)
+void best(const int32_t *unsat, int32_t *unsat_last, int32_t b_loc, int64_t b0, Ctrl *ctrl, bool finalize,
+          cudaStream_t st)
 {
-    if (use_v4_clauses(W))
-        check_v4(c, W, b_pad, R, unsat, ctrl, st);
-    else
-        k_clauses_st<false><<<clause_grid(c, W), 256, 0, st>>>(c, W, b_pad, R, nullptr, unsat, ctrl);
-}
-
-void best(const int32_t *unsat, int32_t b_loc, int64_t b0, Ctrl *ctrl, bool finalize, cudaStream_t st)
-{
-    k_best<<<1, 1024, 0, st>>>(unsat, b_loc, b0, ctrl, finalize ? 1 : 0);
+    k_best<<<1, 1024, 0, st>>>(unsat, unsat_last, b_loc, b0, ctrl, finalize ? 1 : 0);
 }
 
 void finalize(Ctrl *ctrl, int64_t b0, int32_t b_loc, cudaStream_t st)

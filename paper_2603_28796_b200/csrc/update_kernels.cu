@@ -218,13 +218,14 @@ __global__ void __launch_bounds__(256) k_update_st(DevCnf c, StepParams p, RowMa
                                                    int4 *__restrict__ dbg_G, float4 *__restrict__ dbg_g1)
 {
     if (ctrl->stopped) return;
-    const int32_t s = ctrl->t;                       // this step's index (t-1 -> t)
+    const int32_t s = ctrl->t + 1;                   // this step's index (t -> t+1)
     const float2 ac = p.adam_consts[s];              // {2 lr / bc1, 1 / sqrt(bc2)}
     const int lane = threadIdx.x & 31;
     const int32_t CW = p.W < 32 ? p.W : 32;
     const uint32_t r_t = rm.QW >= 256 ? 0u : threadIdx.x / rm.QW;
     const uint32_t q_t = rm.QW >= 256 ? threadIdx.x : threadIdx.x - r_t * rm.QW;
     bool bad = false;
+    clear_counters(p);
     for (uint32_t item = blockIdx.x; item < rm.items; item += gridDim.x) {
         const ItemPos ip = item_pos(rm, item, r_t, q_t);
         const int32_t v = (int32_t)ip.row;
@@ -263,6 +264,7 @@ __global__ void __launch_bounds__(256) k_update_st(DevCnf c, StepParams p, RowMa
         }
     }
     if (bad) atomicOr(&ctrl->nonfinite, 1);
+    last_cta_tick(ctrl);
 }
 
 // -------------------------------- a6 + a7: fused update, TMA-pipelined (W % 32 == 0)
@@ -276,7 +278,7 @@ __global__ void __launch_bounds__(256) k_update_st(DevCnf c, StepParams p, RowMa
 constexpr int kConsumerWarps = 8;
 
 template <bool kDebug, bool kTau1, bool kAdam, bool kPins>
-__global__ void __launch_bounds__(256 + 32) k_update_tma(DevCnf c, StepParams p, RowMap rm, float4 *__restrict__ z4,
+__global__ void __launch_bounds__(256 + 32, kTmaCtasPerSm) k_update_tma(DevCnf c, StepParams p, RowMap rm, float4 *__restrict__ z4,
                                                          float4 *__restrict__ m4, float4 *__restrict__ v4,
                                                          uint32_t *__restrict__ X, uint32_t *__restrict__ R,
                                                          const uint32_t *__restrict__ E,
@@ -326,13 +328,15 @@ __global__ void __launch_bounds__(256 + 32) k_update_tma(DevCnf c, StepParams p,
                 if (ebytes) bulk_g2s(sb, E + ((size_t)ch * c.L + k0) * 32u, ebytes, &full[st]);
             }
         }
-        return;
-    }
-
+    } else {
     // ------------------------------------------------------------------ consumer warps
-    const int32_t s = ctrl->t;
+    const int32_t s = ctrl->t + 1;         // this step's index (t -> t+1)
     const float2 ac = p.adam_consts[s];
     bool bad = false;
+    for (int32_t i = blockIdx.x * 256 + tid; i < p.b_pad; i += gridDim.x * 256) {   // next sweep's counters
+        if (p.clear_a) p.clear_a[i] = 0;
+        if (p.clear_b) p.clear_b[i] = 0;
+    }
     for (uint32_t j = 0;; ++j) {
         const uint32_t item = blockIdx.x + j * gridDim.x;
         if (item >= rm.items) break;
@@ -381,6 +385,8 @@ __global__ void __launch_bounds__(256 + 32) k_update_tma(DevCnf c, StepParams p,
         }
     }
     if (bad) atomicOr(&ctrl->nonfinite, 1);
+    }                                      // consumer warps
+    last_cta_tick(ctrl);                   // one barrier site for producer and consumers
 }
 
 // ------------------------------------------------------------------ launch wrappers
