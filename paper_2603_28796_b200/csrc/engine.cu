@@ -15,6 +15,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -44,6 +45,7 @@ void forward_soft(const DevCnf &c, const StepParams &p, const float *z, float *P
 void update_soft(const DevCnf &c, const StepParams &p, float *z, float *m, float *v, uint32_t *X, uint32_t *R,
                  const float *Es, Ctrl *ctrl, float *dbg_G, float *dbg_g1, cudaStream_t st);
 int soft_chunks();
+cudaError_t configure_kernels();
 }  // namespace launch
 }  // namespace galois
 
@@ -136,6 +138,76 @@ struct galois_cnf {
 static void cnf_release(galois_cnf *c)
 {
     if (c && c->refs.fetch_sub(1) == 1) delete c;
+}
+
+// Sub-allocation plan of one contiguous device block (256-B aligned pieces).
+struct Slab {
+    std::vector<std::pair<void **, size_t>> items;
+    template <typename T>
+    void add(T **p, size_t count)
+    {
+        items.push_back({reinterpret_cast<void **>(p), (count ? count : 1) * sizeof(T)});
+    }
+    static size_t up(size_t x) { return (x + 255) / 256 * 256; }
+    size_t total() const
+    {
+        size_t t = 0;
+        for (const auto &it : items) t += up(it.second);
+        return t;
+    }
+    void assign(void *base) const
+    {
+        char *p = static_cast<char *>(base);
+        for (const auto &it : items) {
+            *it.first = p;
+            p += up(it.second);
+        }
+    }
+};
+
+// Pinned host mirrors of the control block (2 slots per engine) come from one process-wide
+// pinned page: page-locking memory costs ~ms, an engine should not pay it.
+static std::mutex g_pin_mu;
+static Ctrl *g_pin_base = nullptr;
+static std::vector<int> g_pin_free;
+constexpr int kPinSlots = 256;
+
+static cudaError_t pinned_ctrl_acquire(Ctrl **out)
+{
+    std::lock_guard<std::mutex> lock(g_pin_mu);
+    if (!g_pin_base) {
+        cudaError_t e = cudaMallocHost((void **)&g_pin_base, sizeof(Ctrl) * 2 * kPinSlots);
+        if (e != cudaSuccess) return e;
+        for (int i = kPinSlots - 1; i >= 0; --i) g_pin_free.push_back(i);
+    }
+    if (g_pin_free.empty()) return cudaMallocHost((void **)out, 2 * sizeof(Ctrl));   // overflow: own block
+    *out = g_pin_base + 2 * g_pin_free.back();
+    g_pin_free.pop_back();
+    return cudaSuccess;
+}
+
+static void pinned_ctrl_release(Ctrl *p)
+{
+    std::lock_guard<std::mutex> lock(g_pin_mu);
+    if (g_pin_base && p >= g_pin_base && p < g_pin_base + 2 * kPinSlots)
+        g_pin_free.push_back((int)((p - g_pin_base) / 2));
+    else
+        cudaFreeHost(p);
+}
+
+// Keep freed blocks in the device's default memory pool (no release to the OS between
+// engines), so repeated create/free is a pool hit.
+static cudaError_t use_pool_for_device(int device)
+{
+    static std::atomic<uint64_t> done{0};
+    if (device < 64 && (done.load() >> device) & 1ull) return cudaSuccess;
+    cudaMemPool_t pool;
+    cudaError_t e = cudaDeviceGetDefaultMemPool(&pool, device);
+    if (e != cudaSuccess) return e;
+    uint64_t threshold = UINT64_MAX;
+    e = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold);
+    if (e == cudaSuccess && device < 64) done.fetch_or(1ull << device);
+    return e;
 }
 
 template <typename T>
@@ -309,6 +381,7 @@ struct galois_engine {
     // device buffers
     float *z = nullptr, *m = nullptr, *v = nullptr;
     uint32_t *X = nullptr, *R = nullptr, *E = nullptr;
+    void *slab = nullptr;          // one pooled allocation holding every device buffer below
     short4 *partial = nullptr;
     int32_t *lam = nullptr, *unsat = nullptr, *unsat_last = nullptr;   // lam: 2 x b_pad (step parity)
     Ctrl *ctrl = nullptr;
@@ -320,6 +393,10 @@ struct galois_engine {
     float *P = nullptr, *Es = nullptr, *lam_f = nullptr, *dbg_Gf = nullptr;   // SOFT mode
     Ctrl *h_ctrl = nullptr;     // pinned mirror (2 slots)
     cudaEvent_t poll_ev[2] = {nullptr, nullptr};
+    // CUDA graph of kGraphSteps consecutive steps (run(); not while profiling)
+    cudaGraphExec_t graph = nullptr;
+    int32_t graph_steps = 0;
+    bool graph_failed = false;
     // profiling
     struct Rec {
         int cls;
@@ -383,13 +460,13 @@ struct galois_engine {
 
 static void engine_free_buffers(galois_engine *e)
 {
-    cudaFree(e->z); cudaFree(e->m); cudaFree(e->v);
-    cudaFree(e->X); cudaFree(e->R); cudaFree(e->E);
-    cudaFree(e->partial); cudaFree(e->lam); cudaFree(e->unsat); cudaFree(e->unsat_last);
-    cudaFree(e->ctrl); cudaFree(e->best_bits); cudaFree(e->pin_rank);
-    cudaFree(e->adam_consts); cudaFree(e->dbg_G); cudaFree(e->dbg_g1);
-    cudaFree(e->P); cudaFree(e->Es); cudaFree(e->lam_f); cudaFree(e->dbg_Gf);
-    if (e->h_ctrl) cudaFreeHost(e->h_ctrl);
+    if (e->slab) {
+        cudaFreeAsync(e->slab, e->stream);
+        cudaStreamSynchronize(e->stream);
+    }
+    e->slab = nullptr;
+    if (e->h_ctrl) pinned_ctrl_release(e->h_ctrl);
+    e->h_ctrl = nullptr;
     e->z = e->m = e->v = nullptr;
 }
 
@@ -615,6 +692,7 @@ static int prepare(galois_engine *e)
 {
     if (e->prepared) return GALOIS_OK;
     ENG_CUDA(e, cudaSetDevice(e->device));
+    ENG_CUDA(e, launch::configure_kernels());
     galois_cnf *c = e->cnf;
     const int32_t n = c->n;
     // batch slice: b_per = roundup(ceil(B / world), 32); pad the local slice to 32
@@ -635,36 +713,44 @@ static int prepare(galois_engine *e)
         e->own_stream = true;
     }
     const size_t nb = (size_t)n * (size_t)e->b_pad;
-    ENG_CUDA(e, dmalloc(&e->z, nb));
-    ENG_CUDA(e, dmalloc(&e->m, nb));
-    ENG_CUDA(e, dmalloc(&e->v, nb));
-    ENG_CUDA(e, dmalloc(&e->X, (size_t)n * e->W));
-    ENG_CUDA(e, dmalloc(&e->R, (size_t)n * e->W));
-    ENG_CUDA(e, dmalloc(&e->unsat, (size_t)e->b_pad));
-    ENG_CUDA(e, dmalloc(&e->unsat_last, (size_t)e->b_pad));
-    ENG_CUDA(e, cudaMemsetAsync(e->unsat, 0, sizeof(int32_t) * (size_t)e->b_pad, e->stream));
-    ENG_CUDA(e, cudaMemsetAsync(e->unsat_last, 0, sizeof(int32_t) * (size_t)e->b_pad, e->stream));
-    ENG_CUDA(e, dmalloc(&e->ctrl, 1));
-    ENG_CUDA(e, dmalloc(&e->best_bits, (size_t)n));
-    ENG_CUDA(e, cudaMemsetAsync(e->best_bits, 0, (size_t)n, e->stream));
+    // all device buffers of the engine live in ONE stream-ordered allocation from the
+    // device's memory pool (cheap to create and free repeatedly, e.g. time-to-SAT runs)
+    Slab slab;
+    slab.add(&e->z, nb);
+    slab.add(&e->m, nb);
+    slab.add(&e->v, nb);
+    slab.add(&e->X, (size_t)n * e->W);
+    slab.add(&e->R, (size_t)n * e->W);
+    slab.add(&e->unsat, (size_t)e->b_pad);
+    slab.add(&e->unsat_last, (size_t)e->b_pad);
+    slab.add(&e->ctrl, 1);
+    slab.add(&e->best_bits, (size_t)n);
+    slab.add(&e->adam_consts, (size_t)e->T + 2);
+    if (!e->pins.empty()) slab.add(&e->pin_rank, (size_t)n);
     if (e->mode == GALOIS_MODE_ST) {
-        ENG_CUDA(e, dmalloc(&e->E, (size_t)c->L * e->W));
-        ENG_CUDA(e, dmalloc(&e->lam, 2 * (size_t)e->b_pad));
-        ENG_CUDA(e, cudaMemsetAsync(e->lam, 0, 2 * sizeof(int32_t) * (size_t)e->b_pad, e->stream));
-        if (c->num_hub_chunks > 0) ENG_CUDA(e, dmalloc(&e->partial, (size_t)c->num_hub_chunks * (e->b_pad / 4)));
+        slab.add(&e->E, (size_t)c->L * e->W);
+        slab.add(&e->lam, 2 * (size_t)e->b_pad);
+        if (c->num_hub_chunks > 0) slab.add(&e->partial, (size_t)c->num_hub_chunks * (e->b_pad / 4));
         if (e->debug) {
-            ENG_CUDA(e, dmalloc(&e->dbg_G, nb));
-            ENG_CUDA(e, dmalloc(&e->dbg_g1, nb));
+            slab.add(&e->dbg_G, nb);
+            slab.add(&e->dbg_g1, nb);
         }
     } else {
-        ENG_CUDA(e, dmalloc(&e->P, nb));
-        ENG_CUDA(e, dmalloc(&e->Es, (size_t)c->L * e->b_pad));
-        ENG_CUDA(e, dmalloc(&e->lam_f, (size_t)e->b_pad * (1 + launch::soft_chunks())));
+        slab.add(&e->P, nb);
+        slab.add(&e->Es, (size_t)c->L * e->b_pad);
+        slab.add(&e->lam_f, (size_t)e->b_pad * (1 + launch::soft_chunks()));
         if (e->debug) {
-            ENG_CUDA(e, dmalloc(&e->dbg_Gf, nb));
-            ENG_CUDA(e, dmalloc(&e->dbg_g1, nb));
+            slab.add(&e->dbg_Gf, nb);
+            slab.add(&e->dbg_g1, nb);
         }
     }
+    ENG_CUDA(e, use_pool_for_device(e->device));
+    ENG_CUDA(e, cudaMallocAsync(&e->slab, slab.total(), e->stream));
+    slab.assign(e->slab);
+    ENG_CUDA(e, cudaMemsetAsync(e->unsat, 0, sizeof(int32_t) * (size_t)e->b_pad, e->stream));
+    ENG_CUDA(e, cudaMemsetAsync(e->unsat_last, 0, sizeof(int32_t) * (size_t)e->b_pad, e->stream));
+    ENG_CUDA(e, cudaMemsetAsync(e->best_bits, 0, (size_t)n, e->stream));
+    if (e->lam) ENG_CUDA(e, cudaMemsetAsync(e->lam, 0, 2 * sizeof(int32_t) * (size_t)e->b_pad, e->stream));
     // Adam step constants in fp64, per step index: 2 lr / (1 - beta1^t), 1 / sqrt(1 - beta2^t)
     // (the factor 2: z = theta_1 - theta_0 moves by twice the per-logit step)
     std::vector<float2> consts((size_t)e->T + 2);
@@ -673,13 +759,12 @@ static int prepare(galois_engine *e)
         const double bc2 = 1.0 - std::pow(e->beta2, (double)t);
         consts[t] = make_float2(t ? (float)(2.0 * e->lr / bc1) : 0.f, t ? (float)(1.0 / std::sqrt(bc2)) : 0.f);
     }
-    ENG_CUDA(e, dmalloc(&e->adam_consts, consts.size()));
     ENG_CUDA(e, cudaMemcpyAsync(e->adam_consts, consts.data(), consts.size() * sizeof(float2), cudaMemcpyHostToDevice,
                                 e->stream));
+    std::vector<int8_t> pr;
     if (!e->pins.empty()) {
-        std::vector<int8_t> pr((size_t)n, -1);
+        pr.assign((size_t)n, -1);
         for (size_t r = 0; r < e->pins.size(); ++r) pr[e->pins[r]] = (int8_t)r;
-        ENG_CUDA(e, dmalloc(&e->pin_rank, (size_t)n));
         ENG_CUDA(e, cudaMemcpyAsync(e->pin_rank, pr.data(), (size_t)n, cudaMemcpyHostToDevice, e->stream));
     }
     Ctrl h{};
@@ -688,7 +773,7 @@ static int prepare(galois_engine *e)
     h.best_u = INT32_MAX;
     h.best_t = -1;
     h.best_b = -1;
-    ENG_CUDA(e, cudaMallocHost((void **)&e->h_ctrl, 2 * sizeof(Ctrl)));
+    ENG_CUDA(e, pinned_ctrl_acquire(&e->h_ctrl));
     e->h_ctrl[0] = h;
     ENG_CUDA(e, cudaMemcpyAsync(e->ctrl, &e->h_ctrl[0], sizeof(Ctrl), cudaMemcpyHostToDevice, e->stream));
     ENG_CUDA(e, cudaStreamSynchronize(e->stream));   // h_ctrl[0] is reused below
@@ -703,6 +788,47 @@ static int prepare(galois_engine *e)
     e->timed(5, [&] { launch::init(p, e->z, e->m, e->v, e->X, e->R, e->stream); });
     ENG_CUDA(e, cudaGetLastError());
     e->pending_check = true;             // the t = 0 check runs with the first sweep
+    return GALOIS_OK;
+}
+
+// Enqueue G steps as one CUDA graph. The first call captures enqueue_step() G times (the
+// host-side state advances during capture exactly as every replay must) and launches
+// the instantiated graph; later calls replay it. Kernels read the step index from the
+// device control block, so one graph serves every chunk that starts at a multiple of G.
+static int launch_graph_chunk(galois_engine *e, int32_t G)
+{
+    if (e->graph && e->graph_steps == G) {
+        ENG_CUDA(e, cudaGraphLaunch(e->graph, e->stream));
+        e->steps_enqueued += G;
+        e->pending_check = is_check_step(e, e->steps_enqueued);
+        return GALOIS_OK;
+    }
+    if (e->graph) {
+        cudaGraphExecDestroy(e->graph);
+        e->graph = nullptr;
+    }
+    const int32_t s0 = e->steps_enqueued;
+    const bool pend0 = e->pending_check;
+    cudaGraph_t g = nullptr;
+    bool ok = cudaStreamBeginCapture(e->stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+    int rc = GALOIS_OK;
+    for (int32_t i = 0; ok && i < G && rc == GALOIS_OK; ++i) rc = enqueue_step(e);
+    if (ok) ok = cudaStreamEndCapture(e->stream, &g) == cudaSuccess && rc == GALOIS_OK;
+    if (ok) ok = cudaGraphInstantiate(&e->graph, g, 0) == cudaSuccess;
+    if (g) cudaGraphDestroy(g);
+    if (!ok) {                                  // fall back to plain launches for good
+        cudaGetLastError();
+        e->graph = nullptr;
+        e->graph_failed = true;
+        e->poisoned = false;
+        e->steps_enqueued = s0;
+        e->pending_check = pend0;
+        for (int32_t i = 0; i < G; ++i)
+            if (int r2 = enqueue_step(e)) return r2;
+        return GALOIS_OK;
+    }
+    e->graph_steps = G;
+    ENG_CUDA(e, cudaGraphLaunch(e->graph, e->stream));
     return GALOIS_OK;
 }
 
@@ -750,12 +876,25 @@ extern "C" int galois_engine_run(galois_engine *e)
 {
     ENGINE_ENTRY(e);
     if (int rc = prepare(e)) return rc;
-    // chunks of steps; poll the stop flag of chunk i-1 while chunk i is queued
-    const int32_t chunk = std::max<int32_t>(1, std::min<int32_t>(16, e->K * 4));
+    // chunks of G steps (G even and a multiple of K, so every chunk that starts at a
+    // multiple of G has the same kernel sequence and Lambda parity): replayed as one CUDA
+    // graph; the stop flag of chunk i-1 is polled while chunk i is queued
+    const int32_t KK = e->K % 2 == 0 ? e->K : 2 * e->K;
+    const int32_t G = KK * std::max<int32_t>(1, 8 / KK);
+    // graphs only pay off when the capture + instantiation (~ms) is amortised over many
+    // chunks; short runs (time-to-SAT) launch directly
+    const bool graphs = !e->profiling && e->stream != nullptr && e->mode == GALOIS_MODE_ST && !e->graph_failed &&
+                        e->T - e->steps_enqueued >= 32 * G;
     int iter = 0;
     while (e->steps_enqueued < e->T) {
-        for (int32_t i = 0; i < chunk && e->steps_enqueued < e->T; ++i)
-            if (int rc = enqueue_step(e)) return rc;
+        const int32_t s0 = e->steps_enqueued;
+        if (graphs && s0 % G == 0 && s0 + G < e->T) {
+            if (int rc = launch_graph_chunk(e, G)) return rc;
+        } else {
+            const int32_t end = std::min<int32_t>(e->T, (s0 / G + 1) * G);
+            while (e->steps_enqueued < end)
+                if (int rc = enqueue_step(e)) return rc;
+        }
         Ctrl *slot = &e->h_ctrl[iter & 1];
         ENG_CUDA(e, cudaMemcpyAsync(slot, e->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, e->stream));
         ENG_CUDA(e, cudaEventRecord(e->poll_ev[iter & 1], e->stream));
@@ -973,6 +1112,7 @@ extern "C" void galois_engine_free(galois_engine *e)
     for (auto ev : e->ev_pool) cudaEventDestroy(ev);
     for (auto ev : e->poll_ev)
         if (ev) cudaEventDestroy(ev);
+    if (e->graph) cudaGraphExecDestroy(e->graph);
     if (e->own_stream && e->stream) cudaStreamDestroy(e->stream);
     cnf_release(e->cnf);
     cudaSetDevice(cur);

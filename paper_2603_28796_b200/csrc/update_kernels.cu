@@ -12,6 +12,7 @@
 // are first reduced in fixed-size chunks by k_hub_partial (deterministic int16 partials).
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 
 #include "device_utils.cuh"
@@ -456,6 +457,24 @@ struct SelTma {
 
 bool use_tma_update(int32_t W) { return W % 32 == 0; }
 
+// Function attributes (dynamic shared memory of the TMA kernels) for the current device;
+// called once per engine before any launch (and so never during CUDA-graph capture).
+cudaError_t configure_kernels()
+{
+    static std::atomic<uint64_t> done{0};
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 64 && (done.load() >> dev) & 1ull) return cudaSuccess;
+    for (int v = 0; v < 16; ++v) {
+        e = cudaFuncSetAttribute((const void *)pick<SelTma>(v), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 kTmaSmem);
+        if (e != cudaSuccess) return e;
+    }
+    if (dev < 64) done.fetch_or(1ull << dev);
+    return cudaSuccess;
+}
+
 void update_st(const DevCnf &c, const StepParams &p, float *z, float *m, float *v, uint32_t *X, uint32_t *R,
                const uint32_t *E, const short4 *partial, Ctrl *ctrl, int32_t *dbg_G, float *dbg_g1,
                cudaStream_t st)
@@ -464,12 +483,7 @@ void update_st(const DevCnf &c, const StepParams &p, float *z, float *m, float *
     const int variant = (dbg_G ? 8 : 0) | (p.inv_tau == 1.0f ? 4 : 0) | (p.optimizer == 0 ? 2 : 0) |
                         (p.pin_rank ? 1 : 0);
     if (use_tma_update(p.W)) {
-        static bool configured[16] = {false};
-        const UpdKernel k = pick<SelTma>(variant);
-        if (!configured[variant]) {
-            cudaFuncSetAttribute((const void *)k, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
-            configured[variant] = true;
-        }
+        const UpdKernel k = pick<SelTma>(variant);   // smem attribute set by configure_kernels()
         k<<<item_grid(rm, kTmaCtasPerSm), 256 + 32, kTmaSmem, st>>>(c, p, rm, (float4 *)z, (float4 *)m, (float4 *)v, X, R, E,
                                                    partial, ctrl, (int4 *)dbg_G, (float4 *)dbg_g1);
     } else {
