@@ -67,7 +67,8 @@ template <bool kForward, bool kCheck>
 __global__ void __launch_bounds__(256) k_clauses_v4(DevCnf c, int32_t W, int32_t b_pad,
                                                     const uint32_t *__restrict__ X, const uint32_t *__restrict__ R,
                                                     uint32_t *__restrict__ E, int32_t *__restrict__ lam,
-                                                    int32_t *__restrict__ unsat, Ctrl *__restrict__ ctrl)
+                                                    int32_t *__restrict__ unsat, Ctrl *__restrict__ ctrl,
+                                                    BestArgs ba)
 {
     __shared__ int32_t s_lam[kForward ? 4096 : 1];   // members of this block's 128-word chunk
     __shared__ int32_t s_uns[kCheck ? 4096 : 1];
@@ -147,6 +148,31 @@ __global__ void __launch_bounds__(256) k_clauses_v4(DevCnf c, int32_t W, int32_t
         if (kForward && s_lam[i] != 0) atomicAdd(&lam[base + i], s_lam[i]);
         if (kCheck && s_uns[i] != 0) atomicAdd(&unsat[base + i], s_uns[i]);
     }
+    if (kCheck) {
+        // the last CTA to finish reduces the complete counts to the best key (a8) and, on
+        // a single rank, updates the best record and the stop flag (no extra launch)
+        __shared__ bool s_last;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            s_last = atomicAdd(&ctrl->done_ctas, 1u) == gridDim.x * gridDim.y - 1u;
+        }
+        __syncthreads();
+        if (s_last) {
+            __threadfence();
+            block_best(unsat, ba.unsat_last, ba.b_loc, ba.b0, ctrl, ba.finalize != 0);
+            if (threadIdx.x == 0) ctrl->done_ctas = 0;
+            if (ba.extract_n > 0) {          // small n: the winner's bits of R, in this CTA
+                __syncthreads();
+                if (__ldcg(&ctrl->improved)) {
+                    const int64_t lb = ctrl->best_b - ba.b0;
+#pragma unroll 8
+                    for (int32_t v = threadIdx.x; v < ba.extract_n; v += blockDim.x)
+                        ba.best_bits[v] = (uint8_t)((R[(size_t)v * ba.W + (lb >> 5)] >> (lb & 31)) & 1u);
+                }
+            }
+        }
+    }
 }
 
 namespace launch {
@@ -171,15 +197,15 @@ bool use_v4_clauses(int32_t W) { return W % 4 == 0; }
 
 // X != null: forward of the sample X (E, lam); R != null: exact check of R (unsat).
 void clauses_v4(const DevCnf &c, int32_t W, int32_t b_pad, const uint32_t *X, const uint32_t *R, uint32_t *E,
-                int32_t *lam, int32_t *unsat, Ctrl *ctrl, cudaStream_t st)
+                int32_t *lam, int32_t *unsat, Ctrl *ctrl, const BestArgs &ba, cudaStream_t st)
 {
     const dim3 grid = clause_grid_v4(c, W);
     if (X && R)
-        k_clauses_v4<true, true><<<grid, 256, 0, st>>>(c, W, b_pad, X, R, E, lam, unsat, ctrl);
+        k_clauses_v4<true, true><<<grid, 256, 0, st>>>(c, W, b_pad, X, R, E, lam, unsat, ctrl, ba);
     else if (X)
-        k_clauses_v4<true, false><<<grid, 256, 0, st>>>(c, W, b_pad, X, R, E, lam, unsat, ctrl);
+        k_clauses_v4<true, false><<<grid, 256, 0, st>>>(c, W, b_pad, X, R, E, lam, unsat, ctrl, ba);
     else if (R)
-        k_clauses_v4<false, true><<<grid, 256, 0, st>>>(c, W, b_pad, X, R, E, lam, unsat, ctrl);
+        k_clauses_v4<false, true><<<grid, 256, 0, st>>>(c, W, b_pad, X, R, E, lam, unsat, ctrl, ba);
 }
 
 }  // namespace launch

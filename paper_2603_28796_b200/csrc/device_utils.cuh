@@ -45,6 +45,52 @@ __device__ __forceinline__ float sqrt_approx(float x)            // MUFU.SQRT, r
     return y;
 }
 
+// Best record after a check (reading R10): the key (u << 32 | global b) is the
+// minimum over the members (and, with NCCL, over the ranks); the record improves only on
+// a strictly smaller count, so ties keep the earlier step and then the lower member.
+__device__ __forceinline__ void finalize_best(Ctrl *ctrl, unsigned long long key, int64_t b0, int32_t b_loc)
+{
+    const int64_t u = (int64_t)(key >> 32);         // 2^32 - 1 when no rank has members
+    const int64_t b = (int64_t)(key & 0xFFFFFFFFull);
+    ctrl->improved = 0;
+    if (u < (int64_t)ctrl->best_u) {
+        ctrl->best_u = (int32_t)u;
+        ctrl->best_t = ctrl->t;
+        ctrl->best_b = b;
+        ctrl->improved = (b >= b0 && b < b0 + b_loc) ? 1 : 0;
+    }
+    ctrl->last_check_t = ctrl->t;
+    if (ctrl->best_u == 0) ctrl->stopped = 1;
+}
+
+// Block-wide argmin of (unsat[i] << 32 | b0 + i) over the local members; keeps a copy of
+// the counts in unsat_last; thread 0 stores key_local and (one rank) finalizes.
+__device__ __forceinline__ void block_best(const int32_t *unsat, int32_t *unsat_last, int32_t b_loc, int64_t b0,
+                                           Ctrl *ctrl, bool finalize)
+{
+    __shared__ unsigned long long s_min[32];
+    unsigned long long best = ~0ull;
+#pragma unroll 8
+    for (int32_t i = threadIdx.x; i < b_loc; i += blockDim.x) {
+        const int32_t u = __ldcg(unsat + i);
+        unsat_last[i] = u;
+        const unsigned long long key = ((unsigned long long)(uint32_t)u << 32) | (unsigned long long)(b0 + i);
+        best = key < best ? key : best;
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+        const unsigned long long o = __shfl_xor_sync(0xffffffffu, best, d);
+        best = o < best ? o : best;
+    }
+    if ((threadIdx.x & 31) == 0) s_min[threadIdx.x >> 5] = best;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) best = s_min[w] < best ? s_min[w] : best;
+        ctrl->key_local = best;
+        if (finalize) finalize_best(ctrl, best, b0, b_loc);
+    }
+}
+
 // End of an update kernel: the last CTA to finish advances the step counter. Every CTA
 // read ctrl->t at its start, and the last CTA finishes after all of them started, so
 // no CTA can observe the new value. Call with the whole CTA (contains __syncthreads).

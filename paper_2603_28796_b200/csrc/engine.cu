@@ -27,8 +27,8 @@ namespace galois {
 namespace launch {
 void init(const StepParams &p, float *z, float *m, float *v, uint32_t *X, uint32_t *R, cudaStream_t st);
 void resample(const StepParams &p, const float *z, uint32_t *X, uint32_t *R, int32_t t_next, cudaStream_t st);
-int clauses(const DevCnf &c, int32_t W, int32_t b_pad, const uint32_t *X, const uint32_t *R, uint32_t *E,
-            int32_t *lam, int32_t *unsat, Ctrl *ctrl, cudaStream_t st);
+bool clauses(const DevCnf &c, int32_t W, int32_t b_pad, const uint32_t *X, const uint32_t *R, uint32_t *E,
+             int32_t *lam, int32_t *unsat, Ctrl *ctrl, const BestArgs &ba, cudaStream_t st);
 void hub_partial(const DevCnf &c, int32_t W, int32_t b_pad, const uint32_t *E, short4 *partial,
                  const Ctrl *ctrl, cudaStream_t st);
 void update_st(const DevCnf &c, const StepParams &p, float *z, float *m, float *v, uint32_t *X, uint32_t *R,
@@ -612,16 +612,36 @@ static bool is_check_step(const galois_engine *e, int32_t s) { return (s % e->K)
 // Best tracking after the unsat counts of the rounding R_t are in e->unsat (t = ctrl->t):
 // local argmin, [NCCL MIN over ranks, finalize], winner's bits. One timing record per
 // kernel, so the launch counts of galois_engine_kernel_times are exact.
-static int enqueue_best(galois_engine *e)
+static BestArgs best_args(const galois_engine *e)
 {
-    e->timed(3, [&] { launch::best(e->unsat, e->unsat_last, e->b_loc, e->b0, e->ctrl, e->world == 1, e->stream); });
+    BestArgs ba;
+    ba.unsat_last = e->unsat_last;
+    ba.b_loc = e->b_loc;
+    ba.b0 = e->b0;
+    ba.finalize = e->world == 1 ? 1 : 0;
+    // small instances: the sweep's last CTA also copies the winner's bits (n loads in one
+    // CTA); large ones launch the grid-wide k_extract instead
+    ba.best_bits = e->best_bits;
+    ba.W = e->W;
+    ba.extract_n = (e->world == 1 && e->cnf->n <= 32768) ? e->cnf->n : 0;
+    return ba;
+}
+
+// After the counts of a check are complete. best_done: the sweep's last CTA already
+// reduced them (and finalized on one rank). extract: launch k_extract for the winner's
+// bits (false when the sweep's last CTA already copied them).
+static int enqueue_best(galois_engine *e, bool best_done, bool extract)
+{
+    if (!best_done)
+        e->timed(3, [&] { launch::best(e->unsat, e->unsat_last, e->b_loc, e->b0, e->ctrl, e->world == 1, e->stream); });
     if (e->world > 1) {
         std::string why;
         if (!e->comm.allreduce_min_u64(&e->ctrl->key_local, &e->ctrl->key_global, e->stream, &why))
             return poison(e, GALOIS_E_NCCL, why);
         e->timed(3, [&] { launch::finalize(e->ctrl, e->b0, e->b_loc, e->stream); });
     }
-    e->timed(3, [&] { launch::extract(e->R, e->cnf->n, e->W, e->b0, e->ctrl, e->best_bits, e->stream); });
+    if (extract)
+        e->timed(3, [&] { launch::extract(e->R, e->cnf->n, e->W, e->b0, e->ctrl, e->best_bits, e->stream); });
     ENG_CUDA(e, cudaGetLastError());
     return GALOIS_OK;
 }
@@ -633,11 +653,13 @@ static int flush_check(galois_engine *e)
     if (!e->pending_check) return GALOIS_OK;
     const DevCnf c = e->cnf->view();
     ENG_CUDA(e, cudaMemsetAsync(e->unsat, 0, sizeof(int32_t) * (size_t)e->b_pad, e->stream));
+    bool done = false;
     e->timed(2, [&] {
-        launch::clauses(c, e->W, e->b_pad, nullptr, e->R, nullptr, nullptr, e->unsat, e->ctrl, e->stream);
+        done = launch::clauses(c, e->W, e->b_pad, nullptr, e->R, nullptr, nullptr, e->unsat, e->ctrl, best_args(e),
+                               e->stream);
     });
     e->pending_check = false;
-    if (int rc = enqueue_best(e)) return rc;
+    if (int rc = enqueue_best(e, done, !(done && best_args(e).extract_n > 0))) return rc;
     ENG_CUDA(e, cudaGetLastError());
     return GALOIS_OK;
 }
@@ -659,13 +681,14 @@ static int enqueue_step(galois_engine *e)
         int32_t *lam_s = e->lam + (size_t)(s & 1) * e->b_pad;
         p.clear_a = e->lam + (size_t)((s + 1) & 1) * e->b_pad;
         p.clear_b = e->unsat;
+        bool done = false;
         e->timed(0, [&] {
-            launch::clauses(c, e->W, e->b_pad, e->X, chk ? e->R : nullptr, e->E, lam_s, e->unsat, e->ctrl,
-                            e->stream);
+            done = launch::clauses(c, e->W, e->b_pad, e->X, chk ? e->R : nullptr, e->E, lam_s, e->unsat, e->ctrl,
+                                   best_args(e), e->stream);
         });
         if (chk) {
             e->pending_check = false;
-            if (int rc = enqueue_best(e)) return rc;
+            if (int rc = enqueue_best(e, done, !(done && best_args(e).extract_n > 0))) return rc;
         }
         if (c.num_hub_chunks > 0)
             e->timed(4, [&] { launch::hub_partial(c, e->W, e->b_pad, e->E, e->partial, e->ctrl, e->stream); });

@@ -87,6 +87,17 @@ struct StepParams {
     int32_t *clear_b;
 };
 
+// Best tracking done by the last CTA of a checking clause sweep.
+struct BestArgs {
+    int32_t *unsat_last;   // copy of the counts of this check
+    int32_t b_loc;
+    int64_t b0;
+    int32_t finalize;      // 1: single rank — update the best record and stop flag in-kernel
+    uint8_t *best_bits;    // with finalize and extract_n = n: copy the winner's rounding bits
+    int32_t extract_n;     //   in the same CTA (small n); 0: the engine launches k_extract
+    int32_t W;
+};
+
 // Zero the next sweep's counters (grid-stride over the CTAs of an update kernel).
 __device__ __forceinline__ void clear_counters(const StepParams &p)
 {

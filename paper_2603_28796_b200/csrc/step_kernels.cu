@@ -192,45 +192,11 @@ __global__ void __launch_bounds__(256) k_clauses_st(DevCnf c, int32_t W, int32_t
 
 // ------------------------------------------------------------------- a8/a9: best
 // Single block: min over local members of (u << 32 | global b). world == 1 finalizes too.
-__device__ void finalize_best(Ctrl *ctrl, unsigned long long key, int64_t b0, int32_t b_loc)
-{
-    const int64_t u = (int64_t)(key >> 32);         // 2^32 - 1 when no rank has members
-    const int64_t b = (int64_t)(key & 0xFFFFFFFFull);
-    ctrl->improved = 0;
-    if (u < (int64_t)ctrl->best_u) {
-        ctrl->best_u = (int32_t)u;
-        ctrl->best_t = ctrl->t;
-        ctrl->best_b = b;
-        ctrl->improved = (b >= b0 && b < b0 + b_loc) ? 1 : 0;
-    }
-    ctrl->last_check_t = ctrl->t;
-    if (ctrl->best_u == 0) ctrl->stopped = 1;
-}
-
 __global__ void __launch_bounds__(1024) k_best(const int32_t *__restrict__ unsat, int32_t *__restrict__ unsat_last,
                                                int32_t b_loc, int64_t b0, Ctrl *__restrict__ ctrl, int32_t finalize)
 {
-    __shared__ unsigned long long s_min[32];
     if (ctrl->stopped) return;
-    unsigned long long best = ~0ull;
-    for (int32_t i = threadIdx.x; i < b_loc; i += blockDim.x) {
-        const int32_t u = unsat[i];
-        unsat_last[i] = u;                 // counts of the last check (the live buffer is reused)
-        const unsigned long long key = ((unsigned long long)(uint32_t)u << 32) | (unsigned long long)(b0 + i);
-        best = key < best ? key : best;
-    }
-#pragma unroll
-    for (int d = 16; d > 0; d >>= 1) {
-        const unsigned long long o = __shfl_xor_sync(0xffffffffu, best, d);
-        best = o < best ? o : best;
-    }
-    if ((threadIdx.x & 31) == 0) s_min[threadIdx.x >> 5] = best;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) best = s_min[w] < best ? s_min[w] : best;
-        ctrl->key_local = best;
-        if (finalize) finalize_best(ctrl, best, b0, b_loc);
-    }
+    block_best(unsat, unsat_last, b_loc, b0, ctrl, finalize != 0);
 }
 
 __global__ void k_finalize(Ctrl *__restrict__ ctrl, int64_t b0, int32_t b_loc)
@@ -287,21 +253,22 @@ static dim3 clause_grid(const DevCnf &c, int32_t W)
 
 bool use_v4_clauses(int32_t W);
 void clauses_v4(const DevCnf &c, int32_t W, int32_t b_pad, const uint32_t *X, const uint32_t *R, uint32_t *E,
-                int32_t *lam, int32_t *unsat, Ctrl *ctrl, cudaStream_t st);
+                int32_t *lam, int32_t *unsat, Ctrl *ctrl, const BestArgs &ba, cudaStream_t st);
 
 // One sweep over the clauses: forward of the sample X (E, Lambda) when X != null and the
-// exact check of the rounding R (unsat counts) when R != null. Returns kernels launched.
-int clauses(const DevCnf &c, int32_t W, int32_t b_pad, const uint32_t *X, const uint32_t *R, uint32_t *E,
-            int32_t *lam, int32_t *unsat, Ctrl *ctrl, cudaStream_t st)
+// exact check of the rounding R (unsat counts) when R != null. Returns true when the
+// sweep also did the best tracking of the check in its last CTA (vectorised path);
+// otherwise the caller launches k_best.
+bool clauses(const DevCnf &c, int32_t W, int32_t b_pad, const uint32_t *X, const uint32_t *R, uint32_t *E,
+             int32_t *lam, int32_t *unsat, Ctrl *ctrl, const BestArgs &ba, cudaStream_t st)
 {
     if (use_v4_clauses(W)) {
-        clauses_v4(c, W, b_pad, X, R, E, lam, unsat, ctrl, st);
-        return (X || R) ? 1 : 0;
+        clauses_v4(c, W, b_pad, X, R, E, lam, unsat, ctrl, ba, st);
+        return R != nullptr;
     }
-    int k = 0;
-    if (X) { k_clauses_st<true><<<clause_grid(c, W), 256, 0, st>>>(c, W, b_pad, X, E, lam, ctrl); ++k; }
-    if (R) { k_clauses_st<false><<<clause_grid(c, W), 256, 0, st>>>(c, W, b_pad, R, nullptr, unsat, ctrl); ++k; }
-    return k;
+    if (X) k_clauses_st<true><<<clause_grid(c, W), 256, 0, st>>>(c, W, b_pad, X, E, lam, ctrl);
+    if (R) k_clauses_st<false><<<clause_grid(c, W), 256, 0, st>>>(c, W, b_pad, R, nullptr, unsat, ctrl);
+    return false;
 }
 
 void best(const int32_t *unsat, int32_t *unsat_last, int32_t b_loc, int64_t b0, Ctrl *ctrl, bool finalize,

@@ -16,7 +16,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libgalois.so")
+LIB_PATH = os.environ.get("GALOIS_LIB") or os.path.join(_PKG, "libgalois.so")   # override: A/B builds
 
 OK, BUDGET, SAT = 0, 1, 10
 E_ARG, E_VAR_RANGE, E_OFFSETS, E_EMPTY_CLAUSE = -1, -2, -3, -4
