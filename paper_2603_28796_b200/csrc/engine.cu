@@ -368,6 +368,7 @@ struct galois_engine {
     std::vector<int32_t> pins;   // 0-based, ascending
     int32_t rank = 0, world = 1;
     unsigned char nccl_id[128] = {0};
+    bool use_comm = false;         // NCCL path (world > 1, or a 1-rank communicator for tests)
     bool debug = false, profiling = false;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
@@ -560,6 +561,7 @@ extern "C" int galois_engine_set_comm(galois_engine *e, int32_t rank, int32_t wo
     e->rank = rank;
     e->world = world;
     if (id) memcpy(e->nccl_id, id, 128);
+    e->use_comm = world > 1 || id != nullptr;   // world = 1 with an id: the NCCL path on one GPU
     return GALOIS_OK;
 }
 
@@ -618,12 +620,12 @@ static BestArgs best_args(const galois_engine *e)
     ba.unsat_last = e->unsat_last;
     ba.b_loc = e->b_loc;
     ba.b0 = e->b0;
-    ba.finalize = e->world == 1 ? 1 : 0;
+    ba.finalize = e->use_comm ? 0 : 1;
     // small instances: the sweep's last CTA also copies the winner's bits (n loads in one
     // CTA); large ones launch the grid-wide k_extract instead
     ba.best_bits = e->best_bits;
     ba.W = e->W;
-    ba.extract_n = (e->world == 1 && e->cnf->n <= 32768) ? e->cnf->n : 0;
+    ba.extract_n = (!e->use_comm && e->cnf->n <= 32768) ? e->cnf->n : 0;
     return ba;
 }
 
@@ -633,8 +635,8 @@ static BestArgs best_args(const galois_engine *e)
 static int enqueue_best(galois_engine *e, bool best_done, bool extract)
 {
     if (!best_done)
-        e->timed(3, [&] { launch::best(e->unsat, e->unsat_last, e->b_loc, e->b0, e->ctrl, e->world == 1, e->stream); });
-    if (e->world > 1) {
+        e->timed(3, [&] { launch::best(e->unsat, e->unsat_last, e->b_loc, e->b0, e->ctrl, !e->use_comm, e->stream); });
+    if (e->use_comm) {
         std::string why;
         if (!e->comm.allreduce_min_u64(&e->ctrl->key_local, &e->ctrl->key_global, e->stream, &why))
             return poison(e, GALOIS_E_NCCL, why);
@@ -801,7 +803,7 @@ static int prepare(galois_engine *e)
     ENG_CUDA(e, cudaMemcpyAsync(e->ctrl, &e->h_ctrl[0], sizeof(Ctrl), cudaMemcpyHostToDevice, e->stream));
     ENG_CUDA(e, cudaStreamSynchronize(e->stream));   // h_ctrl[0] is reused below
     for (auto &ev : e->poll_ev) ENG_CUDA(e, cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-    if (e->world > 1) {
+    if (e->use_comm) {
         std::string why;
         if (!e->comm.init(e->rank, e->world, e->nccl_id, &why)) return poison(e, GALOIS_E_NCCL, why);
     }
@@ -953,7 +955,7 @@ extern "C" int galois_best_assignment(galois_engine *e, uint8_t *values, int32_t
     if (int rc = prepare(e)) return rc;
     Ctrl h;
     if (int rc = settle(e, &h)) return rc;
-    if (e->world > 1 && h.best_b >= 0) {
+    if (e->use_comm && h.best_b >= 0) {
         const int root = (int)(h.best_b / e->b_per);
         std::string why;
         if (!e->comm.broadcast_bytes(e->best_bits, (size_t)e->cnf->n, root, e->stream, &why))

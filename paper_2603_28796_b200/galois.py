@@ -214,7 +214,7 @@ class Engine:
             _check(L.galois_engine_set_debug(self.handle, 1))
         if stream is not None:
             _check(L.galois_engine_set_stream(self.handle, ctypes.c_void_p(int(stream))))
-        if world > 1:
+        if world > 1 or nccl_id is not None:
             buf = ctypes.create_string_buffer(bytes(nccl_id), 128)
             _check(L.galois_engine_set_comm(self.handle, int(rank), int(world), buf))
 

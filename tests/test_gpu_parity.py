@@ -161,6 +161,26 @@ def test_batch_independence_and_determinism(G):
         np.testing.assert_array_equal(a, b)
 
 
+@pytest.mark.parametrize("batch", [256, 2048])
+def test_nccl_path_single_rank(G, batch):
+    """a9 through NCCL on one GPU: a 1-rank communicator (ncclCommInitRank from our own
+    ncclUniqueId; MIN all-reduce of the best key each check; k_finalize; broadcast of the
+    winner's bits) gives exactly the single-process results."""
+    inst = I.random_ksat(60, 255, 3, 13, planted=True)
+    outs = []
+    for nid in (None, G.galois_comm_unique_id()):
+        cnf = G.Cnf.from_instance(inst)
+        eng = G.Engine(cnf, batch, 40, 0.5, 21, rank=0, world=1, nccl_id=nid)
+        rc = eng.run()
+        best = eng.best_assignment()
+        u, _ = eng.unsat_counts()
+        z = eng.get_iterate()[0]
+        outs.append((rc, best["unsat"], best["step"], best["global_b"], best["values"].tobytes(), u.tobytes(),
+                     z.tobytes()))
+        eng.free()
+    assert outs[0] == outs[1]
+
+
 def test_cubes(G):
     """Lemma 1 cube pins: pinned variables follow alpha = b mod 2^d, never move, and the
     engine matches the oracle with pins."""
