@@ -168,6 +168,32 @@ int galois_engine_set_profiling(galois_engine *eng, int32_t enable);
 /* Produce a 128-byte ncclUniqueId into out (on one rank). E_NCCL if NCCL is absent. */
 int galois_comm_unique_id(void *out128);
 
+/* ------------------------------------- what the CPU stage consumes */
+
+/* theta_sel ("we select the logits theta_sel from the batch with the minimal clause
+ * loss"; "the one with the highest loss value"): rule 0 = the local member with the
+ * fewest unsatisfied clauses at the last check, rule 1 = the most; ties to the lower member.
+ * Outputs its global index, its count and (z may be NULL) its reduced logits
+ * z_v = theta_{v,1} - theta_{v,0} (n floats, host). Local to this rank. */
+int galois_select_member(galois_engine *eng, int32_t rule, int64_t *global_b, int32_t *unsat, float *z);
+
+/* Candidate pool (Eq.10) of member `global_b` (local to this rank): N samples
+ * x^(k)_v = [z_v + ell^(k)_v >= 0] with fresh logistic noise (Philox counter (v, k/4, 0, 2),
+ * word k mod 4, key pool_seed) and confidences c^(k)_v = max(y_0, y_1) = sigma(|z_v + ell|/tau);
+ * and per candidate the S = max(1, ceil(rho * n)) most confident variables (Eq.11,
+ * P:221-237; paper rho = 0.0005) as DIMACS unit literals (+v if x = 1, else -v),
+ * ordered by descending confidence, ties to the lower index.
+ *   values [N][n] uint8 (may be NULL), confidence [N][n] float (may be NULL),
+ *   units [N][S] int32 (may be NULL; S <= 4096), *S_out = S. E_ARG on bad sizes. */
+int galois_candidate_pool(galois_engine *eng, int64_t global_b, int32_t N, double rho, uint64_t pool_seed,
+                          uint8_t *values, float *confidence, int32_t *units, int32_t *S_out);
+
+/* Confidence-guided branching (Lemma 1: "identify d variables with the lowest
+ * confidence"): the d variables of member global_b with the lowest noise-free confidence
+ * sigma(|z_v|/tau) (= smallest |z_v|), ties to the lower index, 1-based ascending — ready
+ * for galois_engine_set_cubes. 1 <= d <= min(n, 4096). */
+int galois_cube_variables(galois_engine *eng, int64_t global_b, int32_t d, int32_t *vars);
+
 /* ------------------------------------------------------ test hooks (parity / resume) */
 
 /* Reduced iterate of the local members, host [b_loc][n] float each (NULL to skip):

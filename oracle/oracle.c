@@ -400,6 +400,28 @@ int32_t oracle_run(const oracle_cnf *f, const oracle_config *cfg, int64_t b0, in
     return t;
 }
 
+/* Candidate pool (Eq.10; SPEC sat-pool.sample_pool): N Gumbel samples of the
+ * selected member's logits, here in reduced form z_v = theta_{v,1} - theta_{v,0}. Sample k
+ * draws ell^(k)_v = ln u - ln(1-u) from Philox counter (v, k/4, 0, 2), word k mod 4, key =
+ * pool_seed (reading R2's layout in a separate counter domain); a = (z_v + ell)/tau;
+ * x^(k)_v = [a >= 0] (Eq.4, ties to 1); c^(k)_v = max(y_0, y_1) = sigma(|a|). */
+void oracle_pool(const double *z, int32_t n, int32_t N, double tau, uint64_t pool_seed,
+                 uint8_t *x /* [N][n] */, double *conf /* [N][n] */)
+{
+    const uint32_t key[2] = {(uint32_t)pool_seed, (uint32_t)(pool_seed >> 32)};
+    for (int32_t k = 0; k < N; k++)
+        for (int32_t v = 0; v < n; v++) {
+            uint32_t ctr[4] = {(uint32_t)v, (uint32_t)(k >> 2), 0u, 2u};
+            uint32_t w[4];
+            oracle_philox4x32_10(ctr, key, w);
+            uint32_t word = w[k & 3];
+            double ell = log(oracle_uniform(word)) - log(oracle_uniform_complement(word));
+            double a = (z[v] + ell) / tau;
+            x[(int64_t)k * n + v] = (uint8_t)(a >= 0.0 ? 1 : 0);
+            conf[(int64_t)k * n + v] = 1.0 / (1.0 + exp(-fabs(a)));
+        }
+}
+
 int32_t oracle_num_threads(void)
 {
 #ifdef _OPENMP

@@ -75,6 +75,7 @@ def lib():
         _lib.oracle_run.argtypes = [P, P, ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
                                     P, P, P, P, P, P, P, P]
         _lib.oracle_run.restype = ctypes.c_int32
+        _lib.oracle_pool.argtypes = [P, ctypes.c_int32, ctypes.c_int32, ctypes.c_double, ctypes.c_uint64, P, P]
         _lib.oracle_num_threads.restype = ctypes.c_int32
         _lib.oracle_set_num_threads.argtypes = [ctypes.c_int32]
     return _lib
@@ -252,6 +253,51 @@ def run(f: Cnf, cfg: Config, b0: int, nb: int, T: int, K: int = 1) -> dict:
     return dict(steps=int(steps), best_unsat=int(bu.value), best_t=int(bt.value), best_b=int(bb.value),
                 best_r=best_r[:n].copy(), last_unsat=last[:nb].copy(),
                 state=State(theta, mom, vel, int(steps), b0))
+
+
+# ------------------------------------------------- what the CPU stage consumes (f1, f3)
+def select_member(counts: np.ndarray, b0: int, rule: int = 0):
+    """theta_sel (P:102 min loss / P:210 max loss) over exact unsat counts, ties to the
+    lower member. Returns (global member, count)."""
+    counts = np.asarray(counts)
+    best = None
+    for i, u in enumerate(counts):
+        key = (u, i) if rule == 0 else (-u, i)
+        if best is None or key < best[0]:
+            best = (key, i)
+    i = best[1]
+    return b0 + i, int(counts[i])
+
+
+def pool(z, N: int, tau: float, pool_seed: int):
+    """Eq.10: N samples of the reduced logits z (fp64) -> (x [N][n] uint8, conf [N][n])."""
+    z = np.ascontiguousarray(z, dtype=np.float64)
+    n = len(z)
+    x = np.zeros((N, n), np.uint8)
+    c = np.zeros((N, n), np.float64)
+    lib().oracle_pool(_ptr(z), n, N, tau, pool_seed & 0xFFFFFFFFFFFFFFFF, _ptr(x), _ptr(c))
+    return x, c
+
+
+def top_confident_units(x, conf, rho: float):
+    """Eq.11 / SPEC extract_partial: |S| = max(1, ceil(rho n)); variables by descending
+    confidence, ties to the lower index; literal +v if x_v = 1 else -v (1-based)."""
+    x = np.asarray(x); conf = np.asarray(conf)
+    n = len(conf)
+    S = max(1, int(np.ceil(rho * n - 1e-9)))
+    order = sorted(range(n), key=lambda v: (-conf[v], v))[:S]
+    return [v + 1 if x[v] else -(v + 1) for v in order]
+
+
+def lowest_confidence_vars(z, d: int, tau: float = 1.0):
+    """Lemma 1 branching (SPEC select_branch_vars): the d variables with the
+    lowest noise-free confidence max(y0, y1) = sigma(|z|/tau), ties to the lower index,
+    returned 1-based ascending."""
+    z = np.asarray(z, dtype=np.float64)
+    # sigma is strictly increasing, so ordering by confidence is ordering by |z| / tau; the
+    # key |z| keeps the order exact where sigma would round to 1.0 (|z| > ~37)
+    order = sorted(range(len(z)), key=lambda v: (abs(z[v]), v))[:d]
+    return sorted(v + 1 for v in order)
 
 
 def num_threads() -> int:

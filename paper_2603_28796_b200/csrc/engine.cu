@@ -46,6 +46,15 @@ void update_soft(const DevCnf &c, const StepParams &p, float *z, float *m, float
                  const float *Es, Ctrl *ctrl, float *dbg_G, float *dbg_g1, cudaStream_t st);
 int soft_chunks();
 cudaError_t configure_kernels();
+// selection (select_kernels.cu)
+void select_member(const int32_t *counts, int32_t b_loc, int64_t b0, int32_t rule, unsigned long long *out,
+                   cudaStream_t st);
+void gather_z(const float *z, int32_t n, int32_t b_pad, int32_t lb, float *out, cudaStream_t st);
+void pool(const float *zsel, int32_t n, int32_t N, float inv_tau, uint64_t pool_seed, uint8_t *x, float *conf,
+          cudaStream_t st);
+void topk(const uint8_t *x, const float *conf, int32_t n, int32_t N, int32_t S, int32_t *units, cudaStream_t st);
+void lowconf(const float *zsel, int32_t n, int32_t d, int32_t *vars, cudaStream_t st);
+int max_sorted();
 }  // namespace launch
 }  // namespace galois
 
@@ -993,6 +1002,110 @@ static int copy_transposed_out(galois_engine *e, const T *dev, T *host)
     ENG_CUDA(e, cudaStreamSynchronize(e->stream));
     for (int32_t b = 0; b < e->b_loc; ++b)
         for (int32_t v = 0; v < n; ++v) host[(size_t)b * n + v] = tmp[(size_t)v * e->b_pad + b];
+    return GALOIS_OK;
+}
+
+// ----------------------------------------------------------- selection (f1, f3)
+// Scratch for the selection calls: temporary stream-ordered allocations (not hot path).
+template <typename T>
+static int tmp_alloc(galois_engine *e, T **p, size_t count)
+{
+    ENG_CUDA(e, cudaMallocAsync((void **)p, std::max<size_t>(count, 1) * sizeof(T), e->stream));
+    return GALOIS_OK;
+}
+
+extern "C" int galois_select_member(galois_engine *e, int32_t rule, int64_t *global_b, int32_t *unsat, float *z)
+{
+    ENGINE_ENTRY(e);
+    if (rule != 0 && rule != 1) return fail(GALOIS_E_ARG, "rule must be 0 (min loss) or 1 (max loss)");
+    if (int rc = prepare(e)) return rc;
+    Ctrl h;
+    if (int rc = settle(e, &h)) return rc;
+    if (e->b_loc == 0) return fail(GALOIS_E_STATE, "this rank has no members");
+    unsigned long long *d_key = nullptr;
+    if (int rc = tmp_alloc(e, &d_key, 1)) return rc;
+    launch::select_member(e->unsat_last, e->b_loc, e->b0, rule, d_key, e->stream);
+    unsigned long long key = 0;
+    ENG_CUDA(e, cudaMemcpyAsync(&key, d_key, 8, cudaMemcpyDeviceToHost, e->stream));
+    ENG_CUDA(e, cudaFreeAsync(d_key, e->stream));
+    ENG_CUDA(e, cudaStreamSynchronize(e->stream));
+    const int64_t b = (int64_t)(key & 0xFFFFFFFFull);
+    const uint32_t u = (uint32_t)(key >> 32);
+    if (global_b) *global_b = b;
+    if (unsat) *unsat = (int32_t)(rule ? ~u : u);
+    if (z) {
+        float *d_z = nullptr;
+        if (int rc = tmp_alloc(e, &d_z, (size_t)e->cnf->n)) return rc;
+        launch::gather_z(e->z, e->cnf->n, e->b_pad, (int32_t)(b - e->b0), d_z, e->stream);
+        ENG_CUDA(e, cudaMemcpyAsync(z, d_z, (size_t)e->cnf->n * 4, cudaMemcpyDeviceToHost, e->stream));
+        ENG_CUDA(e, cudaFreeAsync(d_z, e->stream));
+        ENG_CUDA(e, cudaStreamSynchronize(e->stream));
+    }
+    return GALOIS_OK;
+}
+
+static int local_member(galois_engine *e, int64_t global_b, int32_t *lb)
+{
+    if (global_b < e->b0 || global_b >= e->b0 + e->b_loc)
+        return fail(GALOIS_E_ARG, "member is not local to this rank");
+    *lb = (int32_t)(global_b - e->b0);
+    return GALOIS_OK;
+}
+
+extern "C" int galois_candidate_pool(galois_engine *e, int64_t global_b, int32_t N, double rho, uint64_t pool_seed,
+                                     uint8_t *values, float *confidence, int32_t *units, int32_t *S_out)
+{
+    ENGINE_ENTRY(e);
+    if (N < 1 || !(rho > 0.0 && rho <= 1.0)) return fail(GALOIS_E_ARG, "need N >= 1 and 0 < rho <= 1");
+    if (int rc = prepare(e)) return rc;
+    int32_t lb = 0;
+    if (int rc = local_member(e, global_b, &lb)) return rc;
+    const int32_t n = e->cnf->n;
+    const int32_t S = std::max<int32_t>(1, (int32_t)std::ceil(rho * (double)n - 1e-9));
+    if (S > launch::max_sorted()) return fail(GALOIS_E_ARG, "|S| exceeds 4096");
+    if ((int64_t)N * n > (int64_t(1) << 31)) return fail(GALOIS_E_ARG, "N * n too large");
+    if (S_out) *S_out = S;
+    ENG_CUDA(e, cudaStreamSynchronize(e->stream));
+    float *d_z = nullptr, *d_c = nullptr;
+    uint8_t *d_x = nullptr;
+    int32_t *d_u = nullptr;
+    if (int rc = tmp_alloc(e, &d_z, (size_t)n)) return rc;
+    if (int rc = tmp_alloc(e, &d_c, (size_t)N * n)) return rc;
+    if (int rc = tmp_alloc(e, &d_x, (size_t)N * n)) return rc;
+    if (int rc = tmp_alloc(e, &d_u, (size_t)N * S)) return rc;
+    launch::gather_z(e->z, n, e->b_pad, lb, d_z, e->stream);
+    launch::pool(d_z, n, N, (float)(1.0 / e->tau), pool_seed, d_x, d_c, e->stream);
+    if (units) launch::topk(d_x, d_c, n, N, S, d_u, e->stream);
+    ENG_CUDA(e, cudaGetLastError());
+    if (values) ENG_CUDA(e, cudaMemcpyAsync(values, d_x, (size_t)N * n, cudaMemcpyDeviceToHost, e->stream));
+    if (confidence) ENG_CUDA(e, cudaMemcpyAsync(confidence, d_c, (size_t)N * n * 4, cudaMemcpyDeviceToHost, e->stream));
+    if (units) ENG_CUDA(e, cudaMemcpyAsync(units, d_u, (size_t)N * S * 4, cudaMemcpyDeviceToHost, e->stream));
+    for (void *p : {(void *)d_z, (void *)d_c, (void *)d_x, (void *)d_u}) ENG_CUDA(e, cudaFreeAsync(p, e->stream));
+    ENG_CUDA(e, cudaStreamSynchronize(e->stream));
+    return GALOIS_OK;
+}
+
+extern "C" int galois_cube_variables(galois_engine *e, int64_t global_b, int32_t d, int32_t *vars)
+{
+    ENGINE_ENTRY(e);
+    if (!vars) return fail(GALOIS_E_ARG, "vars is NULL");
+    if (int rc = prepare(e)) return rc;
+    const int32_t n = e->cnf->n;
+    if (d < 1 || d > n || d > launch::max_sorted()) return fail(GALOIS_E_ARG, "need 1 <= d <= min(n, 4096)");
+    int32_t lb = 0;
+    if (int rc = local_member(e, global_b, &lb)) return rc;
+    ENG_CUDA(e, cudaStreamSynchronize(e->stream));
+    float *d_z = nullptr;
+    int32_t *d_v = nullptr;
+    if (int rc = tmp_alloc(e, &d_z, (size_t)n)) return rc;
+    if (int rc = tmp_alloc(e, &d_v, (size_t)d)) return rc;
+    launch::gather_z(e->z, n, e->b_pad, lb, d_z, e->stream);
+    launch::lowconf(d_z, n, d, d_v, e->stream);
+    ENG_CUDA(e, cudaGetLastError());
+    ENG_CUDA(e, cudaMemcpyAsync(vars, d_v, (size_t)d * 4, cudaMemcpyDeviceToHost, e->stream));
+    ENG_CUDA(e, cudaFreeAsync(d_z, e->stream));
+    ENG_CUDA(e, cudaFreeAsync(d_v, e->stream));
+    ENG_CUDA(e, cudaStreamSynchronize(e->stream));
     return GALOIS_OK;
 }
 

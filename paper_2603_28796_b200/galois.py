@@ -36,7 +36,7 @@ EXPORTED = (
     "galois_engine_set_stream", "galois_engine_set_debug", "galois_engine_set_profiling",
     "galois_comm_unique_id", "galois_engine_get_iterate", "galois_engine_set_iterate",
     "galois_engine_get_grad", "galois_engine_get_loss", "galois_engine_get_bits",
-    "galois_engine_kernel_times",
+    "galois_engine_kernel_times", "galois_select_member", "galois_candidate_pool", "galois_cube_variables",
 )
 
 
@@ -87,6 +87,9 @@ def lib() -> ctypes.CDLL:
             "galois_engine_get_loss": [P, P],
             "galois_engine_get_bits": [P, P, P],
             "galois_engine_kernel_times": [P, P, P],
+            "galois_select_member": [P, I32, P, P, P],
+            "galois_candidate_pool": [P, I64, I32, F, U64, P, P, P, P],
+            "galois_cube_variables": [P, I64, I32, P],
         }
         for name, args in sig.items():
             fn = getattr(L, name)
@@ -281,6 +284,32 @@ class Engine:
         x = np.zeros((nb, self.n), np.uint8); r = np.zeros((nb, self.n), np.uint8)
         _check(lib().galois_engine_get_bits(self.handle, _p(x), _p(r)))
         return x, r
+
+    # -- what the CPU stage consumes (f1, f3)
+    def select_member(self, rule: int = 0):
+        """theta_sel: rule 0 = min loss, 1 = max loss at the last check."""
+        b, u = ctypes.c_int64(), ctypes.c_int32()
+        z = np.zeros(self.n, np.float32)
+        _check(lib().galois_select_member(self.handle, int(rule), ctypes.byref(b), ctypes.byref(u), _p(z)))
+        return dict(global_b=b.value, unsat=u.value, z=z)
+
+    def candidate_pool(self, global_b: int, N: int = 100, rho: float = 0.0005, pool_seed: int = 0):
+        """Eq.10-11: N samples of member global_b, their confidences and top-|S| unit literals."""
+        n = self.n
+        S = max(1, int(np.ceil(rho * n - 1e-9)))
+        x = np.zeros((N, n), np.uint8); c = np.zeros((N, n), np.float32); u = np.zeros((N, S), np.int32)
+        s_out = ctypes.c_int32()
+        _check(lib().galois_candidate_pool(self.handle, int(global_b), int(N), float(rho),
+                                           int(pool_seed) & (2 ** 64 - 1), _p(x), _p(c), _p(u),
+                                           ctypes.byref(s_out)))
+        assert s_out.value == S
+        return dict(values=x, confidence=c, units=u, S=S)
+
+    def cube_variables(self, global_b: int, d: int):
+        """Lemma 1 branching: the d least confident variables (1-based, ascending)."""
+        out = np.zeros(d, np.int32)
+        _check(lib().galois_cube_variables(self.handle, int(global_b), int(d), _p(out)))
+        return out
 
     def kernel_times(self):
         ms = np.zeros(NUM_KERNEL_CLASSES, np.float64)

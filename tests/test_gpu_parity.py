@@ -181,6 +181,48 @@ def test_nccl_path_single_rank(G, batch):
     assert outs[0] == outs[1]
 
 
+@pytest.mark.parametrize("batch,n", [(96, 300), (2048, 5000)])
+def test_selection_pool_and_cubes(G, batch, n):
+    """NEXT f1/f3: theta_sel (min and max loss), the candidate pool (Eq.10), the top-|S|
+    unit literals (Eq.11) and the lowest-confidence cube variables (Lemma 1) against the
+    oracle on the engine's own logits. Integer decisions taken in floating point (the
+    sample bit, the |S|-th confidence, |z| order) may differ only inside the fp32 tie zone."""
+    inst = I.industrial(n, 4 * n, 31)
+    cnf = G.Cnf.from_instance(inst)
+    eng = G.Engine(cnf, batch, 12, 0.5, 5)
+    eng.run()
+    counts, b0 = eng.unsat_counts()
+    z_all = eng.get_iterate()[0]
+    for rule in (0, 1):
+        sel = eng.select_member(rule)
+        assert (sel["global_b"], sel["unsat"]) == O.select_member(counts, b0, rule)
+        np.testing.assert_array_equal(sel["z"], z_all[sel["global_b"] - b0])
+    b = eng.select_member(1)["global_b"]
+    z = z_all[b - b0].astype(np.float64)
+    N, rho = 24, 0.01
+    pool = eng.candidate_pool(b, N, rho, pool_seed=77)
+    xo, co = O.pool(z, N, 1.0, 77)
+    ell_zone = np.abs(np.log(co / (1 - co)))          # |a| of the oracle's decision
+    diff = pool["values"] != xo
+    assert not (diff & (ell_zone > 1e-5 * (1 + np.abs(z)))).any()
+    np.testing.assert_allclose(pool["confidence"], co, rtol=2e-6, atol=0)
+    S = pool["S"]
+    for k in range(N):
+        gpu_units = list(pool["units"][k])
+        ora_units = O.top_confident_units(xo[k], co[k], rho)
+        assert len(gpu_units) == S == len(ora_units)
+        if gpu_units != ora_units:
+            # only near-equal confidences at the |S|-th place may swap
+            thr = np.sort(co[k])[::-1][S - 1]
+            for u in set(gpu_units) ^ set(ora_units):
+                assert abs(co[k][abs(u) - 1] - thr) < 1e-6
+    for d in (1, 7, 16):
+        vars_ = eng.cube_variables(b, d)
+        assert list(vars_) == O.lowest_confidence_vars(z, d)     # same fp32 z on both sides: exact
+    eng.free()
+    cnf.free()
+
+
 def test_cubes(G):
     """Lemma 1 cube pins: pinned variables follow alpha = b mod 2^d, never move, and the
     engine matches the oracle with pins."""

@@ -507,3 +507,43 @@ def test_planted_instances_are_satisfied_by_their_model():
     for inst in (I.random_ksat(60, 250, 3, 1, planted=True), I.industrial(300, 1200, 2, planted=True)):
         f = O.Cnf(inst.n, inst.offsets, inst.lits)
         assert O.unsat_count(f, inst.planted) == 0
+
+
+# --------------------------------------------- f1 / f3: pool, partial assignments, cubes
+def test_extract_partial_spec_example():
+    """SPEC extract_partial: top-|S| by descending confidence, Eq.11 literals."""
+    g = golden("spec_pool_examples.json")
+    assert O.top_confident_units(g["x"], g["conf"], g["rho"]) == g["units"]
+    assert len(O.top_confident_units([1] * 100, [0.7] * 100, 0.0005)) == 1      # |S| floors at 1 (S:312)
+    assert O.top_confident_units([1, 0, 1], [0.8, 0.8, 0.8], 1.0) == [1, -2, 3]   # ties -> lower index
+
+
+def test_branch_vars_spec_example():
+    """SPEC select_branch_vars: lowest noise-free confidence, ties lower index."""
+    g = golden("spec_pool_examples.json")
+    th = np.array(g["theta"], dtype=np.float64)
+    assert O.lowest_confidence_vars(th[:, 1] - th[:, 0], g["d"]) == g["vars"]
+    assert O.lowest_confidence_vars(np.zeros(6), 3) == [1, 2, 3]                   # all equal -> first d
+
+
+def test_pool_statistics_and_saturation():
+    """Eq.10: with z = 0 the samples are fair coins and the confidence
+    sigma(|ell|) = max(U, 1-U) for U uniform has mean 3/4 (closed form); with z = +20
+    every candidate is all-true with confidence ~1; pools are deterministic."""
+    x, c = O.pool(np.zeros(500), 40, 1.0, 17)
+    assert abs(x.mean() - 0.5) < 0.01 and abs(c.mean() - 0.75) < 0.005
+    assert (c >= 0.5).all() and (c <= 1.0).all()
+    x2, c2 = O.pool(np.zeros(500), 40, 1.0, 17)
+    np.testing.assert_array_equal(x, x2)
+    x3, _ = O.pool(np.zeros(500), 40, 1.0, 18)
+    assert (x3 != x).any()
+    xs, cs = O.pool(np.full(300, 20.0), 10, 1.0, 3)
+    # |ell| <= ln(2^24) = 16.6 with 23-bit uniforms, so a >= 3.4: all true, confidence ~1
+    assert xs.all() and (cs > 0.96).all() and cs.mean() > 0.9999
+
+
+def test_select_member_rules():
+    """theta_sel: min loss and max loss, ties to the lower member."""
+    counts = np.array([5, 2, 7, 2, 7])
+    assert O.select_member(counts, 100, 0) == (101, 2)
+    assert O.select_member(counts, 100, 1) == (102, 7)
