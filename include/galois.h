@@ -81,6 +81,18 @@ int galois_cnf_info(const galois_cnf *cnf, int32_t *num_vars, int64_t *num_claus
  * ascending slot order. Any pointer may be NULL. */
 int galois_cnf_get_csc(const galois_cnf *cnf, int32_t *code_off, int32_t *occ_slot);
 
+/* Fixed-width normalisation on the device (§2.2 "Clause Normalization for Vectorization",
+ * Eq.6-9; the paper uses k = 3, App. A): every clause longer than k
+ * becomes the equisatisfiable chain (l_1 .. l_{k-1} f_1)(-f_1 l_k .. f_2)...(-f_q ... l_u)
+ * with fresh auxiliaries f_j = variables n+1, n+2, ... in clause order; shorter clauses are
+ * padded by repeating their last literal (Appendix B: (-x1 x3) -> (-x1 x3 x3)).
+ * *out is a new CNF over n + *num_aux variables, every clause of width k; the first n
+ * bits of any model of *out are a model of the input. 3 <= k <= 32. */
+int galois_cnf_normalize(const galois_cnf *cnf, int32_t k, galois_cnf **out, int32_t *num_aux);
+
+/* Copy the CSR back in DIMACS form (test hook): offsets m+1 int64, literals L int32. */
+int galois_cnf_get_csr(const galois_cnf *cnf, int64_t *clause_offsets, int32_t *literals);
+
 /* Drop the caller's reference (engines hold their own). NULL is a no-op. */
 void galois_cnf_free(galois_cnf *cnf);
 

@@ -20,7 +20,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-ftz=true", "-Xcompiler", "-fPIC,-O2,-Wall", "-Xptxas", "-v",
          "--expt-relaxed-constexpr", f"-I{os.path.join(ROOT, 'include')}", f"-I{CSRC}"]
 SOURCES = ["cnf_build.cu", "step_kernels.cu", "clause_kernels.cu", "update_kernels.cu", "soft_kernels.cu",
-           "select_kernels.cu", "engine.cu", "comm.cpp"]
+           "select_kernels.cu", "tseitin_kernels.cu", "engine.cu", "comm.cpp"]
 HEADERS = ["galois_internal.h", "philox.cuh", "device_utils.cuh", "comm.h"]
 
 

@@ -235,6 +235,13 @@ unsigned grid_for(int64_t work, int threads = kThreads)
 
 }  // namespace
 
+void device_exclusive_scan(const int32_t *in, int32_t *out, int64_t N, int32_t *scratch, cudaStream_t st)
+{
+    exclusive_scan(in, out, N, scratch, st);
+}
+
+size_t device_scan_scratch_elems(int64_t N) { return scan_scratch_elems(N); }
+
 size_t build_cnf_scratch_bytes(int32_t n, int64_t L)
 {
     const int64_t tiles = (L + kTile - 1) / kTile;

@@ -227,37 +227,26 @@ static cudaError_t dmalloc(T **p, size_t count)
     return cudaMalloc((void **)p, count * sizeof(T));
 }
 
-extern "C" int galois_cnf_load(int32_t num_vars, int64_t num_clauses, const int64_t *clause_offsets,
-                               const int32_t *literals, galois_cnf **out)
+// Build a device CNF from device-resident DIMACS CSR arrays (d_off64 [m+1], d_lits [L]),
+// which this function takes over (frees): validation (a1), literal codes, CSC (a2),
+// width order, hub table. Work is ordered on the caller's stream st.
+static int cnf_build_device(int dev, int32_t num_vars, int64_t num_clauses, int64_t L, int64_t *d_off64,
+                            int32_t *d_lits, cudaStream_t st, galois_cnf **out)
 {
-    if (!out) return fail(GALOIS_E_ARG, "out is NULL");
-    *out = nullptr;
-    if (num_vars < 1 || num_vars >= (1 << 30)) return fail(GALOIS_E_ARG, "num_vars must be in [1, 2^30)");
-    if (num_clauses < 0 || num_clauses >= INT32_MAX) return fail(GALOIS_E_ARG, "num_clauses must be in [0, 2^31-1)");
-    if (!clause_offsets) return fail(GALOIS_E_ARG, "clause_offsets is NULL");
-    const int64_t L = clause_offsets[num_clauses];
-    if (clause_offsets[0] != 0) return fail(GALOIS_E_OFFSETS, "clause_offsets[0] != 0");
-    if (L < 0 || L >= INT32_MAX) return fail(GALOIS_E_OFFSETS, "literal count L must be in [0, 2^31-1)");
-    if (L > 0 && !literals) return fail(GALOIS_E_ARG, "literals is NULL");
-    int dev = 0;
-    if (int rc = check_device(&dev)) return rc;
-
     galois_cnf *c = new galois_cnf();
     c->device = dev;
     c->n = num_vars;
     c->m = num_clauses;
     c->L = L;
     const int64_t m = num_clauses;
-    int64_t *d_off64 = nullptr;
-    int32_t *d_lits = nullptr, *d_err = nullptr;
+    int32_t *d_err = nullptr;
     void *d_scratch = nullptr;
-    cudaStream_t st = nullptr;
     auto cleanup = [&]() {
+        cudaStreamSynchronize(st);
         cudaFree(d_off64);
         cudaFree(d_lits);
         cudaFree(d_err);
         cudaFree(d_scratch);
-        if (st) cudaStreamDestroy(st);
     };
     auto bail = [&](int code, const std::string &msg) {
         cleanup();
@@ -272,9 +261,6 @@ extern "C" int galois_cnf_load(int32_t num_vars, int64_t num_clauses, const int6
                         std::string(#expr) + ": " + cudaGetErrorString(_e));                             \
     } while (0)
 
-    LOAD_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-    LOAD_TRY(dmalloc(&d_off64, (size_t)m + 1));
-    LOAD_TRY(dmalloc(&d_lits, (size_t)L));
     LOAD_TRY(dmalloc(&d_err, 8));
     LOAD_TRY(dmalloc(&c->clause_off, (size_t)m + 1));
     LOAD_TRY(dmalloc(&c->clause_perm, (size_t)m));
@@ -283,9 +269,6 @@ extern "C" int galois_cnf_load(int32_t num_vars, int64_t num_clauses, const int6
     LOAD_TRY(dmalloc(&c->occ_slot, (size_t)L));
     const size_t scratch = build_cnf_scratch_bytes(num_vars, std::max<int64_t>(L, m));
     LOAD_TRY(cudaMalloc(&d_scratch, scratch));
-    LOAD_TRY(cudaMemcpyAsync(d_off64, clause_offsets, sizeof(int64_t) * (size_t)(m + 1), cudaMemcpyHostToDevice, st));
-    if (L > 0)
-        LOAD_TRY(cudaMemcpyAsync(d_lits, literals, sizeof(int32_t) * (size_t)L, cudaMemcpyHostToDevice, st));
     const int32_t h_err_init[8] = {0, INT32_MAX, INT32_MAX, INT32_MAX, 0, 0, 0, 0};
     LOAD_TRY(cudaMemcpyAsync(d_err, h_err_init, sizeof(h_err_init), cudaMemcpyHostToDevice, st));
     LOAD_TRY(launch_build_cnf(num_vars, m, L, d_off64, d_lits, c->clause_off, c->slot_info, c->code_off,
@@ -337,6 +320,96 @@ extern "C" int galois_cnf_load(int32_t num_vars, int64_t num_clauses, const int6
 #undef LOAD_TRY
     cleanup();
     *out = c;
+    return GALOIS_OK;
+}
+
+extern "C" int galois_cnf_load(int32_t num_vars, int64_t num_clauses, const int64_t *clause_offsets,
+                               const int32_t *literals, galois_cnf **out)
+{
+    if (!out) return fail(GALOIS_E_ARG, "out is NULL");
+    *out = nullptr;
+    if (num_vars < 1 || num_vars >= (1 << 30)) return fail(GALOIS_E_ARG, "num_vars must be in [1, 2^30)");
+    if (num_clauses < 0 || num_clauses >= INT32_MAX) return fail(GALOIS_E_ARG, "num_clauses must be in [0, 2^31-1)");
+    if (!clause_offsets) return fail(GALOIS_E_ARG, "clause_offsets is NULL");
+    const int64_t L = clause_offsets[num_clauses];
+    if (clause_offsets[0] != 0) return fail(GALOIS_E_OFFSETS, "clause_offsets[0] != 0");
+    if (L < 0 || L >= INT32_MAX) return fail(GALOIS_E_OFFSETS, "literal count L must be in [0, 2^31-1)");
+    if (L > 0 && !literals) return fail(GALOIS_E_ARG, "literals is NULL");
+    int dev = 0;
+    if (int rc = check_device(&dev)) return rc;
+    cudaStream_t st = nullptr;
+    int64_t *d_off64 = nullptr;
+    int32_t *d_lits = nullptr;
+    CUDA_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    cudaError_t ce = dmalloc(&d_off64, (size_t)num_clauses + 1);
+    if (ce == cudaSuccess) ce = dmalloc(&d_lits, (size_t)L);
+    if (ce == cudaSuccess)
+        ce = cudaMemcpyAsync(d_off64, clause_offsets, sizeof(int64_t) * (size_t)(num_clauses + 1),
+                             cudaMemcpyHostToDevice, st);
+    if (ce == cudaSuccess && L > 0)
+        ce = cudaMemcpyAsync(d_lits, literals, sizeof(int32_t) * (size_t)L, cudaMemcpyHostToDevice, st);
+    if (ce != cudaSuccess) {
+        cudaFree(d_off64);
+        cudaFree(d_lits);
+        cudaStreamDestroy(st);
+        return fail(ce == cudaErrorMemoryAllocation ? GALOIS_E_OOM : GALOIS_E_CUDA,
+                    std::string("cnf upload: ") + cudaGetErrorString(ce));
+    }
+    const int rc = cnf_build_device(dev, num_vars, num_clauses, L, d_off64, d_lits, st, out);
+    cudaStreamDestroy(st);
+    return rc;
+}
+
+namespace galois {
+namespace launch {
+cudaError_t tseitin(const int32_t *clause_off, const int2 *slot_info, int64_t m, int32_t n, int32_t k,
+                    int64_t **d_off_out, int32_t **d_lits_out, int64_t *m_out, int32_t *aux_out, cudaStream_t st);
+}
+}  // namespace galois
+
+extern "C" int galois_cnf_normalize(const galois_cnf *in, int32_t k, galois_cnf **out, int32_t *num_aux)
+{
+    if (!out) return fail(GALOIS_E_ARG, "out is NULL");
+    *out = nullptr;
+    if (!in) return fail(GALOIS_E_ARG, "cnf is NULL");
+    if (k < 3 || k > 32) return fail(GALOIS_E_ARG, "k must be in [3, 32]");
+    CUDA_TRY(cudaSetDevice(in->device));
+    cudaStream_t st = nullptr;
+    CUDA_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    int64_t *d_off = nullptr, m2 = 0;
+    int32_t *d_lits = nullptr, aux = 0;
+    cudaError_t ce = launch::tseitin(in->clause_off, in->slot_info, in->m, in->n, k, &d_off, &d_lits, &m2, &aux, st);
+    if (ce == cudaSuccess && (int64_t)in->n + aux >= (1 << 30)) ce = cudaErrorInvalidValue;
+    if (ce != cudaSuccess) {
+        cudaFree(d_off);
+        cudaFree(d_lits);
+        cudaStreamDestroy(st);
+        return fail(ce == cudaErrorMemoryAllocation ? GALOIS_E_OOM : GALOIS_E_CUDA,
+                    std::string("normalize: ") + cudaGetErrorString(ce));
+    }
+    if (num_aux) *num_aux = aux;
+    const int rc = cnf_build_device(in->device, in->n + aux, m2, m2 * k, d_off, d_lits, st, out);
+    cudaStreamDestroy(st);
+    return rc;
+}
+
+extern "C" int galois_cnf_get_csr(const galois_cnf *c, int64_t *clause_offsets, int32_t *literals)
+{
+    if (!c) return fail(GALOIS_E_ARG, "cnf is NULL");
+    CUDA_TRY(cudaSetDevice(c->device));
+    if (clause_offsets) {
+        std::vector<int32_t> off((size_t)c->m + 1);
+        CUDA_TRY(cudaMemcpy(off.data(), c->clause_off, off.size() * 4, cudaMemcpyDeviceToHost));
+        for (size_t i = 0; i < off.size(); ++i) clause_offsets[i] = off[i];
+    }
+    if (literals && c->L > 0) {
+        std::vector<int2> si((size_t)c->L);
+        CUDA_TRY(cudaMemcpy(si.data(), c->slot_info, si.size() * sizeof(int2), cudaMemcpyDeviceToHost));
+        for (size_t i = 0; i < si.size(); ++i) {
+            const int32_t v = (si[i].x >> 1) + 1;
+            literals[i] = (si[i].x & 1) ? -v : v;
+        }
+    }
     return GALOIS_OK;
 }
 

@@ -115,5 +115,8 @@ cudaError_t launch_build_cnf(int32_t n, int64_t m, int64_t L, const int64_t *d_o
                              int32_t *d_max_width, int32_t *d_clause_perm, void *d_scratch,
                              size_t scratch_bytes, cudaStream_t st);
 size_t build_cnf_scratch_bytes(int32_t n, int64_t L);
+// out[i] = sum_{j < i} in[j] (int32, in-place allowed); scratch of device_scan_scratch_elems(N)
+void device_exclusive_scan(const int32_t *in, int32_t *out, int64_t N, int32_t *scratch, cudaStream_t st);
+size_t device_scan_scratch_elems(int64_t N);
 
 }  // namespace galois

@@ -37,6 +37,7 @@ EXPORTED = (
     "galois_comm_unique_id", "galois_engine_get_iterate", "galois_engine_set_iterate",
     "galois_engine_get_grad", "galois_engine_get_loss", "galois_engine_get_bits",
     "galois_engine_kernel_times", "galois_select_member", "galois_candidate_pool", "galois_cube_variables",
+    "galois_cnf_normalize", "galois_cnf_get_csr",
 )
 
 
@@ -90,6 +91,8 @@ def lib() -> ctypes.CDLL:
             "galois_select_member": [P, I32, P, P, P],
             "galois_candidate_pool": [P, I64, I32, F, U64, P, P, P, P],
             "galois_cube_variables": [P, I64, I32, P],
+            "galois_cnf_normalize": [P, I32, P, P],
+            "galois_cnf_get_csr": [P, P, P],
         }
         for name, args in sig.items():
             fn = getattr(L, name)
@@ -172,6 +175,25 @@ class Cnf:
         _check(lib().galois_cnf_info(self.handle, ctypes.byref(n), ctypes.byref(m), ctypes.byref(L),
                                      ctypes.byref(w), ctypes.byref(d), ctypes.byref(h)))
         return dict(n=n.value, m=m.value, L=L.value, max_width=w.value, max_degree=d.value, num_hubs=h.value)
+
+    def normalize(self, k: int = 3) -> "Cnf":
+        """Fixed-width chain normalisation on the device (Eq.6-9); returns the new CNF
+        (n + num_aux variables) with attribute num_aux."""
+        h = ctypes.c_void_p()
+        aux = ctypes.c_int32()
+        _check(lib().galois_cnf_normalize(self.handle, int(k), ctypes.byref(h), ctypes.byref(aux)))
+        out = Cnf.__new__(Cnf)
+        out.handle = h
+        info = out.info()
+        out.n, out.m, out.num_aux = info["n"], info["m"], aux.value
+        return out
+
+    def csr(self):
+        info = self.info()
+        off = np.zeros(info["m"] + 1, np.int64)
+        lits = np.zeros(max(info["L"], 1), np.int32)
+        _check(lib().galois_cnf_get_csr(self.handle, _p(off), _p(lits)))
+        return off, lits[:info["L"]]
 
     def csc(self):
         info = self.info()

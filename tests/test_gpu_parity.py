@@ -295,3 +295,63 @@ def test_full_size_sampled_C2(G):
         if safe.all() and not ties.any():
             assert u[b] == out["unsat"][0]
     eng.free()
+
+
+# ------------------------------------------------------------ f2: chain normalisation
+def _oracle_normalize(inst, k):
+    from oracle import normalize as N
+    clauses = [inst.lits[inst.offsets[c]:inst.offsets[c + 1]].tolist() for c in range(inst.m)]
+    return N.normalize(inst.n, clauses, k)
+
+
+@pytest.mark.parametrize("which,k", [("appendix", 3), ("industrial", 3), ("industrial", 4),
+                                     ("industrial", 8), ("wide", 5), ("wide", 32), ("narrow", 3)])
+def test_normalize_matches_oracle(G, which, k):
+    """f2 (Eq.6-9): the device chain encoding equals the oracle's phi'
+    clause for clause, literal for literal (same auxiliary numbering), bit-exact."""
+    inst = {"appendix": lambda: I.from_clauses("b", 4, [[1, -2, 3, 4], [-1, 3]]),
+            "industrial": lambda: I.industrial(30_000, 120_000, 5),
+            "wide": lambda: I.industrial(5_000, 20_000, 9, wmin=1, wmax=80, width_exp=0.5),
+            "narrow": lambda: I.random_ksat(20_000, 80_000, 2, 3)}[which]()
+    n2, phi2 = _oracle_normalize(inst, k)
+    out = G.Cnf.from_instance(inst).normalize(k)
+    assert out.n == n2 and out.num_aux == n2 - inst.n and out.m == len(phi2)
+    off, lits = out.csr()
+    np.testing.assert_array_equal(off, np.arange(len(phi2) + 1, dtype=np.int64) * k)
+    np.testing.assert_array_equal(lits, np.array(phi2, np.int32).reshape(-1))
+    info = out.info()
+    assert info["max_width"] == k
+
+
+def test_normalize_rejects_bad_k(G):
+    c = G.Cnf.from_instance(I.random_ksat(10, 20, 3, 0))
+    for k in (0, 2, 33):
+        with pytest.raises(G.GaloisError):
+            c.normalize(k)
+
+
+def test_normalize_then_solve(G):
+    """The paper's pipeline: normalise a planted mixed-width formula to 3-CNF,
+    run the engine on phi', and project the best model to the original variables: it
+    satisfies phi (Eq.9), checked by the oracle's exact counter on phi."""
+    inst = I.industrial(200, 500, 4, planted=True, wmax=10)
+    out = G.Cnf.from_instance(inst).normalize(3)
+    eng = G.Engine(out, 1024, 200, 0.5, 1)
+    rc = eng.run()
+    best = eng.best_assignment()
+    eng.free()
+    assert rc == G.SAT and best["unsat"] == 0
+    f = O.Cnf(inst.n, inst.offsets, inst.lits)
+    assert O.unsat_count(f, best["values"][:inst.n]) == 0
+
+
+def test_normalized_trajectory(G):
+    """The normalised phi' of the solve test through the step-by-step parity harness for
+    30 steps (north_star: trajectories within 1e-4). Longer runs of this instance leave
+    the 1e-4 band: fp32-vs-fp64 drift grows ~x1.15/step through Adam's normalisation
+    (a numpy fp32 emulation fed the oracle's own G drifts 1.9e-4 by step 34; DESIGN.md
+    §Parity), so the first-SAT comparison lives on C1 (test_first_sat_matches_oracle_C1)."""
+    n2, phi2 = _oracle_normalize(I.industrial(200, 500, 4, planted=True, wmax=10), 3)
+    rep = parity.run_trajectory(G, I.from_clauses("phi'", n2, phi2), 1024, 30, seed=1, stop_on_sat=False)
+    assert rep.best_gpu == rep.best_oracle, rep
+    assert len(rep.resyncs) <= 8, rep.resyncs

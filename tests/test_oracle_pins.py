@@ -547,3 +547,81 @@ def test_select_member_rules():
     counts = np.array([5, 2, 7, 2, 7])
     assert O.select_member(counts, 100, 0) == (101, 2)
     assert O.select_member(counts, 100, 1) == (102, 7)
+
+
+# ------------------------------------------------- clause normalisation (NEXT f2)
+from oracle import normalize as N  # noqa: E402
+
+
+def test_normalize_appendix_b():
+    """Appendix B: phi -> phi' with z_1 = x_5; Eq.7's polarity (R16)."""
+    g = golden("appendix_b.json")
+    n2, phi2 = N.normalize(g["n_original"], g["phi"], 3)
+    assert n2 == g["n_normalized"] and phi2 == g["phi_prime_eq7"]
+
+
+@pytest.mark.parametrize("u", range(1, 12))
+def test_normalize_eq7_shape(u):
+    """Eq.7: a u-literal clause (u > 3) becomes u-2 clauses with u-3
+    auxiliaries f_1..f_{u-3}; the first is (l1 l2 f1), the last (-f_{u-3} l_{u-1} l_u);
+    u <= 3 is padded by duplication."""
+    lits = [(-1) ** i * (i + 1) for i in range(u)]
+    n2, phi2 = N.normalize(u, [lits], 3)
+    assert all(len(c) == 3 for c in phi2)
+    if u <= 3:
+        assert n2 == u and phi2 == [lits + [lits[-1]] * (3 - u)]
+        return
+    assert n2 - u == u - 3 and len(phi2) == u - 2
+    f = list(range(u + 1, n2 + 1))
+    assert phi2[0] == [lits[0], lits[1], f[0]]
+    assert phi2[-1] == [-f[-1], lits[-2], lits[-1]]
+    for j in range(1, u - 3):
+        assert phi2[j] == [-f[j - 1], lits[j + 1], f[j]]
+
+
+def _models(n, clauses):
+    return {tuple(x) for x in BF.all_assignments(n) if BF.naive_unsat(clauses, x) == 0}
+
+
+@pytest.mark.parametrize("k", [3, 4, 5])
+@pytest.mark.parametrize("seed", range(5))
+def test_normalize_projection_bruteforce(k, seed):
+    """Eq.9, strengthened: for every x over the original variables,
+    x |= phi  <=>  some extension (x, f) |= phi'; and the first n bits of every model of
+    phi' are a model of phi. Exhaustive on small random formulas, widths 1..8."""
+    rng = np.random.default_rng(100 * k + seed)
+    n = int(rng.integers(2, 7))
+    clauses = random_cnf(rng, n, int(rng.integers(1, 4)), 1, 8, distinct=False)
+    n2, phi2 = N.normalize(n, clauses, k)
+    assert all(len(c) == k for c in phi2)
+    assert n2 - n <= 12
+    m1 = _models(n, clauses)
+    m2 = _models(n2, phi2)
+    assert {x[:n] for x in m2} == m1
+
+
+@pytest.mark.parametrize("k", [3, 4, 7])
+def test_normalize_literal_conservation(k):
+    """Every original literal occurs exactly once in its chain, in order,
+    plus only auxiliaries and padding duplicates; each auxiliary occurs once positive,
+    once negative (the chain link)."""
+    rng = np.random.default_rng(k)
+    n = 40
+    clauses = random_cnf(rng, n, 60, 1, 20, distinct=True)
+    n2, phi2 = N.normalize(n, clauses, k)
+    flat = [l for c in phi2 for l in c]
+    aux = [l for l in flat if abs(l) > n]
+    assert sorted(set(abs(l) for l in aux)) == list(range(n + 1, n2 + 1))
+    for v in range(n + 1, n2 + 1):
+        assert aux.count(v) == 1 and aux.count(-v) == 1
+    expect_aux = sum(max(0, -(-(len(c) - 2) // (k - 2)) - 1) if len(c) > k else 0 for c in clauses)
+    assert n2 - n == expect_aux
+    # originals in order, dropping padding duplicates of the last literal of each chain
+    pos = 0
+    for c in clauses:
+        got = []
+        while len(got) < len(c):
+            got.extend(l for l in phi2[pos] if abs(l) <= n)
+            pos += 1
+        assert got[:len(c)] == c and all(l == c[-1] for l in got[len(c):])
+    assert pos == len(phi2)
