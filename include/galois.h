@@ -171,6 +171,24 @@ int galois_engine_set_comm(galois_engine *eng, int32_t rank, int32_t world, cons
 /* Use the caller's CUDA stream (a cudaStream_t, e.g. torch.cuda.current_stream()). */
 int galois_engine_set_stream(galois_engine *eng, void *cuda_stream);
 
+/* Sub-batching for memory ("the batch is divided into sub-batches ... due to
+ * memory limits"). sub_batch = 0 (default) keeps every local member
+ * resident; a multiple of 32 smaller than the local slice makes the engine hold only
+ * sub_batch members in HBM and galois_engine_run process the slice in consecutive
+ * windows of sub_batch members, each run from t = 0 (members are independent: the
+ * straight-through loss is a sum over members and every member's RNG counters use its
+ * global index, so each member's trajectory is unchanged). A window after a SAT at step
+ * t* runs at most t* steps. The best record is the lexicographic (unsat, step, member)
+ * minimum over all windows — exactly the full-batch result; unsat_counts reports each
+ * member's last check, info the slice and the full batch's step count. Only run() drives a
+ * sub-batched engine (step/enqueue/set_iterate and the selection calls return E_STATE).
+ * With world > 1 every rank runs ceil(b_per / sub_batch) windows in lock step. */
+int galois_engine_set_subbatch(galois_engine *eng, int32_t sub_batch);
+
+/* Device bytes one member costs in the given mode (z, m, v, bit planes, E or soft
+ * buffers, counters), for sizing sub_batch to a memory budget. */
+int galois_engine_bytes_per_member(const galois_cnf *cnf, int32_t mode, int64_t *bytes);
+
 /* Test hook: also store the per-step clause signal G and gradient g1 (see get_grad). */
 int galois_engine_set_debug(galois_engine *eng, int32_t enable);
 

@@ -460,6 +460,17 @@ struct galois_engine {
     int32_t steps_enqueued = 0;
     int64_t b_per = 0, b0 = 0;
     int32_t b_loc = 0, b_pad = 0, W = 0;
+    // sub-batching (f4): `windows` consecutive windows of `sub` members over the local
+    // slice [slice_b0, slice_b0 + slice_loc); b0 / b_loc describe the resident window
+    int32_t sub = 0, windows = 1;
+    int64_t slice_b0 = 0, slice_loc = 0;
+    struct Agg {
+        int32_t u = INT32_MAX, t = -1, steps = 0;
+        int64_t b = -1;
+        bool sat = false, ran = false;
+    } agg;
+    std::vector<uint8_t> agg_bits;     // winner's rounding over all windows
+    std::vector<int32_t> agg_counts;   // each local member's last check
     Comm comm;
     // device buffers
     float *z = nullptr, *m = nullptr, *v = nullptr;
@@ -580,6 +591,11 @@ extern "C" int galois_engine_create(const galois_cnf *cnf, int64_t batch, int32_
         if ((e)->poisoned) return fail(GALOIS_E_STATE, "engine is poisoned by an earlier error"); \
     } while (0)
 
+#define WHOLE_SLICE_ONLY(e)                                                                                  \
+    do {                                                                                                     \
+        if ((e)->windows > 1) return fail(GALOIS_E_STATE, "not available on a sub-batched engine (run only)"); \
+    } while (0)
+
 #define SETTER_ENTRY(e)                                                                        \
     do {                                                                                       \
         ENGINE_ENTRY(e);                                                                       \
@@ -644,6 +660,28 @@ extern "C" int galois_engine_set_comm(galois_engine *e, int32_t rank, int32_t wo
     e->world = world;
     if (id) memcpy(e->nccl_id, id, 128);
     e->use_comm = world > 1 || id != nullptr;   // world = 1 with an id: the NCCL path on one GPU
+    return GALOIS_OK;
+}
+
+extern "C" int galois_engine_set_subbatch(galois_engine *e, int32_t sub_batch)
+{
+    SETTER_ENTRY(e);
+    if (sub_batch < 0 || sub_batch % 32 != 0) return fail(GALOIS_E_ARG, "sub_batch must be 0 or a positive multiple of 32");
+    e->sub = sub_batch;
+    return GALOIS_OK;
+}
+
+extern "C" int galois_engine_bytes_per_member(const galois_cnf *c, int32_t mode, int64_t *bytes)
+{
+    if (!c || !bytes) return fail(GALOIS_E_ARG, "cnf and bytes are required");
+    if (mode != GALOIS_MODE_ST && mode != GALOIS_MODE_SOFT) return fail(GALOIS_E_ARG, "mode must be 0 or 1");
+    // mirrors prepare(): z, m, v fp32 + X, R bits + unsat, unsat_last (+ mode buffers)
+    int64_t b = 12 * (int64_t)c->n + ((int64_t)c->n + 3) / 4 + 8;
+    if (mode == GALOIS_MODE_ST)
+        b += ((int64_t)c->L + 7) / 8 + 8 + 2 * (int64_t)c->num_hub_chunks;   // E bits, lam x 2, hub partials
+    else
+        b += 4 * (int64_t)c->n + 4 * (int64_t)c->L + 4 * (1 + launch::soft_chunks());   // P, Es, lam_f
+    *bytes = b;
     return GALOIS_OK;
 }
 
@@ -809,9 +847,18 @@ static int prepare(galois_engine *e)
     e->b0 = per * e->rank;
     const int64_t left = e->B - e->b0;
     e->b_loc = (int32_t)std::max<int64_t>(0, std::min<int64_t>(per, left));
+    e->slice_b0 = e->b0;
+    e->slice_loc = e->b_loc;
+    // f4: windows of sub members; with NCCL every rank runs the same number of windows
+    const int64_t span = e->use_comm ? e->b_per : e->slice_loc;
+    if (e->sub > 0 && e->sub < span) {
+        e->windows = (int32_t)((span + e->sub - 1) / e->sub);
+        e->b_loc = (int32_t)std::min<int64_t>(e->sub, e->slice_loc);
+    }
+    const int32_t resident = e->windows > 1 ? e->sub : e->b_loc;
     // pad to 32 members (one bit word) up to 1024, then to whole 1024-member chunks, so that
     // W <= 32 or W % 32 == 0 (chunk-major E, TMA-staged update)
-    e->b_pad = e->b_loc <= 1024 ? std::max<int32_t>(32, (e->b_loc + 31) / 32 * 32) : (e->b_loc + 1023) / 1024 * 1024;
+    e->b_pad = resident <= 1024 ? std::max<int32_t>(32, (resident + 31) / 32 * 32) : (resident + 1023) / 1024 * 1024;
     e->W = e->b_pad / 32;
     if ((uint64_t)n * (uint64_t)e->b_pad / 4 >= (1ull << 40))
         return poison(e, GALOIS_E_ARG, "n * local batch too large");
@@ -960,6 +1007,7 @@ extern "C" int galois_engine_step(galois_engine *e)
 {
     ENGINE_ENTRY(e);
     if (int rc = prepare(e)) return rc;
+    WHOLE_SLICE_ONLY(e);
     Ctrl h;
     if (int rc = read_ctrl(e, &h)) return rc;
     if (h.stopped) return GALOIS_SAT;
@@ -973,16 +1021,18 @@ extern "C" int galois_engine_enqueue(galois_engine *e, int32_t max_steps)
 {
     ENGINE_ENTRY(e);
     if (int rc = prepare(e)) return rc;
+    WHOLE_SLICE_ONLY(e);
     if (e->steps_enqueued >= e->T) return GALOIS_BUDGET;
     for (int32_t i = 0; i < max_steps && e->steps_enqueued < e->T; ++i)
         if (int rc = enqueue_step(e)) return rc;
     return GALOIS_OK;
 }
 
-extern "C" int galois_engine_run(galois_engine *e)
+static int run_windows(galois_engine *e);
+
+// Steps of the resident members until SAT or e->T (see galois_engine_run).
+static int run_steps(galois_engine *e)
 {
-    ENGINE_ENTRY(e);
-    if (int rc = prepare(e)) return rc;
     // chunks of G steps (G even and a multiple of K, so every chunk that starts at a
     // multiple of G has the same kernel sequence and Lambda parity): replayed as one CUDA
     // graph; the stop flag of chunk i-1 is polled while chunk i is queued
@@ -1016,11 +1066,99 @@ extern "C" int galois_engine_run(galois_engine *e)
     return h.stopped ? GALOIS_SAT : GALOIS_BUDGET;
 }
 
+extern "C" int galois_engine_run(galois_engine *e)
+{
+    ENGINE_ENTRY(e);
+    if (int rc = prepare(e)) return rc;
+    return e->windows > 1 ? run_windows(e) : run_steps(e);
+}
+
+// f4: put window w of the local slice into the resident buffers and initialise it at t = 0
+// (the same init, RNG counters and best record a full-batch engine gives those members).
+static int reseat(galois_engine *e, int32_t w)
+{
+    e->b0 = e->slice_b0 + (int64_t)w * e->sub;
+    e->b_loc = (int32_t)std::max<int64_t>(0, std::min<int64_t>(e->sub, e->slice_loc - (int64_t)w * e->sub));
+    if (e->graph) {                     // captured kernels carry b0 / b_loc in their parameters
+        ENG_CUDA(e, cudaGraphExecDestroy(e->graph));
+        e->graph = nullptr;
+    }
+    ENG_CUDA(e, cudaStreamSynchronize(e->stream));
+    Ctrl h{};
+    h.best_u = INT32_MAX;
+    h.best_t = -1;
+    h.best_b = -1;
+    e->h_ctrl[0] = h;
+    ENG_CUDA(e, cudaMemcpyAsync(e->ctrl, &e->h_ctrl[0], sizeof(Ctrl), cudaMemcpyHostToDevice, e->stream));
+    ENG_CUDA(e, cudaMemsetAsync(e->unsat, 0, sizeof(int32_t) * (size_t)e->b_pad, e->stream));
+    ENG_CUDA(e, cudaMemsetAsync(e->unsat_last, 0, sizeof(int32_t) * (size_t)e->b_pad, e->stream));
+    ENG_CUDA(e, cudaMemsetAsync(e->best_bits, 0, (size_t)e->cnf->n, e->stream));
+    if (e->lam) ENG_CUDA(e, cudaMemsetAsync(e->lam, 0, 2 * sizeof(int32_t) * (size_t)e->b_pad, e->stream));
+    e->steps_enqueued = 0;
+    const StepParams p = e->params();
+    e->timed(5, [&] { launch::init(p, e->z, e->m, e->v, e->X, e->R, e->stream); });
+    ENG_CUDA(e, cudaGetLastError());
+    ENG_CUDA(e, cudaStreamSynchronize(e->stream));   // h_ctrl[0] is reused by the polls
+    e->pending_check = true;
+    return GALOIS_OK;
+}
+
+// f4: every window runs from t = 0 (after a SAT at t*, at most t* steps); the best is the
+// lexicographic (u, t, b) minimum over the windows' records, the full-batch result.
+static int run_windows(galois_engine *e)
+{
+    if (e->agg.ran) return e->agg.sat ? GALOIS_SAT : GALOIS_BUDGET;
+    const int32_t T = e->T;
+    e->agg_bits.assign((size_t)e->cnf->n, 0);
+    e->agg_counts.assign((size_t)e->slice_loc, 0);
+    for (int32_t w = 0; w < e->windows; ++w) {
+        if (w > 0)
+            if (int rc = reseat(e, w)) return rc;
+        e->T = e->agg.sat ? e->agg.t : T;
+        const int rc = run_steps(e);
+        e->T = T;
+        if (rc != GALOIS_SAT && rc != GALOIS_BUDGET) return rc;
+        Ctrl h;
+        if (int r2 = read_ctrl(e, &h)) return r2;
+        const galois_engine::Agg &a = e->agg;
+        const bool better = h.best_b >= 0 &&
+                            (h.best_u != a.u ? h.best_u < a.u : h.best_t != a.t ? h.best_t < a.t : h.best_b < a.b);
+        if (better) {
+            if (e->use_comm) {
+                std::string why;
+                if (!e->comm.broadcast_bytes(e->best_bits, (size_t)e->cnf->n, (int)(h.best_b / e->b_per), e->stream,
+                                             &why))
+                    return poison(e, GALOIS_E_NCCL, why);
+            }
+            ENG_CUDA(e, cudaMemcpyAsync(e->agg_bits.data(), e->best_bits, (size_t)e->cnf->n, cudaMemcpyDeviceToHost,
+                                        e->stream));
+            e->agg.u = h.best_u;
+            e->agg.t = h.best_t;
+            e->agg.b = h.best_b;
+        }
+        if (e->b_loc > 0)
+            ENG_CUDA(e, cudaMemcpyAsync(e->agg_counts.data() + (size_t)w * e->sub, e->unsat_last,
+                                        sizeof(int32_t) * (size_t)e->b_loc, cudaMemcpyDeviceToHost, e->stream));
+        ENG_CUDA(e, cudaStreamSynchronize(e->stream));
+        e->agg.steps = std::max(e->agg.steps, h.t);
+        if (h.stopped) e->agg.sat = true;
+    }
+    e->agg.ran = true;
+    return e->agg.sat ? GALOIS_SAT : GALOIS_BUDGET;
+}
+
 extern "C" int galois_engine_info(galois_engine *e, int64_t *local_batch, int64_t *first_global_b,
                                   int32_t *steps_done, int32_t *stopped)
 {
     ENGINE_ENTRY(e);
     if (int rc = prepare(e)) return rc;
+    if (e->windows > 1) {
+        if (local_batch) *local_batch = e->slice_loc;
+        if (first_global_b) *first_global_b = e->slice_b0;
+        if (steps_done) *steps_done = e->agg.sat ? e->agg.t : e->agg.steps;   // what the full batch did
+        if (stopped) *stopped = e->agg.sat;
+        return GALOIS_OK;
+    }
     Ctrl h;
     if (int rc = settle(e, &h)) return rc;
     if (local_batch) *local_batch = e->b_loc;
@@ -1035,6 +1173,14 @@ extern "C" int galois_best_assignment(galois_engine *e, uint8_t *values, int32_t
 {
     ENGINE_ENTRY(e);
     if (int rc = prepare(e)) return rc;
+    if (e->windows > 1) {
+        if (values && e->agg.ran) memcpy(values, e->agg_bits.data(), (size_t)e->cnf->n);
+        else if (values) memset(values, 0, (size_t)e->cnf->n);
+        if (unsat) *unsat = e->agg.u;
+        if (global_b) *global_b = e->agg.b;
+        if (step) *step = e->agg.t;
+        return GALOIS_OK;
+    }
     Ctrl h;
     if (int rc = settle(e, &h)) return rc;
     if (e->use_comm && h.best_b >= 0) {
@@ -1055,6 +1201,12 @@ extern "C" int galois_unsat_counts(galois_engine *e, int32_t *counts, int64_t *f
 {
     ENGINE_ENTRY(e);
     if (int rc = prepare(e)) return rc;
+    if (e->windows > 1) {
+        if (counts && e->agg.ran) memcpy(counts, e->agg_counts.data(), sizeof(int32_t) * (size_t)e->slice_loc);
+        else if (counts) memset(counts, 0, sizeof(int32_t) * (size_t)e->slice_loc);
+        if (first_global_b) *first_global_b = e->slice_b0;
+        return GALOIS_OK;
+    }
     Ctrl h;
     if (int rc = settle(e, &h)) return rc;
     if (counts && e->b_loc > 0)
@@ -1092,6 +1244,7 @@ extern "C" int galois_select_member(galois_engine *e, int32_t rule, int64_t *glo
     ENGINE_ENTRY(e);
     if (rule != 0 && rule != 1) return fail(GALOIS_E_ARG, "rule must be 0 (min loss) or 1 (max loss)");
     if (int rc = prepare(e)) return rc;
+    WHOLE_SLICE_ONLY(e);
     Ctrl h;
     if (int rc = settle(e, &h)) return rc;
     if (e->b_loc == 0) return fail(GALOIS_E_STATE, "this rank has no members");
@@ -1131,6 +1284,7 @@ extern "C" int galois_candidate_pool(galois_engine *e, int64_t global_b, int32_t
     ENGINE_ENTRY(e);
     if (N < 1 || !(rho > 0.0 && rho <= 1.0)) return fail(GALOIS_E_ARG, "need N >= 1 and 0 < rho <= 1");
     if (int rc = prepare(e)) return rc;
+    WHOLE_SLICE_ONLY(e);
     int32_t lb = 0;
     if (int rc = local_member(e, global_b, &lb)) return rc;
     const int32_t n = e->cnf->n;
@@ -1163,6 +1317,7 @@ extern "C" int galois_cube_variables(galois_engine *e, int64_t global_b, int32_t
     ENGINE_ENTRY(e);
     if (!vars) return fail(GALOIS_E_ARG, "vars is NULL");
     if (int rc = prepare(e)) return rc;
+    WHOLE_SLICE_ONLY(e);
     const int32_t n = e->cnf->n;
     if (d < 1 || d > n || d > launch::max_sorted()) return fail(GALOIS_E_ARG, "need 1 <= d <= min(n, 4096)");
     int32_t lb = 0;
@@ -1186,6 +1341,7 @@ extern "C" int galois_engine_get_iterate(galois_engine *e, float *z, float *m, f
 {
     ENGINE_ENTRY(e);
     if (int rc = prepare(e)) return rc;
+    WHOLE_SLICE_ONLY(e);
     if (z) if (int rc = copy_transposed_out(e, e->z, z)) return rc;
     if (m) if (int rc = copy_transposed_out(e, e->m, m)) return rc;
     if (v) if (int rc = copy_transposed_out(e, e->v, v)) return rc;
@@ -1203,6 +1359,7 @@ extern "C" int galois_engine_set_iterate(galois_engine *e, const float *z, const
     if (!z || !m || !v) return fail(GALOIS_E_ARG, "z, m and v are required");
     if (t < 0 || t > e->T) return fail(GALOIS_E_ARG, "t must be in [0, steps]");
     if (int rc = prepare(e)) return rc;
+    WHOLE_SLICE_ONLY(e);
     const int32_t n = e->cnf->n;
     const float *src[3] = {z, m, v};
     float *dst[3] = {e->z, e->m, e->v};
@@ -1236,6 +1393,7 @@ extern "C" int galois_engine_get_grad(galois_engine *e, int32_t *G, float *g1)
     ENGINE_ENTRY(e);
     if (!e->debug) return fail(GALOIS_E_STATE, "get_grad needs set_debug(1) before the first step");
     if (int rc = prepare(e)) return rc;
+    WHOLE_SLICE_ONLY(e);
     if (G) {
         if (e->mode == GALOIS_MODE_ST) {
             if (int rc = copy_transposed_out(e, e->dbg_G, G)) return rc;
@@ -1254,6 +1412,7 @@ extern "C" int galois_engine_get_loss(galois_engine *e, float *lambda)
     ENGINE_ENTRY(e);
     if (!lambda) return fail(GALOIS_E_ARG, "lambda is NULL");
     if (int rc = prepare(e)) return rc;
+    WHOLE_SLICE_ONLY(e);
     if (e->mode == GALOIS_MODE_ST) {
         // Lambda of the last completed step t lives in lam[t & 1] (see enqueue_step)
         Ctrl h;
@@ -1274,6 +1433,7 @@ extern "C" int galois_engine_get_bits(galois_engine *e, uint8_t *x_next, uint8_t
 {
     ENGINE_ENTRY(e);
     if (int rc = prepare(e)) return rc;
+    WHOLE_SLICE_ONLY(e);
     const int32_t n = e->cnf->n;
     std::vector<uint32_t> tmp((size_t)n * e->W);
     uint8_t *outs[2] = {x_next, r};

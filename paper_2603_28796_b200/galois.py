@@ -37,7 +37,7 @@ EXPORTED = (
     "galois_comm_unique_id", "galois_engine_get_iterate", "galois_engine_set_iterate",
     "galois_engine_get_grad", "galois_engine_get_loss", "galois_engine_get_bits",
     "galois_engine_kernel_times", "galois_select_member", "galois_candidate_pool", "galois_cube_variables",
-    "galois_cnf_normalize", "galois_cnf_get_csr",
+    "galois_cnf_normalize", "galois_cnf_get_csr", "galois_engine_set_subbatch", "galois_engine_bytes_per_member",
 )
 
 
@@ -93,6 +93,8 @@ def lib() -> ctypes.CDLL:
             "galois_cube_variables": [P, I64, I32, P],
             "galois_cnf_normalize": [P, I32, P, P],
             "galois_cnf_get_csr": [P, P, P],
+            "galois_engine_set_subbatch": [P, I32],
+            "galois_engine_bytes_per_member": [P, I32, P],
         }
         for name, args in sig.items():
             fn = getattr(L, name)
@@ -188,6 +190,15 @@ class Cnf:
         out.n, out.m, out.num_aux = info["n"], info["m"], aux.value
         return out
 
+    def bytes_per_member(self, mode: int = 0) -> int:
+        out = ctypes.c_int64()
+        _check(lib().galois_engine_bytes_per_member(self.handle, int(mode), ctypes.byref(out)))
+        return out.value
+
+    def sub_batch_for(self, budget_bytes: int, mode: int = 0) -> int:
+        """Largest multiple of 32 members whose engine state fits budget_bytes (f4)."""
+        return max(32, int(budget_bytes // self.bytes_per_member(mode)) // 32 * 32)
+
     def csr(self):
         info = self.info()
         off = np.zeros(info["m"] + 1, np.int64)
@@ -221,7 +232,7 @@ class Engine:
                  mode: int = 0, tau: float = 1.0, beta1: float = 0.9, beta2: float = 0.999,
                  eps: float = 1e-8, optimizer: int = 0, check_interval: int = 1,
                  cubes: Sequence[int] = (), debug: bool = False, stream=None,
-                 rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None):
+                 rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None, sub_batch: int = 0):
         self.cnf = cnf
         self.n = cnf.n
         self.handle = galois_engine_create(cnf.handle, batch, steps, lr, seed)
@@ -239,6 +250,8 @@ class Engine:
             _check(L.galois_engine_set_debug(self.handle, 1))
         if stream is not None:
             _check(L.galois_engine_set_stream(self.handle, ctypes.c_void_p(int(stream))))
+        if sub_batch:
+            _check(L.galois_engine_set_subbatch(self.handle, int(sub_batch)))
         if world > 1 or nccl_id is not None:
             buf = ctypes.create_string_buffer(bytes(nccl_id), 128)
             _check(L.galois_engine_set_comm(self.handle, int(rank), int(world), buf))

@@ -355,3 +355,83 @@ def test_normalized_trajectory(G):
     rep = parity.run_trajectory(G, I.from_clauses("phi'", n2, phi2), 1024, 30, seed=1, stop_on_sat=False)
     assert rep.best_gpu == rep.best_oracle, rep
     assert len(rep.resyncs) <= 8, rep.resyncs
+
+
+# ------------------------------------------------------------------ f4: sub-batching
+def _solve(G, inst, batch, steps, seed, **kw):
+    cnf = G.Cnf.from_instance(inst)
+    eng = G.Engine(cnf, batch, steps, 0.5, seed, **kw)
+    rc = eng.run()
+    best = eng.best_assignment()
+    counts, b0 = eng.unsat_counts()
+    info = eng.info()
+    eng.free()
+    return rc, (best["unsat"], best["step"], best["global_b"]), best["values"], counts, info
+
+
+@pytest.mark.parametrize("K,sub", [(1, 1024), (4, 992), (3, 32)])
+def test_subbatch_equals_full_batch(G, K, sub):
+    """f4: windows of sub members give the full-batch result exactly — best
+    (u, t, b), its bits, every member's last count and the step count (no SAT here,
+    every window runs the whole budget; ragged last window)."""
+    inst = I.random_ksat(300, 1290, 3, 5)
+    B, T = 3000 if sub >= 512 else 200, 40
+    full = _solve(G, inst, B, T, 7, check_interval=K)
+    part = _solve(G, inst, B, T, 7, check_interval=K, sub_batch=sub)
+    assert full[0] == part[0] == G.BUDGET
+    assert full[1] == part[1]
+    np.testing.assert_array_equal(full[2], part[2])
+    np.testing.assert_array_equal(full[3], part[3])
+    assert full[4] == part[4]
+
+
+@pytest.mark.parametrize("sub", [256, 1024])
+def test_subbatch_first_sat(G, sub):
+    """SAT stop across windows: the first satisfying (step, member) of the full batch,
+    its bits and the step count (windows after the SAT run at most t* steps)."""
+    inst = I.random_ksat(50, 213, 3, 0)
+    full = _solve(G, inst, 4096, 100, 0)
+    part = _solve(G, inst, 4096, 100, 0, sub_batch=sub)
+    assert full[0] == part[0] == G.SAT
+    assert full[1] == part[1] and full[1][0] == 0
+    np.testing.assert_array_equal(full[2], part[2])
+    assert full[4]["steps_done"] == part[4]["steps_done"] and part[4]["stopped"]
+
+
+def test_subbatch_cubes_and_nccl(G):
+    """Windows keep global member indices: cube pins (alpha = b mod 2^d) and the NCCL
+    MIN path (1-rank communicator) give the unwindowed result."""
+    inst = I.random_ksat(200, 852, 3, 9)
+    pins = [3, 17, 40, 41, 99]
+    full = _solve(G, inst, 2048, 30, 2, cubes=pins)
+    part = _solve(G, inst, 2048, 30, 2, cubes=pins, sub_batch=640)
+    assert full[1] == part[1]
+    np.testing.assert_array_equal(full[3], part[3])
+    nid = G.galois_comm_unique_id()
+    comm = _solve(G, inst, 2048, 30, 2, cubes=pins, sub_batch=640, nccl_id=nid)
+    assert comm[1] == full[1]
+    np.testing.assert_array_equal(comm[2], full[2])
+
+
+def test_subbatch_gating_and_sizing(G):
+    import torch
+    inst = I.random_ksat(1000, 4200, 3, 1)
+    cnf = G.Cnf.from_instance(inst)
+    with pytest.raises(G.GaloisError):
+        G.Engine(cnf, 4096, 10, 0.5, 0, sub_batch=100)          # not a multiple of 32
+    eng = G.Engine(cnf, 4096, 10, 0.5, 0, sub_batch=1024)
+    with pytest.raises(G.GaloisError) as e:
+        eng.step()
+    assert e.value.code == G.E_STATE
+    eng.free()
+    per = cnf.bytes_per_member()
+    assert per >= 12 * inst.n + inst.lits.size // 8
+    assert cnf.sub_batch_for(per * 1000) == 992
+    # the resident footprint scales with sub_batch, not B
+    torch.cuda.synchronize()
+    free0 = torch.cuda.mem_get_info()[0]
+    big = G.Engine(cnf, 1 << 20, 1, 0.5, 0, sub_batch=2048)
+    big.info()
+    used = free0 - torch.cuda.mem_get_info()[0]
+    big.free()
+    assert used < 4 * per * 2048 + (64 << 20), used
