@@ -12,8 +12,10 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-OBJ = os.path.join(ROOT, "build", "obj")
-LIB = os.path.join(PKG, "libgalois.so")
+# developer knobs for A/B builds: extra nvcc flags, and a separate object dir / library path
+EXTRA = os.environ.get("GALOIS_NVCC_EXTRA", "").split()
+OBJ = os.environ.get("GALOIS_OBJ_DIR", os.path.join(ROOT, "build", "obj"))
+LIB = os.environ.get("GALOIS_LIB_OUT", os.path.join(PKG, "libgalois.so"))
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -36,7 +38,7 @@ def _stale(obj: str, src: str) -> bool:
 def _compile(src: str, verbose: bool) -> str:
     path = os.path.join(CSRC, src)
     obj = os.path.join(OBJ, src + ".o")
-    cmd = [NVCC, *ARCH, *FLAGS, "-c", path, "-o", obj]
+    cmd = [NVCC, *ARCH, *FLAGS, *EXTRA, "-c", path, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")

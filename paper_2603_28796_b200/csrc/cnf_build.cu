@@ -225,6 +225,30 @@ __global__ void k_slot_info(const uint32_t *__restrict__ codes, const int32_t *_
     }
 }
 
+__global__ void k_sweep_widths(int64_t m, const int32_t *__restrict__ clause_off, const int32_t *__restrict__ perm,
+                               int32_t *__restrict__ w)
+{
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c <= m; c += (int64_t)gridDim.x * blockDim.x) {
+        int32_t x = 0;
+        if (c < m) {
+            const int32_t cl = perm[c];
+            x = clause_off[cl + 1] - clause_off[cl];
+        }
+        w[c] = x;
+    }
+}
+
+__global__ void k_sweep_slots(int64_t m, const int32_t *__restrict__ clause_off, const int32_t *__restrict__ perm,
+                              const int2 *__restrict__ slot_info, const int32_t *__restrict__ sweep_off,
+                              int2 *__restrict__ sweep_slot)
+{
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < m; c += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t cl = perm[c];
+        const int32_t lo = clause_off[cl], w = clause_off[cl + 1] - lo, dst = sweep_off[c];
+        for (int32_t i = 0; i < w; ++i) sweep_slot[dst + i] = slot_info[lo + i];
+    }
+}
+
 unsigned grid_for(int64_t work, int threads = kThreads)
 {
     int64_t g = (work + threads - 1) / threads;
@@ -241,6 +265,18 @@ void device_exclusive_scan(const int32_t *in, int32_t *out, int64_t N, int32_t *
 }
 
 size_t device_scan_scratch_elems(int64_t N) { return scan_scratch_elems(N); }
+
+cudaError_t launch_sweep_order(int64_t m, const int32_t *d_clause_off, const int32_t *d_clause_perm,
+                               const int2 *d_slot_info, int32_t *d_sweep_off, int2 *d_sweep_slot, int32_t *d_scratch,
+                               cudaStream_t st)
+{
+    k_sweep_widths<<<grid_for(m + 1), kThreads, 0, st>>>(m, d_clause_off, d_clause_perm, d_sweep_off);
+    exclusive_scan(d_sweep_off, d_sweep_off, m + 1, d_scratch, st);
+    if (m > 0)
+        k_sweep_slots<<<grid_for(m), kThreads, 0, st>>>(m, d_clause_off, d_clause_perm, d_slot_info, d_sweep_off,
+                                                       d_sweep_slot);
+    return cudaGetLastError();
+}
 
 size_t build_cnf_scratch_bytes(int32_t n, int64_t L)
 {

@@ -127,8 +127,12 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t by
                  : "memory");
 }
 
+// Wait for the phase with the given parity. The suspend-time hint lets the hardware park
+// the warp until the phase completes (instead of re-issuing try_wait + branch in a tight
+// loop, which steals issue slots from the compute warps of the same SM sub-partition).
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase)
 {
+#ifdef GALOIS_MBAR_NOHINT
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "WAIT_%=:\n\t"
@@ -136,6 +140,15 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase)
         "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
         "r"(phase)
         : "memory");
+#else
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(phase), "r"(0x989680u)
+        : "memory");
+#endif
 }
 
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar)

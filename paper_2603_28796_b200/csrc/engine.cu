@@ -100,7 +100,9 @@ struct galois_cnf {
     int32_t max_degree = 0;
     int32_t *clause_off = nullptr;
     int32_t *clause_perm = nullptr;
+    int32_t *sweep_off = nullptr;
     int2 *slot_info = nullptr;
+    int2 *sweep_slot = nullptr;
     int32_t *code_off = nullptr;
     int32_t *occ_slot = nullptr;
     int32_t *hub_of_var = nullptr;
@@ -117,6 +119,8 @@ struct galois_cnf {
         d.L = (int32_t)L;
         d.clause_off = clause_off;
         d.clause_perm = clause_perm;
+        d.sweep_off = sweep_off;
+        d.sweep_slot = sweep_slot;
         d.slot_info = slot_info;
         d.code_off = code_off;
         d.occ_slot = occ_slot;
@@ -134,6 +138,8 @@ struct galois_cnf {
         cudaSetDevice(device);
         cudaFree(clause_off);
         cudaFree(clause_perm);
+        cudaFree(sweep_off);
+        cudaFree(sweep_slot);
         cudaFree(slot_info);
         cudaFree(code_off);
         cudaFree(occ_slot);
@@ -292,6 +298,10 @@ static int cnf_build_device(int dev, int32_t num_vars, int64_t num_clauses, int6
         return bail(GALOIS_E_VAR_RANGE, buf);
     }
     c->max_width = h_err[4];
+    LOAD_TRY(dmalloc(&c->sweep_off, (size_t)m + 1));
+    LOAD_TRY(dmalloc(&c->sweep_slot, (size_t)std::max<int64_t>(L, 1)));
+    LOAD_TRY(launch_sweep_order(m, c->clause_off, c->clause_perm, c->slot_info, c->sweep_off, c->sweep_slot,
+                                (int32_t *)d_scratch, st));
 
     // hub table: variables with more than kHubDegree occurrences are reduced in chunks
     std::vector<int32_t> code_off(2 * (size_t)num_vars + 1);

@@ -41,6 +41,8 @@ struct DevCnf {
     int32_t L;
     const int32_t *clause_off;   // [m+1]
     const int32_t *clause_perm;  // [m] clauses in stable width order (warp-uniform widths)
+    const int32_t *sweep_off;    // [m+1] CSR offsets in clause_perm order
+    const int2 *sweep_slot;      // [L] slot_info in clause_perm order (sweep c = clause_perm[c])
     const int2 *slot_info;       // [L] {code, csc position}
     const int32_t *code_off;     // [2n+1]
     const int32_t *occ_slot;     // [L]
@@ -115,6 +117,11 @@ cudaError_t launch_build_cnf(int32_t n, int64_t m, int64_t L, const int64_t *d_o
                              int32_t *d_max_width, int32_t *d_clause_perm, void *d_scratch,
                              size_t scratch_bytes, cudaStream_t st);
 size_t build_cnf_scratch_bytes(int32_t n, int64_t L);
+// sweep order: sweep_off = scan of the widths in clause_perm order, sweep_slot = slot_info
+// regrouped so that the clauses of one sweep are contiguous (scratch: device_scan_scratch_elems(m+1))
+cudaError_t launch_sweep_order(int64_t m, const int32_t *d_clause_off, const int32_t *d_clause_perm,
+                               const int2 *d_slot_info, int32_t *d_sweep_off, int2 *d_sweep_slot, int32_t *d_scratch,
+                               cudaStream_t st);
 // out[i] = sum_{j < i} in[j] (int32, in-place allowed); scratch of device_scan_scratch_elems(N)
 void device_exclusive_scan(const int32_t *in, int32_t *out, int64_t N, int32_t *scratch, cudaStream_t st);
 size_t device_scan_scratch_elems(int64_t N);

@@ -270,13 +270,21 @@ __global__ void __launch_bounds__(256) k_update_st(DevCnf c, StepParams p, RowMa
 
 // -------------------------------- a6 + a7: fused update, TMA-pipelined (W % 32 == 0)
 // Persistent CTAs of 8 consumer warps (one quad per thread) + 1 producer warp; item =
-// (variable, 1024-member chunk). The producer's elected lane runs kStages items ahead:
-// per item it issues 1-D TMA bulk copies (cp.async.bulk) of the z, m, v rows (3 x 4 KB)
-// and, for variables of degree <= kStageRows, of their contiguous E block (deg x 128 B)
-// into a shared-memory stage completing on the stage's `full` mbarrier; consumer warps
-// release a stage through its `empty` mbarrier (one arrive per warp). No CTA-wide
-// barrier in the loop; the memory system sees kStages items per CTA in flight.
+// (variable, 1024-member chunk). The producer's elected lane runs kStages stages ahead of
+// the consumers: an item's first stage carries the z, m, v rows (3 x 4 KB, 1-D TMA bulk
+// copies, cp.async.bulk) and the first kStageRows rows of the variable's contiguous E
+// block; a variable of higher degree streams its remaining E rows through further stages
+// (one 4 KB piece each), so every non-hub degree is counted from shared memory. Stages
+// complete on their `full` mbarrier (transaction bytes); consumer warps release them
+// through `empty` (one arrive per warp). No CTA-wide barrier in the loop. Hub variables
+// (degree > kHubDegree) take one stage for z, m, v and read their partial sums.
 constexpr int kConsumerWarps = 8;
+
+struct StageHdr {
+    int32_t v;       // variable
+    int32_t k1;      // first negative CSC position of v
+    int32_t r0, r1;  // CSC rows staged in this piece
+};
 
 template <bool kDebug, bool kTau1, bool kAdam, bool kPins>
 __global__ void __launch_bounds__(256 + 32, kTmaCtasPerSm) k_update_tma(DevCnf c, StepParams p, RowMap rm, float4 *__restrict__ z4,
@@ -288,8 +296,8 @@ __global__ void __launch_bounds__(256 + 32, kTmaCtasPerSm) k_update_tma(DevCnf c
 {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ uint64_t full[kStages], empty[kStages];
-    __shared__ int4 hdr[kStages];          // {v, k0, k1, k2}
-    __shared__ int32_t hmode[kStages];     // 1 = E staged, 2 = hub, 0 = E from global
+    __shared__ StageHdr hdr[kStages];
+    __shared__ int32_t hflags[kStages];    // bit 0 first piece, bit 1 last piece, bit 2 hub
     if (ctrl->stopped) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t QW = rm.QW;
@@ -305,28 +313,34 @@ __global__ void __launch_bounds__(256 + 32, kTmaCtasPerSm) k_update_tma(DevCnf c
 
     if (warp == kConsumerWarps) {          // ------------------------------ producer warp
         if (lane == 0) {
-            for (uint32_t j = 0;; ++j) {
-                const uint32_t item = blockIdx.x + j * gridDim.x;
-                if (item >= rm.items) break;
-                const int st = (int)(j % kStages);
-                if (j >= (uint32_t)kStages) {
-                    mbar_wait(&empty[st], ((j / kStages) - 1u) & 1u);
-                    fence_proxy_async_smem();
-                }
+            uint32_t slot = 0;
+            for (uint32_t item = blockIdx.x; item < rm.items; item += gridDim.x) {
                 const uint32_t v = div_cpr(rm, item), ch = item - v * rm.cpr;
                 const int32_t k0 = c.code_off[2 * v], k1 = c.code_off[2 * v + 1], k2 = c.code_off[2 * v + 2];
-                const int32_t hub = c.num_hubs > 0 ? c.hub_of_var[v] : -1;
-                const bool staged = hub < 0 && (k2 - k0) <= kStageRows;
-                hdr[st] = make_int4((int32_t)v, k0, k1, k2);
-                hmode[st] = hub >= 0 ? 2 : (staged ? 1 : 0);
-                uint8_t *sb = smem + st * kStageBytes;
-                const uint32_t ebytes = staged ? (uint32_t)(k2 - k0) * 128u : 0u;
-                mbar_arrive_expect_tx(&full[st], 3u * 4096u + ebytes);
+                const bool hub = c.num_hubs > 0 && c.hub_of_var[v] >= 0;
+                const int32_t pieces = hub ? 1 : max(1, (k2 - k0 + kStageRows - 1) / kStageRows);
                 const size_t off = (size_t)v * QW + (size_t)ch * 256u;
-                bulk_g2s(sb + kStageE, z4 + off, 4096u, &full[st]);
-                bulk_g2s(sb + kStageE + 4096, m4 + off, 4096u, &full[st]);
-                bulk_g2s(sb + kStageE + 8192, v4 + off, 4096u, &full[st]);
-                if (ebytes) bulk_g2s(sb, E + ((size_t)ch * c.L + k0) * 32u, ebytes, &full[st]);
+                const uint32_t *Ech = E + (size_t)ch * c.L * 32u;
+                for (int32_t pc = 0; pc < pieces; ++pc, ++slot) {
+                    const int st = (int)(slot % kStages);
+                    if (slot >= (uint32_t)kStages) {
+                        mbar_wait(&empty[st], ((slot / kStages) - 1u) & 1u);
+                        fence_proxy_async_smem();
+                    }
+                    const int32_t r0 = hub ? k0 : k0 + pc * kStageRows;
+                    const int32_t r1 = hub ? k0 : min(k2, r0 + kStageRows);
+                    hdr[st] = StageHdr{(int32_t)v, k1, r0, r1};
+                    hflags[st] = (pc == 0 ? 1 : 0) | (pc == pieces - 1 ? 2 : 0) | (hub ? 4 : 0);
+                    uint8_t *sb = smem + st * kStageBytes;
+                    const uint32_t ebytes = (uint32_t)(r1 - r0) * 128u;
+                    mbar_arrive_expect_tx(&full[st], (pc == 0 ? 3u * 4096u : 0u) + ebytes);
+                    if (pc == 0) {
+                        bulk_g2s(sb + kStageE, z4 + off, 4096u, &full[st]);
+                        bulk_g2s(sb + kStageE + 4096, m4 + off, 4096u, &full[st]);
+                        bulk_g2s(sb + kStageE + 8192, v4 + off, 4096u, &full[st]);
+                    }
+                    if (ebytes) bulk_g2s(sb, Ech + (size_t)r0 * 32u, ebytes, &full[st]);
+                }
             }
         }
     } else {
@@ -338,35 +352,39 @@ __global__ void __launch_bounds__(256 + 32, kTmaCtasPerSm) k_update_tma(DevCnf c
         if (p.clear_a) p.clear_a[i] = 0;
         if (p.clear_b) p.clear_b[i] = 0;
     }
-    for (uint32_t j = 0;; ++j) {
-        const uint32_t item = blockIdx.x + j * gridDim.x;
-        if (item >= rm.items) break;
-        const int st = (int)(j % kStages);
-        mbar_wait(&full[st], (j / kStages) & 1u);
-        const int4 h = hdr[st];
-        const int mode = hmode[st];
-        const int32_t v = h.x;
-        const uint32_t ch = item - (uint32_t)v * rm.cpr;
-        const uint32_t q = ch * 256u + (uint32_t)tid;
-        const uint8_t *sb = smem + st * kStageBytes;
-        float4 z = reinterpret_cast<const float4 *>(sb + kStageE)[tid];
-        float4 m = reinterpret_cast<const float4 *>(sb + kStageE + 4096)[tid];
-        float4 vv = reinterpret_cast<const float4 *>(sb + kStageE + 8192)[tid];
-        const int sh = 4 * (tid & 7);
+    const int sh = 4 * (tid & 7);
+    uint32_t slot = 0;
+    for (uint32_t item = blockIdx.x; item < rm.items; item += gridDim.x) {
+        float4 z, m, vv;
         int32_t G[4] = {0, 0, 0, 0};
-        if (mode == 1) {
-            const uint32_t *srow = reinterpret_cast<const uint32_t *>(sb) + (tid >> 3);
-            count_bits_smem(srow, h.z - h.y, sh, 1, G);
-            count_bits_smem(srow + (h.z - h.y) * 32, h.w - h.z, sh, -1, G);
-        } else if (mode == 2) {
-            hub_signal(c, partial, QW, c.hub_of_var[v], q, G);
-        } else {
-            const uint32_t *col = E + (size_t)ch * c.L * 32u + (tid >> 3);
-            count_bits(col, 32, h.y, h.z, sh, 1, G);
-            count_bits(col, 32, h.z, h.w, sh, -1, G);
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[st]);   // this warp is done reading the stage
+        int32_t v = 0, flags = 0;
+        do {
+            const int st = (int)(slot % kStages);
+            mbar_wait(&full[st], (slot / kStages) & 1u);
+            ++slot;
+            const StageHdr h = hdr[st];
+            flags = hflags[st];
+            v = h.v;
+            const uint8_t *sb = smem + st * kStageBytes;
+            if (flags & 1) {
+                z = reinterpret_cast<const float4 *>(sb + kStageE)[tid];
+                m = reinterpret_cast<const float4 *>(sb + kStageE + 4096)[tid];
+                vv = reinterpret_cast<const float4 *>(sb + kStageE + 8192)[tid];
+            }
+            if (flags & 4) {
+                const uint32_t q = (item - (uint32_t)v * rm.cpr) * 256u + (uint32_t)tid;
+                hub_signal(c, partial, QW, c.hub_of_var[v], q, G);
+            } else {
+                // rows [r0, r1): positive below k1, negative from k1 on
+                const uint32_t *srow = reinterpret_cast<const uint32_t *>(sb) + (tid >> 3);
+                const int32_t npos = min(max(h.k1 - h.r0, 0), h.r1 - h.r0);
+                count_bits_smem(srow, npos, sh, 1, G);
+                count_bits_smem(srow + npos * 32, h.r1 - h.r0 - npos, sh, -1, G);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[st]);   // this warp is done reading the stage
+        } while (!(flags & 2));
+        const uint32_t q = (item - (uint32_t)v * rm.cpr) * 256u + (uint32_t)tid;
         const int64_t bq = p.b0 + 4 * (int64_t)q;
         uint32_t xn, rn;
         float g1o[4];
@@ -388,6 +406,68 @@ __global__ void __launch_bounds__(256 + 32, kTmaCtasPerSm) k_update_tma(DevCnf c
     if (bad) atomicOr(&ctrl->nonfinite, 1);
     }                                      // consumer warps
     last_cta_tick(ctrl);                   // one barrier site for producer and consumers
+}
+
+// --------------------------------------------- a6: hub partial sums, TMA-staged (W % 32 == 0)
+// Item = (hub chunk of <= kHubChunk occurrences, 1024-member chunk): the chunk's E rows
+// (<= 16 KB, contiguous) arrive by one bulk copy; per quad the signed count (|.| <= 128).
+constexpr int kHubStageBytes = kHubChunk * 128;
+
+__global__ void __launch_bounds__(256 + 32, kTmaCtasPerSm) k_hub_partial_tma(DevCnf c, RowMap rm,
+                                                                           const uint32_t *__restrict__ E,
+                                                                           short4 *__restrict__ partial,
+                                                                           const Ctrl *__restrict__ ctrl)
+{
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ uint64_t full[kStages], empty[kStages];
+    __shared__ int4 hdr[kStages];          // {first row, positive rows, rows, hub chunk}
+    if (ctrl->stopped) return;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) {
+        for (int i = 0; i < kStages; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], kConsumerWarps);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (warp == kConsumerWarps) {
+        if (lane == 0) {
+            uint32_t slot = 0;
+            for (uint32_t item = blockIdx.x; item < rm.items; item += gridDim.x, ++slot) {
+                const int st = (int)(slot % kStages);
+                if (slot >= (uint32_t)kStages) {
+                    mbar_wait(&empty[st], ((slot / kStages) - 1u) & 1u);
+                    fence_proxy_async_smem();
+                }
+                const uint32_t hc = div_cpr(rm, item), ch = item - hc * rm.cpr;
+                const int2 info = c.hub_chunk[hc];             // {variable, first CSC position}
+                const int32_t split = c.code_off[2 * info.x + 1], end = c.code_off[2 * info.x + 2];
+                const int32_t k1 = min(info.y + kHubChunk, end);
+                const int32_t npos = min(max(split - info.y, 0), k1 - info.y);
+                hdr[st] = make_int4(info.y, npos, k1 - info.y, (int32_t)hc);
+                const uint32_t bytes = (uint32_t)(k1 - info.y) * 128u;
+                mbar_arrive_expect_tx(&full[st], bytes);
+                bulk_g2s(smem + st * kHubStageBytes, E + ((size_t)ch * c.L + info.y) * 32u, bytes, &full[st]);
+            }
+        }
+    } else {
+        const int sh = 4 * (tid & 7);
+        uint32_t slot = 0;
+        for (uint32_t item = blockIdx.x; item < rm.items; item += gridDim.x, ++slot) {
+            const int st = (int)(slot % kStages);
+            mbar_wait(&full[st], (slot / kStages) & 1u);
+            const int4 h = hdr[st];
+            const uint32_t *srow = reinterpret_cast<const uint32_t *>(smem + st * kHubStageBytes) + (tid >> 3);
+            int32_t G[4] = {0, 0, 0, 0};
+            count_bits_smem(srow, h.y, sh, 1, G);
+            count_bits_smem(srow + h.y * 32, h.z - h.y, sh, -1, G);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[st]);
+            const uint32_t ch = item - (uint32_t)h.w * rm.cpr;
+            partial[(size_t)h.w * rm.QW + ch * 256u + tid] = make_short4((short)G[0], (short)G[1], (short)G[2], (short)G[3]);
+        }
+    }
 }
 
 // ------------------------------------------------------------------ launch wrappers
@@ -426,7 +506,11 @@ void hub_partial(const DevCnf &c, int32_t W, int32_t b_pad, const uint32_t *E, s
 {
     if (c.num_hub_chunks == 0) return;
     const RowMap rm = make_rowmap((uint32_t)c.num_hub_chunks, (uint32_t)b_pad);
-    k_hub_partial<<<item_grid(rm, 8), 256, 0, st>>>(c, W < 32 ? W : 32, rm, E, partial, ctrl);
+    if (W % 32 == 0)
+        k_hub_partial_tma<<<item_grid(rm, kTmaCtasPerSm), 256 + 32, kStages * kHubStageBytes, st>>>(c, rm, E, partial,
+                                                                                                   ctrl);
+    else
+        k_hub_partial<<<item_grid(rm, 8), 256, 0, st>>>(c, W < 32 ? W : 32, rm, E, partial, ctrl);
 }
 
 using UpdKernel = void (*)(DevCnf, StepParams, RowMap, float4 *, float4 *, float4 *, uint32_t *, uint32_t *,
@@ -471,6 +555,9 @@ cudaError_t configure_kernels()
                                  kTmaSmem);
         if (e != cudaSuccess) return e;
     }
+    e = cudaFuncSetAttribute((const void *)k_hub_partial_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             kStages * kHubStageBytes);
+    if (e != cudaSuccess) return e;
     if (dev < 64) done.fetch_or(1ull << dev);
     return cudaSuccess;
 }

@@ -1,0 +1,46 @@
+#!/usr/bin/env bash
+# One GPU session's evidence: tests, smoke, bench lines, launch list and ncu captures.
+#   gpurun --timeout 1800 -- 'bash tools/gpu_round.sh <tag> [parts]'
+# parts (default all): tests bench launches full
+set -u
+TAG=${1:-r01}
+PARTS=${2:-"tests bench launches full"}
+OUT=gpurun_out/$TAG
+mkdir -p "$OUT"
+python -m paper_2603_28796_b200.build > "$OUT/build.log" 2>&1 || { cat "$OUT/build.log"; exit 1; }
+has() { [[ " $PARTS " == *" $1 "* ]]; }
+if has tests; then
+    timeout 900 python -m pytest tests -m gpu -q > "$OUT/pytest_gpu.log" 2>&1
+    tail -3 "$OUT/pytest_gpu.log"
+    timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > "$OUT/smoke.log" 2>&1
+    tail -1 "$OUT/smoke.log"
+fi
+if has bench; then
+    for W in C2 C1 C3a C3b C4 C5; do
+        extra="--no-cpu-baseline"
+        [ "$W" = C2 ] && extra=""
+        timeout 600 python bench.py --workload $W $extra > "$OUT/bench_$W.json" 2> "$OUT/bench_$W.err"
+        tail -c 400 "$OUT/bench_$W.json"; echo
+    done
+    timeout 300 python bench.py --impl reference --steps 3 --warmup 1 > "$OUT/bench_reference.json" 2> "$OUT/bench_reference.err"
+    tail -c 300 "$OUT/bench_reference.json"; echo
+fi
+NCU=/usr/local/cuda/bin/ncu
+if has launches; then
+    for W in C2 C4; do
+        timeout 600 $NCU --metrics gpu__time_duration.sum --clock-control none --csv \
+            --log-file "$OUT/launches_$W.csv" python bench.py --workload $W --steps 4 --warmup 3 \
+            --no-cpu-baseline --no-e2e > "$OUT/launches_$W.log" 2>&1
+        echo "launches $W rc=$?"
+    done
+fi
+if has full; then
+    for W in C2 C4; do
+        for K in k_update_tma k_clauses_v4; do
+            timeout 900 $NCU --set full --clock-control none --import-source on -k regex:$K -s 6 -c 2 \
+                -o "$OUT/full_${W}_$K" python bench.py --workload $W --steps 3 --warmup 3 --no-cpu-baseline \
+                --no-e2e > "$OUT/full_${W}_$K.log" 2>&1
+            echo "full $W $K rc=$?"
+        done
+    done
+fi
