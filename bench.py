@@ -52,7 +52,7 @@ def peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def ncu_traffic(workload):
+def ncu_traffic(workload, cls="update"):
     """Per-launch DRAM bytes of the dominant kernel from the committed ncu --set full
     summary (profiles/ncu_traffic.json), or None."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -60,52 +60,86 @@ def ncu_traffic(workload):
         return None
     with open(path) as f:
         d = json.load(f)
-    e = d.get(workload, {}).get("update")
+    e = d.get(workload, {}).get(cls)
     return None if e is None else e.get("dram_bytes_per_launch")
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled DURING the timed region."""
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """SM clocks and throttle reasons sampled DURING the timed region: an NVML thread
+    polls every 2 ms between start() and stop() (nvidia-smi -lms 50 if NVML is absent)."""
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
 
     def __init__(self, index):
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+        if vis and vis.split(",")[0].strip().isdigit():
+            index = int(vis.split(",")[index].strip())
         self.index = index
+        self.rows = []
+        self.stop_flag = None
+        self.thread = None
         self.proc = None
-        self.path = os.path.join("/tmp", f"galois_clocks_{os.getpid()}.csv")
+
+    def _nvml_loop(self, nv, h, masks):
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        while not self.stop_flag.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.rows.append((float(sm), float(mx), [n for n, m in zip(self.NAMES, masks) if r & m]))
+            except Exception:
+                pass
+            time.sleep(0.002)
 
     def start(self):
+        import threading
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+            import pynvml as nv
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            masks = (nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                     nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap)
+            self.stop_flag = threading.Event()
+            self.thread = threading.Thread(target=self._nvml_loop, args=(nv, h, masks), daemon=True)
+            self.thread.start()
+            return
+        except Exception:
+            self.thread = None
+        try:
+            self.path = os.path.join("/tmp", f"galois_clocks_{os.getpid()}.csv")
+            q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
                                           "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
 
     def stop(self):
-        if self.proc is None:
+        if self.thread is not None:
+            self.stop_flag.set()
+            self.thread.join(timeout=5)
+            src = "nvml 2 ms"
+        elif self.proc is not None:
+            time.sleep(0.1)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            with open(self.path) as f:
+                for line in f:
+                    p = [x.strip() for x in line.split(",")]
+                    if len(p) >= 9 and p[1].replace(".", "").isdigit():
+                        self.rows.append((float(p[1]), float(p[2]),
+                                          [n for i, n in enumerate(self.NAMES) if p[5 + i].lower() == "active"]))
+            src = "nvidia-smi 50 ms"
+        else:
             return None
-        time.sleep(0.15)
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except Exception:
-            self.proc.kill()
-        rows = []
-        with open(self.path) as f:
-            for line in f:
-                parts = [x.strip() for x in line.split(",")]
-                if len(parts) >= 9:
-                    rows.append(parts)
-        if not rows:
+        if not self.rows:
             return None
-        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(rows)}
+        return {"sm_mhz": statistics.median(r[0] for r in self.rows), "sm_max_mhz": max(r[1] for r in self.rows),
+                "reasons": sorted({n for r in self.rows for n in r[2]}), "samples": len(self.rows), "source": src}
 
 
 def oracle_sample(inst, batch, seconds=12.0, rank_b0=0):
@@ -243,18 +277,38 @@ def main():
     L = info["L"]
     value = L * B * args.steps / (ms_max / 1e3)
 
-    # dominant kernel: the fused update (a6 + a7); algorithmic bytes per launch
-    n, W, b_pad = inst.n, (eng.info()["local_batch"] + 31) // 32, ((eng.info()["local_batch"] + 31) // 32) * 32
-    upd_ms, upd_n = kt["update"]
-    hub = info["num_hubs"] > 0
-    bytes_update = (L * W * 4          # read E (CSC order), one bit per member per slot
-                    + 24 * n * b_pad   # z, m, v read + write (fp32)
-                    + 2 * n * W * 4    # X, R bit rows written
-                    + 4 * (2 * n + 1)) # CSC offsets
-    fwd_ms, fwd_n = kt["forward"]
-    bytes_forward = L * W * 4 * 2 + 8 * L + 4 * (inst.m + 1)
+    # algorithmic bytes per launch of each kernel class; roofline = the
+    # class with the largest share of the timed kernel time
+    b_loc = eng.info()["local_batch"]      # the engine's padding: 32 up to 1024, then 1024
+    b_pad = max(32, (b_loc + 31) // 32 * 32) if b_loc <= 1024 else (b_loc + 1023) // 1024 * 1024
+    n, W = inst.n, b_pad // 32
+    deg = np.bincount(np.abs(inst.lits.astype(np.int64)) - 1, minlength=n)
+    hubs = deg > 256
+    L_hub = int(deg[hubs].sum())
+    hub_chunks = int(((deg[hubs] + 127) // 128).sum())
+    alg = {
+        # E of non-hub occurrences (hubs: int16x4 partials) + z, m, v read/write + X, R + offsets
+        "update": (L - L_hub) * W * 4 + hub_chunks * b_pad * 2 + 24 * n * b_pad + 2 * n * W * 4 + 4 * (2 * n + 1),
+        # fused sweep (check interval 1): gather X and R rows per slot, write E, sweep-order index
+        "forward": L * W * 4 * 3 + 8 * L + 4 * (inst.m + 1),
+        # E rows of hub occurrences read, int16x4 partials written
+        "hub_partial": L_hub * W * 4 + hub_chunks * b_pad * 2,
+    }
     peak, peak_src = peaks()
-    achieved = bytes_update / (upd_ms / upd_n / 1e3) / 1e9 if upd_n else None
+    per_kernel = {}
+    for cls, nbytes in alg.items():
+        t, c = kt.get(cls, (0.0, 0))
+        if c:
+            gbs = nbytes / (t / c / 1e3) / 1e9
+            per_kernel[cls] = {"ms_per_launch": t / c, "algorithmic_bytes_per_launch": nbytes,
+                               "achieved_gbs": gbs, "frac": gbs / peak, "ms_per_step": t / args.steps}
+    dom = max(per_kernel, key=lambda k: per_kernel[k]["ms_per_step"]) if per_kernel else "update"
+    KNAME = {"update": "k_update_tma (fused signal reduction + Adam + round + sample)",
+             "forward": "k_sweep (clause forward of X_s fused with the exact check of R_{s-1})",
+             "hub_partial": "k_hub_partial_tma (signal partial sums of hub variables)"}
+    ws = 12 * n * b_pad + L * b_pad // 8 + n * b_pad // 4     # z, m, v + E + X, R
+    l2_note = (f"inputs larger than L2: working set {ws / 1e6:.0f} MB per GPU > 126 MB, no flush" if ws > 126e6 else
+               f"working set {ws / 1e6:.0f} MB per GPU fits the 126 MB L2 (not flushed; small config)")
     gpu_launches = int(sum(c for _, c in kt.values()))
     total_kernel_ms = sum(t for t, _ in kt.values())
 
@@ -273,19 +327,18 @@ def main():
             "config": {"workload": args.workload, "instance": WORKLOADS[args.workload]["desc"],
                        "global_batch": B, "batch_per_gpu": per_gpu, "n": n, "m": inst.m, "L": L,
                        "check_interval": 1, "lr": 0.5, "tau": 1.0, "optimizer": "adam",
-                       "l2": f"inputs larger than L2 (fp32 state {3 * 4 * n * b_pad / 1e6:.0f} MB per GPU > 126 MB)",
+                       "l2": l2_note,
                        "parallelism": f"dp{world} (batch sharding, NCCL MIN all-reduce of the best key per step)"},
-            "roofline": {"bound": "hbm", "kernel": "k_update_tma (fused signal reduction + Adam + round + sample)",
-                         "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": (achieved / peak) if achieved else None,
-                         "traffic": ncu_traffic(args.workload), "algorithmic_bytes_per_launch": bytes_update,
-                         "peak_source": peak_src,
-                         "ms_per_launch": upd_ms / upd_n if upd_n else None,
-                         "share_of_kernel_time": upd_ms / total_kernel_ms if total_kernel_ms else None},
+            "roofline": {"bound": "hbm", "kernel": KNAME[dom],
+                         "achieved": per_kernel.get(dom, {}).get("achieved_gbs"), "peak": peak, "unit": "GB/s",
+                         "frac": per_kernel.get(dom, {}).get("frac"),
+                         "traffic": ncu_traffic(args.workload, dom),
+                         "algorithmic_bytes_per_launch": alg[dom], "peak_source": peak_src,
+                         "ms_per_launch": per_kernel.get(dom, {}).get("ms_per_launch"),
+                         "share_of_kernel_time": (per_kernel[dom]["ms_per_step"] * args.steps / total_kernel_ms)
+                         if dom in per_kernel and total_kernel_ms else None},
             "kernels_ms_per_step": {k: (t / args.steps) for k, (t, c) in kt.items() if c},
-            "forward": {"ms_per_launch": fwd_ms / fwd_n if fwd_n else None,
-                        "achieved_gbs": bytes_forward / (fwd_ms / fwd_n / 1e3) / 1e9 if fwd_n else None,
-                        "algorithmic_bytes_per_launch": bytes_forward},
+            "per_kernel": per_kernel,
             "gpu_launches": gpu_launches,
             "clocks": clk,
             "completed_all_steps": completed,
