@@ -24,9 +24,15 @@ namespace galois {
 namespace {
 
 constexpr int kBatch = 8;             // independent E loads in flight per thread (global path)
-constexpr int kStages = 3;            // TMA pipeline depth
+#ifndef GALOIS_UPD_STAGES
+#define GALOIS_UPD_STAGES 3
+#endif
+#ifndef GALOIS_UPD_CTAS
+#define GALOIS_UPD_CTAS 4
+#endif
+constexpr int kStages = GALOIS_UPD_STAGES;   // TMA pipeline depth
 constexpr int kStageRows = 32;        // E rows staged per item (variables with degree <= 32)
-constexpr int kTmaCtasPerSm = 4;      // 4 x (3 x 16 KB) shared memory per SM
+constexpr int kTmaCtasPerSm = GALOIS_UPD_CTAS;   // 4 x (3 x 16 KB) shared memory per SM
 constexpr int kStageE = kStageRows * 128;
 constexpr int kStageBytes = kStageE + 3 * 4096;   // E rows + z, m, v of 256 quads
 constexpr int kTmaSmem = kStages * kStageBytes;
@@ -65,10 +71,14 @@ __device__ __forceinline__ void count_bits(const uint32_t *__restrict__ col, int
 }
 
 // Same count over rows staged in shared memory (row = 32 words = 128 B).
+#ifndef GALOIS_CNT_UNROLL
+#define GALOIS_CNT_UNROLL 8
+#endif
+template <int kUnroll = GALOIS_CNT_UNROLL>
 __device__ __forceinline__ void count_bits_smem(const uint32_t *srow, int32_t n, int sh, int32_t sign, int32_t G[4])
 {
-    uint32_t acc = 0;                     // n <= kStageRows < 256: no overflow
-#pragma unroll 8
+    uint32_t acc = 0;                     // n <= 128 < 256: no overflow
+#pragma unroll kUnroll
     for (int32_t k = 0; k < n; ++k) acc += spread4((srow[k * 32] >> sh) & 15u);
 #pragma unroll
     for (int j = 0; j < 4; ++j) G[j] += sign * (int32_t)((acc >> (8 * j)) & 255u);
@@ -460,8 +470,8 @@ __global__ void __launch_bounds__(256 + 32, kTmaCtasPerSm) k_hub_partial_tma(Dev
             const int4 h = hdr[st];
             const uint32_t *srow = reinterpret_cast<const uint32_t *>(smem + st * kHubStageBytes) + (tid >> 3);
             int32_t G[4] = {0, 0, 0, 0};
-            count_bits_smem(srow, h.y, sh, 1, G);
-            count_bits_smem(srow + h.y * 32, h.z - h.y, sh, -1, G);
+            count_bits_smem<8>(srow, h.y, sh, 1, G);
+            count_bits_smem<8>(srow + h.y * 32, h.z - h.y, sh, -1, G);
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[st]);
             const uint32_t ch = item - (uint32_t)h.w * rm.cpr;
