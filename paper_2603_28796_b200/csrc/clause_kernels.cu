@@ -127,15 +127,17 @@ __global__ void __launch_bounds__(256) k_clauses_v4(DevCnf c, int32_t W, int32_t
             for (int i = 0; i < kCached; ++i)
                 if (i < width) {
                     const uint4 s = S[i];
-                    const uint4 e = make_uint4(~any.x | (s.x & ~two.x), ~any.y | (s.y & ~two.y),
-                                               ~any.z | (s.z & ~two.z), ~any.w | (s.w & ~two.w));
+                    const uint32_t nm = 0u - (uint32_t)(si[i].x & 1);   // negative: stored complemented
+                    const uint4 e = make_uint4((~any.x | (s.x & ~two.x)) ^ nm, (~any.y | (s.y & ~two.y)) ^ nm,
+                                               (~any.z | (s.z & ~two.z)) ^ nm, (~any.w | (s.w & ~two.w)) ^ nm);
                     *reinterpret_cast<uint4 *>(Ecol + (size_t)si[i].y * CW) = e;
                 }
             for (int i = kCached; i < width; ++i) {
                 const int2 sj = c.slot_info[lo + i];
                 const uint4 s = lit4(BX, VW, sj.x);
-                const uint4 e = make_uint4(~any.x | (s.x & ~two.x), ~any.y | (s.y & ~two.y),
-                                           ~any.z | (s.z & ~two.z), ~any.w | (s.w & ~two.w));
+                const uint32_t nm = 0u - (uint32_t)(sj.x & 1);
+                const uint4 e = make_uint4((~any.x | (s.x & ~two.x)) ^ nm, (~any.y | (s.y & ~two.y)) ^ nm,
+                                           (~any.z | (s.z & ~two.z)) ^ nm, (~any.w | (s.w & ~two.w)) ^ nm);
                 *reinterpret_cast<uint4 *>(Ecol + (size_t)sj.y * CW) = e;
             }
             count_bits_smem4(s_lam, vl, make_uint4(~any.x, ~any.y, ~any.z, ~any.w));
@@ -330,15 +332,17 @@ __global__ void __launch_bounds__(256, GALOIS_SWEEP_MINB) k_sweep(DevCnf c, int3
                 for (int i = 0; i < kSweepCached; ++i)
                     if (i < width) {
                         const uint4 s = S[i];
-                        const uint4 e = make_uint4(~any.x | (s.x & ~two.x), ~any.y | (s.y & ~two.y),
-                                                   ~any.z | (s.z & ~two.z), ~any.w | (s.w & ~two.w));
+                        const uint32_t nm = 0u - (uint32_t)(si[i].x & 1);   // negative: stored complemented
+                        const uint4 e = make_uint4((~any.x | (s.x & ~two.x)) ^ nm, (~any.y | (s.y & ~two.y)) ^ nm,
+                                                   (~any.z | (s.z & ~two.z)) ^ nm, (~any.w | (s.w & ~two.w)) ^ nm);
                         *reinterpret_cast<uint4 *>(Ecol + (size_t)si[i].y * 32) = e;
                     }
                 for (int i = kSweepCached; i < width; ++i) {
                     const int2 sj = c.sweep_slot[lo + i];
                     const uint4 s = lit4(BX, VW, sj.x);
-                    const uint4 e = make_uint4(~any.x | (s.x & ~two.x), ~any.y | (s.y & ~two.y),
-                                               ~any.z | (s.z & ~two.z), ~any.w | (s.w & ~two.w));
+                    const uint32_t nm = 0u - (uint32_t)(sj.x & 1);
+                    const uint4 e = make_uint4((~any.x | (s.x & ~two.x)) ^ nm, (~any.y | (s.y & ~two.y)) ^ nm,
+                                               (~any.z | (s.z & ~two.z)) ^ nm, (~any.w | (s.w & ~two.w)) ^ nm);
                     *reinterpret_cast<uint4 *>(Ecol + (size_t)sj.y * 32) = e;
                 }
             }

@@ -7,7 +7,9 @@
 //        [code_off[c], code_off[c+1]), ascending slot order (stable counting sort)
 //   state z, m, v float [n][b_pad]  (reduced iterate z = theta_1 - theta_0)
 //   bits  X, R uint32 [n][W]        (bit j of word w = member 32w + j)
-//   E     uint32 [L][W] in CSC order (exclusive products of each occurrence)
+//   E     uint32 [L][W] in CSC order (exclusive products of each occurrence); the row of a
+//         NEGATIVE occurrence is stored complemented, so the signed signal of a variable is
+//         (sum of all its row bits) - (number of its negative rows) — one count pass
 #pragma once
 #include <cuda_runtime.h>
 

@@ -161,18 +161,19 @@ __global__ void __launch_bounds__(256) k_clauses_st(DevCnf c, int32_t W, int32_t
         }
         if (kForward) {
             // E_i = prod_{j != i} (1 - s_j): all other literals false <=> none true, or
-            // exactly one true and it is i. Chunk-major layout E[chunk][csc position][LW].
+            // exactly one true and it is i. Chunk-major layout E[chunk][csc position][LW];
+            // rows of negative occurrences are stored complemented (galois_internal.h).
             uint32_t *Ec = E + (size_t)blockIdx.y * c.L * LW + wl;
 #pragma unroll
             for (int i = 0; i < 8; ++i)
                 if (i < width) {
                     const int2 si = c.slot_info[lo + i];
-                    Ec[(size_t)si.y * LW] = ~any | (S[i] & ~two);
+                    Ec[(size_t)si.y * LW] = (~any | (S[i] & ~two)) ^ (0u - (uint32_t)(si.x & 1));
                 }
             for (int i = 8; i < width; ++i) {
                 const int2 si = c.slot_info[lo + i];
                 const uint32_t s = bits[(size_t)(si.x >> 1) * W + word] ^ (0u - (uint32_t)(si.x & 1));
-                Ec[(size_t)si.y * LW] = ~any | (s & ~two);
+                Ec[(size_t)si.y * LW] = (~any | (s & ~two)) ^ (0u - (uint32_t)(si.x & 1));
             }
         }
         uint32_t U = ~any;                  // U = prod_i (1 - s_i): clause unsatisfied

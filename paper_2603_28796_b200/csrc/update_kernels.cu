@@ -39,9 +39,11 @@ constexpr int kTmaSmem = kStages * kStageBytes;
 
 // Count the E bits of one quad (bits sh..sh+3 of column `col`, row stride CW words) over
 // occurrences [k0, k1): kBatch independent predicated loads per round trip; four 8-bit
-// counters in one register (spread4), flushed before they can overflow.
+// counters in one register (spread4), flushed before they can overflow. Rows of negative
+// occurrences are stored complemented, so sum over all rows = G + (number of negative
+// rows): the callers subtract that count (one pass, no sign split).
 __device__ __forceinline__ void count_bits(const uint32_t *__restrict__ col, int32_t CW, int32_t k0, int32_t k1,
-                                           int sh, int32_t sign, int32_t G[4])
+                                           int sh, int32_t G[4])
 {
     const uint32_t *ptr = col + (size_t)k0 * CW;
     int32_t left = k1 - k0;
@@ -66,7 +68,7 @@ __device__ __forceinline__ void count_bits(const uint32_t *__restrict__ col, int
             for (int i = 0; i < kBatch - 1; ++i) acc += spread4((e[i] >> sh) & 15u);
         }
 #pragma unroll
-        for (int j = 0; j < 4; ++j) G[j] += sign * (int32_t)((acc >> (8 * j)) & 255u);
+        for (int j = 0; j < 4; ++j) G[j] += (int32_t)((acc >> (8 * j)) & 255u);
     }
 }
 
@@ -75,13 +77,13 @@ __device__ __forceinline__ void count_bits(const uint32_t *__restrict__ col, int
 #define GALOIS_CNT_UNROLL 8
 #endif
 template <int kUnroll = GALOIS_CNT_UNROLL>
-__device__ __forceinline__ void count_bits_smem(const uint32_t *srow, int32_t n, int sh, int32_t sign, int32_t G[4])
+__device__ __forceinline__ void count_bits_smem(const uint32_t *srow, int32_t n, int sh, int32_t G[4])
 {
     uint32_t acc = 0;                     // n <= 128 < 256: no overflow
 #pragma unroll kUnroll
     for (int32_t k = 0; k < n; ++k) acc += spread4((srow[k * 32] >> sh) & 15u);
 #pragma unroll
-    for (int j = 0; j < 4; ++j) G[j] += sign * (int32_t)((acc >> (8 * j)) & 255u);
+    for (int j = 0; j < 4; ++j) G[j] += (int32_t)((acc >> (8 * j)) & 255u);
 }
 
 struct ItemPos {
@@ -213,8 +215,9 @@ __global__ void __launch_bounds__(256) k_hub_partial(DevCnf c, int32_t CW, RowMa
         const uint32_t *col = e_column(E, c.L, CW, ip.q);
         const int sh = 4 * (ip.q & 7);
         int32_t G[4] = {0, 0, 0, 0};
-        count_bits(col, CW, info.y, min(split, k1), sh, 1, G);
-        count_bits(col, CW, max(split, info.y), k1, sh, -1, G);
+        count_bits(col, CW, info.y, k1, sh, G);
+        const int32_t nneg = k1 - max(split, info.y);
+        if (nneg > 0) { G[0] -= nneg; G[1] -= nneg; G[2] -= nneg; G[3] -= nneg; }
         partial[(size_t)ip.row * rm.QW + ip.q] = make_short4((short)G[0], (short)G[1], (short)G[2], (short)G[3]);
     }
 }
@@ -254,8 +257,8 @@ __global__ void __launch_bounds__(256) k_update_st(DevCnf c, StepParams p, RowMa
                 const int32_t k0 = c.code_off[2 * v], k1 = c.code_off[2 * v + 1], k2 = c.code_off[2 * v + 2];
                 const uint32_t *col = e_column(E, c.L, CW, q);
                 const int sh = 4 * (q & 7);
-                count_bits(col, CW, k0, k1, sh, 1, G);
-                count_bits(col, CW, k1, k2, sh, -1, G);
+                count_bits(col, CW, k0, k2, sh, G);
+                G[0] -= k2 - k1; G[1] -= k2 - k1; G[2] -= k2 - k1; G[3] -= k2 - k1;
             }
             float g1o[4];
             quad_update<kTau1, kAdam, kPins>(p, ac, v, bq, s, G, z, m, vv, xn, rn, g1o, bad);
@@ -385,11 +388,11 @@ __global__ void __launch_bounds__(256 + 32, kTmaCtasPerSm) k_update_tma(DevCnf c
                 const uint32_t q = (item - (uint32_t)v * rm.cpr) * 256u + (uint32_t)tid;
                 hub_signal(c, partial, QW, c.hub_of_var[v], q, G);
             } else {
-                // rows [r0, r1): positive below k1, negative from k1 on
+                // rows [r0, r1): negative ones (from k1 on) are stored complemented
                 const uint32_t *srow = reinterpret_cast<const uint32_t *>(sb) + (tid >> 3);
-                const int32_t npos = min(max(h.k1 - h.r0, 0), h.r1 - h.r0);
-                count_bits_smem(srow, npos, sh, 1, G);
-                count_bits_smem(srow + npos * 32, h.r1 - h.r0 - npos, sh, -1, G);
+                const int32_t nneg = h.r1 - max(h.k1, h.r0);
+                count_bits_smem(srow, h.r1 - h.r0, sh, G);
+                if (nneg > 0) { G[0] -= nneg; G[1] -= nneg; G[2] -= nneg; G[3] -= nneg; }
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[st]);   // this warp is done reading the stage
@@ -470,8 +473,9 @@ __global__ void __launch_bounds__(256 + 32, kTmaCtasPerSm) k_hub_partial_tma(Dev
             const int4 h = hdr[st];
             const uint32_t *srow = reinterpret_cast<const uint32_t *>(smem + st * kHubStageBytes) + (tid >> 3);
             int32_t G[4] = {0, 0, 0, 0};
-            count_bits_smem<8>(srow, h.y, sh, 1, G);
-            count_bits_smem<8>(srow + h.y * 32, h.z - h.y, sh, -1, G);
+            count_bits_smem<8>(srow, h.z, sh, G);                 // h.z rows, the last h.z - h.y negative
+            const int32_t nneg = h.z - h.y;
+            G[0] -= nneg; G[1] -= nneg; G[2] -= nneg; G[3] -= nneg;
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[st]);
             const uint32_t ch = item - (uint32_t)h.w * rm.cpr;
