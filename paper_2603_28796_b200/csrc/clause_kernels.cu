@@ -186,8 +186,8 @@ __global__ void __launch_bounds__(256) k_clauses_v4(DevCnf c, int32_t W, int32_t
 // (sub) per warp. Lanes with equal vl hold the same 128 members of 4 different clauses, so
 // a two-round butterfly (shfl_xor 8, 16) adds their 4 U words and leaves lane (sub, vl)
 // with the 3-bit counts of word 4 vl + sub (a reduce-scatter of a 4 x 4 bit-word block).
-// Each lane adds that into an 8-plane vertical counter (one full adder per plane, LOP3);
-// every 63 groups (<= 252 clauses, below 2^8) the planes are flushed into shared counters
+// Each lane adds that into a vertical counter of 8 (or 6) planes (one full adder per plane);
+// every 63 (15) groups, before a count can reach 2^planes, they are flushed into shared counters
 // with weight 2^k. At dense unsat patterns (C4: ~7% of clause-member pairs) this replaces
 // ~40 instructions per U word by ~10.
 namespace {
@@ -196,7 +196,8 @@ __device__ __forceinline__ uint32_t sel(uint32_t m, uint32_t a, uint32_t b) { re
 
 // U: this lane's 4 words; bm/cm: all-ones masks of sub bit 0 / bit 1. Adds the butterfly
 // counts of word (sub) into planes P[0..7].
-__device__ __forceinline__ void butterfly_add(uint32_t (&P)[8], uint4 U, uint32_t bm, uint32_t cm)
+template <int kPlanes>
+__device__ __forceinline__ void butterfly_add(uint32_t (&P)[kPlanes], uint4 U, uint32_t bm, uint32_t cm)
 {
     // round 1 (partner sub ^ 1): keep words {b, b + 2}, send {1 - b, 3 - b}
     const uint32_t k0 = sel(bm, U.y, U.x), s0 = sel(bm, U.x, U.y);
@@ -222,18 +223,19 @@ __device__ __forceinline__ void butterfly_add(uint32_t (&P)[8], uint4 U, uint32_
     P[2] ^= t2 ^ carry;
     carry = nc;
 #pragma unroll
-    for (int k = 3; k < 8; ++k) {
+    for (int k = 3; k < kPlanes; ++k) {
         nc = P[k] & carry;
         P[k] ^= carry;
         carry = nc;
     }
 }
 
-__device__ __forceinline__ void flush_planes(uint32_t (&P)[8], int32_t *s_cnt, int word)
+template <int kPlanes>
+__device__ __forceinline__ void flush_planes(uint32_t (&P)[kPlanes], int32_t *s_cnt, int word)
 {
     int32_t *dst = s_cnt + word * 32;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
+    for (int k = 0; k < kPlanes; ++k) {
         uint32_t u = P[k];
         while (u) {
             const int j = __ffs(u) - 1;
@@ -246,16 +248,18 @@ __device__ __forceinline__ void flush_planes(uint32_t (&P)[8], int32_t *s_cnt, i
 
 }  // namespace
 
-#ifndef GALOIS_SWEEP_CACHED
-#define GALOIS_SWEEP_CACHED 2
-#endif
-#ifndef GALOIS_SWEEP_MINB
-#define GALOIS_SWEEP_MINB 3
-#endif
-constexpr int kSweepCached = GALOIS_SWEEP_CACHED;
+// Two shapes: kWide (average clause width >= 4.5: many gathers per clause, L2-resident
+// rows) trades register caching and counter planes for a 4th resident CTA per SM.
+template <bool kWide>
+struct SweepShape {
+    static constexpr int kPlanes = kWide ? 6 : 8;            // counts < 2^kPlanes between flushes
+    static constexpr int kFlushGroups = ((1 << kPlanes) - 1) / 4;   // a group adds <= 4 per member
+    static constexpr int kCached = kWide ? 0 : 2;            // slots kept in registers for the E pass
+    static constexpr int kMinBlocks = kWide ? 4 : 3;
+};
 
-template <bool kForward, bool kCheck>
-__global__ void __launch_bounds__(256, GALOIS_SWEEP_MINB) k_sweep(DevCnf c, int32_t W, int32_t b_pad, const uint32_t *__restrict__ X,
+template <bool kForward, bool kCheck, bool kWide>
+__global__ void __launch_bounds__(256, SweepShape<kWide>::kMinBlocks) k_sweep(DevCnf c, int32_t W, int32_t b_pad, const uint32_t *__restrict__ X,
                                                const uint32_t *__restrict__ R, uint32_t *__restrict__ E,
                                                int32_t *__restrict__ lam, int32_t *__restrict__ unsat,
                                                Ctrl *__restrict__ ctrl, BestArgs ba)
@@ -279,9 +283,11 @@ __global__ void __launch_bounds__(256, GALOIS_SWEEP_MINB) k_sweep(DevCnf c, int3
     uint32_t *Ecol = kForward ? E + (size_t)blockIdx.y * c.L * 32 + vl * 4 : nullptr;
     const uint4 *BX = reinterpret_cast<const uint4 *>(X) + vw;
     const uint4 *BR = reinterpret_cast<const uint4 *>(R) + vw;
-    uint32_t PL[8], PU[8];
+    constexpr int kPlanes = SweepShape<kWide>::kPlanes;
+    constexpr int kSweepCached = SweepShape<kWide>::kCached;
+    uint32_t PL[kPlanes], PU[kPlanes];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) PL[k] = PU[k] = 0;
+    for (int k = 0; k < kPlanes; ++k) PL[k] = PU[k] = 0;
     int since = 0;
 
     // the offsets of the next group are loaded one iteration ahead (sweep order: no
@@ -350,7 +356,7 @@ __global__ void __launch_bounds__(256, GALOIS_SWEEP_MINB) k_sweep(DevCnf c, int3
         // U = ~any (clause unsatisfied); an absent clause (ci >= m) contributes 0
         if (kForward) butterfly_add(PL, make_uint4(~any.x, ~any.y, ~any.z, ~any.w), bm, cm);
         if (kCheck) butterfly_add(PU, make_uint4(~anyR.x, ~anyR.y, ~anyR.z, ~anyR.w), bm, cm);
-        if (++since == 63) {                          // warp-uniform: counts stay below 2^8
+        if (++since == SweepShape<kWide>::kFlushGroups) {                // warp-uniform: counts stay below 2^kPlanes
             if (kForward) flush_planes(PL, s_lam, vl * 4 + sub);
             if (kCheck) flush_planes(PU, s_uns, vl * 4 + sub);
             since = 0;
@@ -410,35 +416,31 @@ static dim3 clause_grid_v4(const DevCnf &c, int32_t W)
 
 bool use_v4_clauses(int32_t W) { return W % 4 == 0; }
 
-// resident sweep CTAs per SM (tuning knob: GALOIS_SWEEP_CTAS, default 3)
-static int sweep_ctas_per_sm()
-{
-    static int v = [] {
-        const char *e = getenv("GALOIS_SWEEP_CTAS");
-        const int x = e ? atoi(e) : 0;
-        return x > 0 && x <= 8 ? x : 3;
-    }();
-    return v;
-}
+
 
 // X != null: forward of the sample X (E, lam); R != null: exact check of R (unsat).
 void clauses_v4(const DevCnf &c, int32_t W, int32_t b_pad, const uint32_t *X, const uint32_t *R, uint32_t *E,
                 int32_t *lam, int32_t *unsat, Ctrl *ctrl, const BestArgs &ba, cudaStream_t st)
 {
     if (W % 32 == 0) {
+        const bool wide = (int64_t)c.L >= (int64_t)c.m * 9 / 2;      // average width >= 4.5
         const unsigned chunks = (unsigned)(W / 32);
         const int64_t groups = ((int64_t)c.m + 3) / 4;
         int64_t bx = (groups + 7) / 8;
-        const int64_t cap = (sweep_ctas_per_sm() * 148 + chunks - 1) / chunks;
+        const int64_t cap = ((wide ? 4 : 3) * 148 + chunks - 1) / chunks;
         if (bx > cap) bx = cap;
         if (bx < 1) bx = 1;
         const dim3 grid((unsigned)bx, chunks);
+#define GALOIS_SWEEP(F, C)                                                                                   \
+    (wide ? k_sweep<F, C, true><<<grid, 256, 0, st>>>(c, W, b_pad, X, R, E, lam, unsat, ctrl, ba)           \
+          : k_sweep<F, C, false><<<grid, 256, 0, st>>>(c, W, b_pad, X, R, E, lam, unsat, ctrl, ba))
         if (X && R)
-            k_sweep<true, true><<<grid, 256, 0, st>>>(c, W, b_pad, X, R, E, lam, unsat, ctrl, ba);
+            GALOIS_SWEEP(true, true);
         else if (X)
-            k_sweep<true, false><<<grid, 256, 0, st>>>(c, W, b_pad, X, R, E, lam, unsat, ctrl, ba);
+            GALOIS_SWEEP(true, false);
         else if (R)
-            k_sweep<false, true><<<grid, 256, 0, st>>>(c, W, b_pad, X, R, E, lam, unsat, ctrl, ba);
+            GALOIS_SWEEP(false, true);
+#undef GALOIS_SWEEP
         return;
     }
     const dim3 grid = clause_grid_v4(c, W);

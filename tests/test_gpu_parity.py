@@ -93,6 +93,18 @@ def test_one_step_tma_path(G, batch):
     assert res["tie_x"] + res["tie_r"] <= 3
 
 
+@pytest.mark.parametrize("k,batch", [(5, 1024), (7, 2048)])
+def test_wide_clause_sweep(G, k, batch):
+    """Average width >= 4.5 selects the sweep's wide shape (6 counter planes, no register
+    cache, 4 CTAs per SM): one step from identical iterates and a 12-step trajectory
+    (Lambda, G, unsat counts, best) against the oracle."""
+    inst = I.random_ksat(120, {5: 2400, 7: 9000}[k], k, 8)
+    res = parity.one_step(G, inst, batch, 3)
+    assert res["tie_x"] + res["tie_r"] <= 3
+    rep = parity.run_trajectory(G, inst, batch, 12, seed=2, stop_on_sat=False)
+    assert rep.best_gpu == rep.best_oracle
+
+
 def test_trajectory_50_steps(G):
     """North star: per-step trajectories within 1e-4 for 50 steps on small instances."""
     inst = I.random_ksat(50, 213, 3, 5)
