@@ -142,13 +142,19 @@ class ClockSampler:
                 "reasons": sorted({n for r in self.rows for n in r[2]}), "samples": len(self.rows), "source": src}
 
 
-def oracle_sample(inst, batch, seconds=12.0, rank_b0=0):
-    """The fp64 oracle as it stands, timed on the host cores on a bounded sample of the
-    same workload: whole steps of up to 64 members, repeated until `seconds` elapse."""
-    from oracle import oracle as O
-    f = O.Cnf(inst.n, inst.offsets, inst.lits)
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def _oracle_rate(O, f, inst, nb, seconds, rank_b0):
     cfg = O.Config(seed=0)
-    nb = min(batch, max(16, 4 * O.num_threads()))
     st = O.State.init(inst.n, rank_b0, nb, 0)
     steps = 0
     t0 = time.perf_counter()
@@ -158,10 +164,30 @@ def oracle_sample(inst, batch, seconds=12.0, rank_b0=0):
         el = time.perf_counter() - t0
         if el >= seconds or steps >= 1000:
             break
-    value = inst.L * nb * steps / el
-    return {"value": value, "unit": UNIT, "cores": O.num_threads(), "kind": "oracle",
+    return inst.L * nb * steps / el, steps, el
+
+
+def oracle_sample(inst, batch, seconds=12.0, rank_b0=0):
+    """The fp64 oracle as it stands, timed on the host cores on a bounded sample of the
+    same workload: whole steps of up to 4 x cores members, repeated until the time share
+    elapses — once with OpenMP over all host cores (the reported value) and once on one
+    core (members are independent, so cost is linear in members)."""
+    from oracle import oracle as O
+    f = O.Cnf(inst.n, inst.offsets, inst.lits)
+    cores = O.num_threads()
+    nb = min(batch, max(16, 4 * cores))
+    value, steps, el = _oracle_rate(O, f, inst, nb, seconds * 0.75, rank_b0)
+    O.set_num_threads(1)
+    try:
+        nb1 = min(batch, 4)
+        v1, steps1, el1 = _oracle_rate(O, f, inst, nb1, seconds * 0.25, rank_b0)
+    finally:
+        O.set_num_threads(cores)
+    return {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
             "sample": f"{nb} members x {steps} steps of the {batch}-member workload "
-                      f"(fp64 C oracle, OpenMP over members), {el:.1f} s"}
+                      f"(fp64 C oracle, OpenMP over members), {el:.1f} s",
+            "single_core": {"value": v1, "sample": f"{nb1} members x {steps1} steps, 1 thread, {el1:.1f} s"},
+            "cpu_model": cpu_model()}
 
 
 def dist_env():
@@ -180,8 +206,10 @@ def run_reference(args):
     per_gpu = WORKLOADS[args.workload]["batch"]
     B = per_gpu * args.gpus
     samples = []
+    # each step is a bounded sample: the whole --steps K --warmup W run stays within ~3 min
+    per_step = max(0.25, min(args.ref_seconds, 180.0 / (args.warmup + args.steps)))
     for i in range(args.warmup + args.steps):
-        s = oracle_sample(inst, B, seconds=args.ref_seconds)
+        s = oracle_sample(inst, B, seconds=per_step)
         if i >= args.warmup:
             samples.append(s)
     value = statistics.median(s["value"] for s in samples)
@@ -304,6 +332,18 @@ def main():
             per_kernel[cls] = {"ms_per_launch": t / c, "algorithmic_bytes_per_launch": nbytes,
                                "achieved_gbs": gbs, "frac": gbs / peak, "ms_per_step": t / args.steps}
     dom = max(per_kernel, key=lambda k: per_kernel[k]["ms_per_step"]) if per_kernel else "update"
+    # north_star: the forward + backward kernels together (sweep, hub partials and the fused
+    # backward+update) against HBM peak — model bytes and, where a committed ncu capture
+    # exists for this workload, measured DRAM bytes per launch
+    fb_ms = sum(per_kernel[k]["ms_per_step"] for k in per_kernel)
+    fb_model = sum(alg[k] for k in per_kernel)
+    fb_dram = [ncu_traffic(args.workload, k) for k in per_kernel]
+    fwd_bwd = {"kernels": sorted(per_kernel), "ms_per_step": fb_ms,
+               "model_gbs": fb_model / (fb_ms / 1e3) / 1e9 if fb_ms else None,
+               "model_frac": fb_model / (fb_ms / 1e3) / 1e9 / peak if fb_ms else None,
+               "measured_dram_gbs": (sum(fb_dram) / (fb_ms / 1e3) / 1e9) if fb_ms and all(fb_dram) else None,
+               "measured_frac": (sum(fb_dram) / (fb_ms / 1e3) / 1e9 / peak) if fb_ms and all(fb_dram) else None,
+               "measured_source": "profiles/ncu_traffic.json (dram__bytes_read.sum + dram__bytes_write.sum per launch)"}
     KNAME = {"update": "k_update_tma (fused signal reduction + Adam + round + sample)",
              "forward": "k_sweep (clause forward of X_s fused with the exact check of R_{s-1})",
              "hub_partial": "k_hub_partial_tma (signal partial sums of hub variables)"}
@@ -344,6 +384,7 @@ def main():
                          if dom in per_kernel and total_kernel_ms else None},
             "kernels_ms_per_step": {k: (t / args.steps) for k, (t, c) in kt.items() if c},
             "per_kernel": per_kernel,
+            "fwd_bwd": fwd_bwd,
             "gpu_launches": gpu_launches,
             "clocks": clk,
             "completed_all_steps": completed,
