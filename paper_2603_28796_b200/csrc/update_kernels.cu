@@ -445,7 +445,12 @@ __global__ void __launch_bounds__(256 + 32, kTmaCtasPerSm) k_update_tma(DevCnf c
         const int64_t bq = p.b0 + 4 * (int64_t)q;
         uint32_t xn, rn;
         float g1o[4];
-        quad_update<kTau1, kAdam, kPins>(p, ac, v, bq, s, G, z, m, vv, xn, rn, g1o, bad);
+        // cube pins (C5: 16 of 100k variables): the pinned code path only where the
+        // item's variable is pinned (uniform over the item), the plain one elsewhere
+        if (kPins && p.pin_rank[v] >= 0)
+            quad_update<kTau1, kAdam, true>(p, ac, v, bq, s, G, z, m, vv, xn, rn, g1o, bad);
+        else
+            quad_update<kTau1, kAdam, false>(p, ac, v, bq, s, G, z, m, vv, xn, rn, g1o, bad);
         const size_t idx = (size_t)v * QW + q;
         z4[idx] = z;
         m4[idx] = m;
