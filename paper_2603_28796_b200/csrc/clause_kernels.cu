@@ -258,36 +258,40 @@ struct SweepShape {
     static constexpr int kMinBlocks = kWide ? 4 : 3;
 };
 
-template <bool kForward, bool kCheck, bool kWide>
+template <bool kForward, bool kCheck, bool kWide, bool kLoop>
 __global__ void __launch_bounds__(256, SweepShape<kWide>::kMinBlocks) k_sweep(DevCnf c, int32_t W, int32_t b_pad, const uint32_t *__restrict__ X,
                                                const uint32_t *__restrict__ R, uint32_t *__restrict__ E,
                                                int32_t *__restrict__ lam, int32_t *__restrict__ unsat,
                                                Ctrl *__restrict__ ctrl, BestArgs ba)
 {
-    __shared__ int32_t s_lam[kForward ? 1024 : 1];   // members of this block's 1024-member chunk
+    __shared__ int32_t s_lam[kForward ? 1024 : 1];   // members of the current 1024-member chunk
     __shared__ int32_t s_uns[kCheck ? 1024 : 1];
     if (ctrl->stopped) return;
-    for (int i = threadIdx.x; i < 1024; i += blockDim.x) {
-        if (kForward) s_lam[i] = 0;
-        if (kCheck) s_uns[i] = 0;
-    }
-    __syncthreads();
-
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int sub = lane >> 3, vl = lane & 7;
     const uint32_t bm = 0u - (uint32_t)(sub & 1), cm = 0u - (uint32_t)((sub >> 1) & 1);
     const int VW = W >> 2;
-    const int vw = blockIdx.y * 8 + vl;               // this lane's 16-B vector word of a row
     const int32_t ngroups = (c.m + 3) / 4;
     const int32_t stride = gridDim.x * (blockDim.x >> 5);
-    uint32_t *Ecol = kForward ? E + (size_t)blockIdx.y * c.L * 32 + vl * 4 : nullptr;
-    const uint4 *BX = reinterpret_cast<const uint4 *>(X) + vw;
-    const uint4 *BR = reinterpret_cast<const uint4 *>(R) + vw;
     constexpr int kPlanes = SweepShape<kWide>::kPlanes;
     constexpr int kSweepCached = SweepShape<kWide>::kCached;
     uint32_t PL[kPlanes], PU[kPlanes];
 #pragma unroll
     for (int k = 0; k < kPlanes; ++k) PL[k] = PU[k] = 0;
+    // Chunks blockIdx.y, blockIdx.y + gridDim.y, ...: the launcher sizes gridDim.y so that
+    // the X and R slices of the chunks in flight stay L2-resident (C5: one 1024-member chunk
+    // of all 100k rows at a time instead of all 64 chunks' 1.6 GB).
+    const int chunk_end = kLoop ? W / 32 : (int)blockIdx.y + 1;   // !kLoop: one chunk per CTA
+    for (int chunk = blockIdx.y; chunk < chunk_end; chunk += gridDim.y) {
+    for (int i = threadIdx.x; i < 1024; i += blockDim.x) {
+        if (kForward) s_lam[i] = 0;
+        if (kCheck) s_uns[i] = 0;
+    }
+    __syncthreads();
+    const int vw = chunk * 8 + vl;                    // this lane's 16-B vector word of a row
+    uint32_t *Ecol = kForward ? E + (size_t)chunk * c.L * 32 + vl * 4 : nullptr;
+    const uint4 *BX = reinterpret_cast<const uint4 *>(X) + vw;
+    const uint4 *BR = reinterpret_cast<const uint4 *>(R) + vw;
     int since = 0;
 
     // the offsets of the next group are loaded one iteration ahead (sweep order: no
@@ -365,12 +369,14 @@ __global__ void __launch_bounds__(256, SweepShape<kWide>::kMinBlocks) k_sweep(De
     if (kForward) flush_planes(PL, s_lam, vl * 4 + sub);
     if (kCheck) flush_planes(PU, s_uns, vl * 4 + sub);
     __syncthreads();
-    const int base = blockIdx.y * 1024;
+    const int base = chunk * 1024;
     for (int i = threadIdx.x; i < 1024; i += blockDim.x) {
         if (base + i >= b_pad) break;
         if (kForward && s_lam[i] != 0) atomicAdd(&lam[base + i], s_lam[i]);
         if (kCheck && s_uns[i] != 0) atomicAdd(&unsat[base + i], s_uns[i]);
     }
+    if (kLoop) __syncthreads();                       // s_lam / s_uns are reused by the next chunk
+    }                                                 // chunk loop
     if (kCheck) {
         __shared__ bool s_last;
         __syncthreads();
@@ -425,15 +431,23 @@ void clauses_v4(const DevCnf &c, int32_t W, int32_t b_pad, const uint32_t *X, co
     if (W % 32 == 0) {
         const bool wide = (int64_t)c.L >= (int64_t)c.m * 9 / 2;      // average width >= 4.5
         const unsigned chunks = (unsigned)(W / 32);
+        // chunks in flight: their X and R slices (2 n 128 B each) within ~48 MB of L2
+        const int64_t slice = 2 * (int64_t)c.n * 128;
+        int64_t gy = (48ll << 20) / (slice > 0 ? slice : 1);
+        if (gy < 1) gy = 1;
+        if (gy > (int64_t)chunks) gy = chunks;
         const int64_t groups = ((int64_t)c.m + 3) / 4;
         int64_t bx = (groups + 7) / 8;
-        const int64_t cap = ((wide ? 4 : 3) * 148 + chunks - 1) / chunks;
+        const int64_t cap = ((wide ? 4 : 3) * 148 + gy - 1) / gy;
         if (bx > cap) bx = cap;
         if (bx < 1) bx = 1;
-        const dim3 grid((unsigned)bx, chunks);
+        const dim3 grid((unsigned)bx, (unsigned)gy);
+        const bool loop = gy < (int64_t)chunks;
 #define GALOIS_SWEEP(F, C)                                                                                   \
-    (wide ? k_sweep<F, C, true><<<grid, 256, 0, st>>>(c, W, b_pad, X, R, E, lam, unsat, ctrl, ba)           \
-          : k_sweep<F, C, false><<<grid, 256, 0, st>>>(c, W, b_pad, X, R, E, lam, unsat, ctrl, ba))
+    (wide ? (loop ? k_sweep<F, C, true, true><<<grid, 256, 0, st>>>(c, W, b_pad, X, R, E, lam, unsat, ctrl, ba)  \
+                  : k_sweep<F, C, true, false><<<grid, 256, 0, st>>>(c, W, b_pad, X, R, E, lam, unsat, ctrl, ba)) \
+          : (loop ? k_sweep<F, C, false, true><<<grid, 256, 0, st>>>(c, W, b_pad, X, R, E, lam, unsat, ctrl, ba) \
+                  : k_sweep<F, C, false, false><<<grid, 256, 0, st>>>(c, W, b_pad, X, R, E, lam, unsat, ctrl, ba)))
         if (X && R)
             GALOIS_SWEEP(true, true);
         else if (X)

@@ -175,7 +175,7 @@ def one_step(G, inst, batch, t, seed=0, *, mode=0, tau=1.0, lr=0.5, optimizer=0,
         np.testing.assert_array_equal(lam[~tie_x], out["lam"][~tie_x])
         dg = 1e-5 * np.abs(go) + 1e-30            # north_star: relative 1e-5 (fp32 vs fp64)
         nz = okx & (go != 0)
-        res["max_g1_rel"] = float((np.abs(g1 - go) / np.abs(go))[nz].max()) if nz.any() else 0.0
+        res["max_g1_rel"] = float((np.abs(g1 - go)[nz] / np.abs(go)[nz]).max()) if nz.any() else 0.0
     else:
         # SOFT: fp32 sums of reals; absolute bound on the scale A_v = sum |E| <= degree
         deg = np.bincount(np.abs(inst.lits) - 1, minlength=inst.n).astype(np.float64)
