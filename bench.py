@@ -35,12 +35,81 @@ WORKLOADS = {
     "C3b": dict(desc="random 7-SAT n=500 m=43895 (ratio 87.79), seed 0", batch=16384),
     "C4": dict(desc="industrial-like n=1M m=4.2M widths 2-30 power-law occurrences, seed 0", batch=1024),
     "C5": dict(desc="cube-split random 3-SAT n=100k m=426k, 16 cube pins, seed 0", batch=65536),
+    # the paper's own GPU-stage configuration (App. A) on the C4 instance:
+    # Tseitin k = 3 on the device, B = 3000, 10 epochs, lr 0.5, tau 1, then theta_sel, the
+    # N = 100 candidate pool and the top 0.05 % confident literals (f1 + f2 + f4)
+    "P4": dict(desc="C4 instance normalised to 3-CNF on the device; paper config B=3000, 10 epochs, "
+                    "sub-batches of 1024 (state 12 B x 6.1M vars x 3072 > 180 GB), pool N=100, rho=0.0005",
+               batch=3000, base="C4"),
 }
 
 
 def make_instance(name):
     from paper_2603_28796_b200 import instances as I
-    return I.CONFIGS[name][0]()
+    return I.CONFIGS[WORKLOADS[name].get("base", name)][0]()
+
+
+def paper_pipeline(G, torch, dev, args):
+    """P4: the paper's GPU stage end to end through the C ABI — device Tseitin chain
+    normalisation to k = 3 (f2), a 3000-member Adam run of 10 epochs in 1024-member
+    sub-batches (f4), theta_sel by minimal loss and the N = 100 Gumbel candidate pool with
+    the top-|S| confident literals, |S| = ceil(0.0005 n') (f1). Device-timed per phase."""
+    inst = make_instance("P4")
+    steps = 10
+    t = {}
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    cnf0 = G.Cnf.from_instance(inst)
+    torch.cuda.synchronize(dev)
+    t["load_s"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    cnf = cnf0.normalize(3)
+    torch.cuda.synchronize(dev)
+    t["normalize_s"] = time.perf_counter() - t0
+    info = cnf.info()
+    # a first (cold) pass maps the device memory pool and loads the kernels; the timed
+    # pass is the second, in the same process
+    for rep in range(2):
+        eng = G.Engine(cnf, 3000, steps, 0.5, 0, sub_batch=1024)
+        eng.set_profiling(rep == 1 and bool(os.environ.get("GALOIS_P4_PROFILE")))
+        clocks = ClockSampler(0)
+        clocks.start()
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        rc = eng.run()
+        torch.cuda.synchronize(dev)
+        t["train_s" if rep else "train_cold_s"] = time.perf_counter() - t0
+        clk = clocks.stop()
+        if rep == 0:
+            eng.free()
+    best = eng.best_assignment()
+    kt = {k: v for k, v in eng.kernel_times().items() if v[1]}
+    # theta_sel (min loss, P:102) kept by the sub-batched run; N = 100 Gumbel candidates of
+    # it and their top-|S| confident literals, |S| = ceil(0.0005 n') (Eq.10-11, P:208-237)
+    t0 = time.perf_counter()
+    sel = eng.select_member(0)
+    pool = eng.candidate_pool(sel["global_b"], 100, 0.0005, 7, arrays=False)
+    torch.cuda.synchronize(dev)
+    t["theta_sel_and_pool_s"] = time.perf_counter() - t0
+    pool_info = {"theta_sel_member": sel["global_b"], "theta_sel_unsat": sel["unsat"], "N": 100, "S": pool["S"]}
+    L = info["L"]
+    value = L * 3000 * steps / t["train_s"]
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": steps, "warmup": 0,
+            "ms_per_step": t["train_s"] * 1e3 / steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u32-bits+f32", "data": "synthetic",
+            "config": {"workload": "P4", "instance": WORKLOADS["P4"]["desc"], "n_original": inst.n,
+                       "n": info["n"], "m": info["m"], "L": L, "global_batch": 3000, "sub_batch": 1024,
+                       "lr": 0.5, "tau": 1.0, "optimizer": "adam", "check_interval": 1},
+            "phases_s": t, "best": {"unsat": best["unsat"], "step": best["step"], "member": best["global_b"]},
+            "pool": pool_info, "clocks": clk, "kernel_ms": {k: v[0] for k, v in kt.items()},
+            "kernel_launches": {k: v[1] for k, v in kt.items()},
+            "note": "timed region = galois_engine_run over 3 windows of 1024 members x 10 epochs (each window "
+                    "initialised from t = 0, init included); wall clock bracketed by device syncs; second pass "
+                    "in the process (train_cold_s: the first)"}
+    eng.free()
+    cnf.free()
+    cnf0.free()
+    return line
 
 
 def peaks():
@@ -254,6 +323,10 @@ def main():
         args.gpus = world if world > 1 else args.gpus
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    if args.workload == "P4":
+        if rank == 0:
+            print(json.dumps(paper_pipeline(G, torch, dev, args)), flush=True)
+        return 0
     if args.tts:
         print(json.dumps({"time_to_first_sat": time_to_sat(G, torch, dev, args.tts, range(args.tts_seeds))}),
               flush=True)

@@ -181,7 +181,10 @@ int galois_engine_set_stream(galois_engine *eng, void *cuda_stream);
  * t* runs at most t* steps. The best record is the lexicographic (unsat, step, member)
  * minimum over all windows — exactly the full-batch result; unsat_counts reports each
  * member's last check, info the slice and the full batch's step count. Only run() drives a
- * sub-batched engine (step/enqueue/set_iterate and the selection calls return E_STATE).
+ * sub-batched engine (step/enqueue/set_iterate and the test hooks return E_STATE); run()
+ * also keeps the theta_sel members (rule 0 and 1 of galois_select_member over every
+ * member's last count) with their final iterates, so select_member, candidate_pool and
+ * cube_variables work for those two members as on a resident batch.
  * With world > 1 every rank runs ceil(b_per / sub_batch) windows in lock step. */
 int galois_engine_set_subbatch(galois_engine *eng, int32_t sub_batch);
 

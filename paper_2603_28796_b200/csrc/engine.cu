@@ -481,6 +481,11 @@ struct galois_engine {
     } agg;
     std::vector<uint8_t> agg_bits;     // winner's rounding over all windows
     std::vector<int32_t> agg_counts;   // each local member's last check
+    // theta_sel over the windows (rule 0 min / rule 1 max of each member's last count):
+    // key as k_select, and that member's iterate at the end of its window (device [2][n])
+    unsigned long long sel_key[2] = {~0ull, ~0ull};
+    float *sel_z = nullptr;
+    unsigned long long *sel_dkey = nullptr;
     Comm comm;
     // device buffers
     float *z = nullptr, *m = nullptr, *v = nullptr;
@@ -564,6 +569,10 @@ struct galois_engine {
 
 static void engine_free_buffers(galois_engine *e)
 {
+    if (e->sel_z) cudaFreeAsync(e->sel_z, e->stream);
+    if (e->sel_dkey) cudaFreeAsync(e->sel_dkey, e->stream);
+    e->sel_z = nullptr;
+    e->sel_dkey = nullptr;
     if (e->slab) {
         cudaFreeAsync(e->slab, e->stream);
         cudaStreamSynchronize(e->stream);
@@ -1142,13 +1151,30 @@ static int run_windows(galois_engine *e)
             }
             ENG_CUDA(e, cudaMemcpyAsync(e->agg_bits.data(), e->best_bits, (size_t)e->cnf->n, cudaMemcpyDeviceToHost,
                                         e->stream));
+
             e->agg.u = h.best_u;
             e->agg.t = h.best_t;
             e->agg.b = h.best_b;
         }
-        if (e->b_loc > 0)
+        if (e->b_loc > 0) {
             ENG_CUDA(e, cudaMemcpyAsync(e->agg_counts.data() + (size_t)w * e->sub, e->unsat_last,
                                         sizeof(int32_t) * (size_t)e->b_loc, cudaMemcpyDeviceToHost, e->stream));
+            // theta_sel candidates of this window (f1): keep the iterate of a new min / max
+            if (!e->sel_z) {
+                ENG_CUDA(e, cudaMallocAsync((void **)&e->sel_z, 2 * (size_t)e->cnf->n * 4, e->stream));
+                ENG_CUDA(e, cudaMallocAsync((void **)&e->sel_dkey, 2 * sizeof(unsigned long long), e->stream));
+            }
+            for (int r = 0; r < 2; ++r) launch::select_member(e->unsat_last, e->b_loc, e->b0, r, e->sel_dkey + r, e->stream);
+            unsigned long long k[2];
+            ENG_CUDA(e, cudaMemcpyAsync(k, e->sel_dkey, sizeof(k), cudaMemcpyDeviceToHost, e->stream));
+            ENG_CUDA(e, cudaStreamSynchronize(e->stream));
+            for (int r = 0; r < 2; ++r)
+                if (k[r] < e->sel_key[r]) {
+                    e->sel_key[r] = k[r];
+                    launch::gather_z(e->z, e->cnf->n, e->b_pad, (int32_t)((int64_t)(k[r] & 0xFFFFFFFFull) - e->b0),
+                                     e->sel_z + (size_t)r * e->cnf->n, e->stream);
+                }
+        }
         ENG_CUDA(e, cudaStreamSynchronize(e->stream));
         e->agg.steps = std::max(e->agg.steps, h.t);
         if (h.stopped) e->agg.sat = true;
@@ -1254,7 +1280,20 @@ extern "C" int galois_select_member(galois_engine *e, int32_t rule, int64_t *glo
     ENGINE_ENTRY(e);
     if (rule != 0 && rule != 1) return fail(GALOIS_E_ARG, "rule must be 0 (min loss) or 1 (max loss)");
     if (int rc = prepare(e)) return rc;
-    WHOLE_SLICE_ONLY(e);
+    if (e->windows > 1) {                 // sub-batched: tracked over the windows by run()
+        if (!e->agg.ran || e->sel_key[rule] == ~0ull)
+            return fail(GALOIS_E_STATE, "sub-batched engine: call run() first (this rank has members)");
+        const unsigned long long key = e->sel_key[rule];
+        const uint32_t u = (uint32_t)(key >> 32);
+        if (global_b) *global_b = (int64_t)(key & 0xFFFFFFFFull);
+        if (unsat) *unsat = (int32_t)(rule ? ~u : u);
+        if (z) {
+            ENG_CUDA(e, cudaMemcpyAsync(z, e->sel_z + (size_t)rule * e->cnf->n, (size_t)e->cnf->n * 4,
+                                        cudaMemcpyDeviceToHost, e->stream));
+            ENG_CUDA(e, cudaStreamSynchronize(e->stream));
+        }
+        return GALOIS_OK;
+    }
     Ctrl h;
     if (int rc = settle(e, &h)) return rc;
     if (e->b_loc == 0) return fail(GALOIS_E_STATE, "this rank has no members");
@@ -1288,15 +1327,31 @@ static int local_member(galois_engine *e, int64_t global_b, int32_t *lb)
     return GALOIS_OK;
 }
 
+// The iterate of member global_b into d_z: a resident member, or on a sub-batched engine
+// the retained winner of run() (theta_sel; other members' windows are gone).
+static int member_z(galois_engine *e, int64_t global_b, float *d_z)
+{
+    if (e->windows > 1) {
+        for (int r = 0; r < 2 && e->agg.ran; ++r)
+            if (e->sel_key[r] != ~0ull && (int64_t)(e->sel_key[r] & 0xFFFFFFFFull) == global_b) {
+                ENG_CUDA(e, cudaMemcpyAsync(d_z, e->sel_z + (size_t)r * e->cnf->n, (size_t)e->cnf->n * 4,
+                                            cudaMemcpyDeviceToDevice, e->stream));
+                return GALOIS_OK;
+            }
+        return fail(GALOIS_E_STATE, "sub-batched engine: only the theta_sel members (after run) are retained");
+    }
+    int32_t lb = 0;
+    if (int rc = local_member(e, global_b, &lb)) return rc;
+    launch::gather_z(e->z, e->cnf->n, e->b_pad, lb, d_z, e->stream);
+    return GALOIS_OK;
+}
+
 extern "C" int galois_candidate_pool(galois_engine *e, int64_t global_b, int32_t N, double rho, uint64_t pool_seed,
                                      uint8_t *values, float *confidence, int32_t *units, int32_t *S_out)
 {
     ENGINE_ENTRY(e);
     if (N < 1 || !(rho > 0.0 && rho <= 1.0)) return fail(GALOIS_E_ARG, "need N >= 1 and 0 < rho <= 1");
     if (int rc = prepare(e)) return rc;
-    WHOLE_SLICE_ONLY(e);
-    int32_t lb = 0;
-    if (int rc = local_member(e, global_b, &lb)) return rc;
     const int32_t n = e->cnf->n;
     const int32_t S = std::max<int32_t>(1, (int32_t)std::ceil(rho * (double)n - 1e-9));
     if (S > launch::max_sorted()) return fail(GALOIS_E_ARG, "|S| exceeds 4096");
@@ -1310,7 +1365,10 @@ extern "C" int galois_candidate_pool(galois_engine *e, int64_t global_b, int32_t
     if (int rc = tmp_alloc(e, &d_c, (size_t)N * n)) return rc;
     if (int rc = tmp_alloc(e, &d_x, (size_t)N * n)) return rc;
     if (int rc = tmp_alloc(e, &d_u, (size_t)N * S)) return rc;
-    launch::gather_z(e->z, n, e->b_pad, lb, d_z, e->stream);
+    if (int rc = member_z(e, global_b, d_z)) {
+        for (void *p : {(void *)d_z, (void *)d_c, (void *)d_x, (void *)d_u}) cudaFreeAsync(p, e->stream);
+        return rc;
+    }
     launch::pool(d_z, n, N, (float)(1.0 / e->tau), pool_seed, d_x, d_c, e->stream);
     if (units) launch::topk(d_x, d_c, n, N, S, d_u, e->stream);
     ENG_CUDA(e, cudaGetLastError());
@@ -1327,17 +1385,18 @@ extern "C" int galois_cube_variables(galois_engine *e, int64_t global_b, int32_t
     ENGINE_ENTRY(e);
     if (!vars) return fail(GALOIS_E_ARG, "vars is NULL");
     if (int rc = prepare(e)) return rc;
-    WHOLE_SLICE_ONLY(e);
     const int32_t n = e->cnf->n;
     if (d < 1 || d > n || d > launch::max_sorted()) return fail(GALOIS_E_ARG, "need 1 <= d <= min(n, 4096)");
-    int32_t lb = 0;
-    if (int rc = local_member(e, global_b, &lb)) return rc;
     ENG_CUDA(e, cudaStreamSynchronize(e->stream));
     float *d_z = nullptr;
     int32_t *d_v = nullptr;
     if (int rc = tmp_alloc(e, &d_z, (size_t)n)) return rc;
     if (int rc = tmp_alloc(e, &d_v, (size_t)d)) return rc;
-    launch::gather_z(e->z, n, e->b_pad, lb, d_z, e->stream);
+    if (int rc = member_z(e, global_b, d_z)) {
+        cudaFreeAsync(d_z, e->stream);
+        cudaFreeAsync(d_v, e->stream);
+        return rc;
+    }
     launch::lowconf(d_z, n, d, d_v, e->stream);
     ENG_CUDA(e, cudaGetLastError());
     ENG_CUDA(e, cudaMemcpyAsync(vars, d_v, (size_t)d * 4, cudaMemcpyDeviceToHost, e->stream));

@@ -32,13 +32,11 @@ __global__ void __launch_bounds__(256) k_init(StepParams p, float4 *__restrict__
                                               uint32_t *__restrict__ R)
 {
     const int lane = threadIdx.x & 31;
-    const uint32_t QW = (uint32_t)p.b_pad / 4u;
-    const uint64_t total = (uint64_t)p.n * QW;
+    const uint32_t QW = (uint32_t)p.b_pad / 4u;               // a multiple of 8: whole words per 8 lanes
     const uint2 key = make_uint2((uint32_t)p.seed, (uint32_t)(p.seed >> 32));
-    for (uint64_t flat = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; flat < total;
-         flat += (uint64_t)gridDim.x * blockDim.x) {
-        const int32_t v = (int32_t)(flat / QW);
-        const uint32_t q = (uint32_t)(flat - (uint64_t)v * QW);
+    // rows blockIdx.x, blockIdx.x + gridDim.x, ...; quads of a row across the CTA (no division)
+    for (int32_t v = blockIdx.x; v < p.n; v += gridDim.x)
+    for (uint32_t q = threadIdx.x; q < QW; q += blockDim.x) {
         const int64_t bq = p.b0 + 4 * (int64_t)q;           // global index of member 0 of the quad
         float zz[4];
 #pragma unroll
@@ -84,13 +82,11 @@ __global__ void __launch_bounds__(256) k_resample(StepParams p, const float4 *__
                                                   int32_t t_next)
 {
     const int lane = threadIdx.x & 31;
-    const uint32_t QW = (uint32_t)p.b_pad / 4u;
-    const uint64_t total = (uint64_t)p.n * QW;
+    const uint32_t QW = (uint32_t)p.b_pad / 4u;               // a multiple of 8: whole words per 8 lanes
     const uint2 key = make_uint2((uint32_t)p.seed, (uint32_t)(p.seed >> 32));
-    for (uint64_t flat = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; flat < total;
-         flat += (uint64_t)gridDim.x * blockDim.x) {
-        const int32_t v = (int32_t)(flat / QW);
-        const uint32_t q = (uint32_t)(flat - (uint64_t)v * QW);
+    // rows blockIdx.x, blockIdx.x + gridDim.x, ...; quads of a row across the CTA (no division)
+    for (int32_t v = blockIdx.x; v < p.n; v += gridDim.x)
+    for (uint32_t q = threadIdx.x; q < QW; q += blockDim.x) {
         const int64_t bq = p.b0 + 4 * (int64_t)q;
         const float4 z = z4[(size_t)v * QW + q];
         const float zz[4] = {z.x, z.y, z.z, z.w};
@@ -229,8 +225,8 @@ static unsigned grid_cap(uint64_t work, unsigned threads, unsigned cap)
 
 void init(const StepParams &p, float *z, float *m, float *v, uint32_t *X, uint32_t *R, cudaStream_t st)
 {
-    const uint64_t total = (uint64_t)p.n * (p.b_pad / 4);
-    k_init<<<grid_cap(total, 256, 148 * 16), 256, 0, st>>>(p, (float4 *)z, (float4 *)m, (float4 *)v, X, R);
+    const unsigned rows = (unsigned)(p.n < 148 * 16 ? (p.n > 0 ? p.n : 1) : 148 * 16);
+    k_init<<<rows, 256, 0, st>>>(p, (float4 *)z, (float4 *)m, (float4 *)v, X, R);
 }
 
 void resample(const StepParams &p, const float *z, uint32_t *X, uint32_t *R, int32_t t_next, cudaStream_t st)

@@ -328,11 +328,15 @@ class Engine:
         _check(lib().galois_select_member(self.handle, int(rule), ctypes.byref(b), ctypes.byref(u), _p(z)))
         return dict(global_b=b.value, unsat=u.value, z=z)
 
-    def candidate_pool(self, global_b: int, N: int = 100, rho: float = 0.0005, pool_seed: int = 0):
-        """Eq.10-11: N samples of member global_b, their confidences and top-|S| unit literals."""
+    def candidate_pool(self, global_b: int, N: int = 100, rho: float = 0.0005, pool_seed: int = 0,
+                       arrays: bool = True):
+        """Eq.10-11: N samples of member global_b, their confidences and top-|S| unit literals
+        (arrays=False: the unit lists only; values / confidence stay on the device)."""
         n = self.n
         S = max(1, int(np.ceil(rho * n - 1e-9)))
-        x = np.zeros((N, n), np.uint8); c = np.zeros((N, n), np.float32); u = np.zeros((N, S), np.int32)
+        x = np.zeros((N, n), np.uint8) if arrays else None
+        c = np.zeros((N, n), np.float32) if arrays else None
+        u = np.zeros((N, S), np.int32)
         s_out = ctypes.c_int32()
         _check(lib().galois_candidate_pool(self.handle, int(global_b), int(N), float(rho),
                                            int(pool_seed) & (2 ** 64 - 1), _p(x), _p(c), _p(u),

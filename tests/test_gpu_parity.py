@@ -447,3 +447,28 @@ def test_subbatch_gating_and_sizing(G):
     used = free0 - torch.cuda.mem_get_info()[0]
     big.free()
     assert used < 4 * per * 2048 + (64 << 20), used
+
+
+def test_subbatch_theta_sel_and_pool(G):
+    """f4 + f1: a sub-batched run keeps theta_sel (min and max of every member's last count)
+    and its final iterate, so select_member, the candidate pool and the cube variables
+    equal those of the resident batch (no SAT stop: every window runs the budget)."""
+    inst = I.random_ksat(300, 1290, 3, 5)
+    out = []
+    for sub in (0, 1024):
+        cnf = G.Cnf.from_instance(inst)
+        eng = G.Engine(cnf, 3000, 25, 0.5, 3, sub_batch=sub)
+        assert eng.run() == G.BUDGET
+        sel = [eng.select_member(r) for r in (0, 1)]
+        b0 = sel[0]["global_b"]
+        pool = eng.candidate_pool(b0, 16, 0.02, 5)
+        cubes = eng.cube_variables(b0, 7)
+        out.append((sel, pool, cubes))
+        eng.free()
+    (s0, p0, c0), (s1, p1, c1) = out
+    for r in (0, 1):
+        assert s0[r]["global_b"] == s1[r]["global_b"] and s0[r]["unsat"] == s1[r]["unsat"]
+        np.testing.assert_array_equal(s0[r]["z"], s1[r]["z"])
+    np.testing.assert_array_equal(p0["values"], p1["values"])
+    np.testing.assert_array_equal(p0["units"], p1["units"])
+    np.testing.assert_array_equal(c0, c1)
