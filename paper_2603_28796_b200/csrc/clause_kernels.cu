@@ -147,9 +147,10 @@ __global__ void __launch_bounds__(256) k_clauses_v4(DevCnf c, int32_t W, int32_t
     __syncthreads();
     const int base = blockIdx.y * 4096;
     for (int i = threadIdx.x; i < 4096; i += blockDim.x) {
-        if (base + i >= b_pad) break;
-        if (kForward && s_lam[i] != 0) atomicAdd(&lam[base + i], s_lam[i]);
-        if (kCheck && s_uns[i] != 0) atomicAdd(&unsat[base + i], s_uns[i]);
+        const int mb = base + member_of_slot(i);       // i = word * 32 + bit position
+        if (mb >= b_pad) continue;
+        if (kForward && s_lam[i] != 0) atomicAdd(&lam[mb], s_lam[i]);
+        if (kCheck && s_uns[i] != 0) atomicAdd(&unsat[mb], s_uns[i]);
     }
     if (kCheck) {
         // the last CTA to finish reduces the complete counts to the best key (a8) and, on
@@ -171,7 +172,8 @@ __global__ void __launch_bounds__(256) k_clauses_v4(DevCnf c, int32_t W, int32_t
                     const int64_t lb = ctrl->best_b - ba.b0;
 #pragma unroll 8
                     for (int32_t v = threadIdx.x; v < ba.extract_n; v += blockDim.x)
-                        ba.best_bits[v] = (uint8_t)((R[(size_t)v * ba.W + (lb >> 5)] >> (lb & 31)) & 1u);
+                        ba.best_bits[v] =
+                            (uint8_t)((R[(size_t)v * ba.W + (lb >> 5)] >> bitpos((int)(lb & 31))) & 1u);
                 }
             }
         }
@@ -371,9 +373,10 @@ __global__ void __launch_bounds__(256, SweepShape<kWide>::kMinBlocks) k_sweep(De
     __syncthreads();
     const int base = chunk * 1024;
     for (int i = threadIdx.x; i < 1024; i += blockDim.x) {
-        if (base + i >= b_pad) break;
-        if (kForward && s_lam[i] != 0) atomicAdd(&lam[base + i], s_lam[i]);
-        if (kCheck && s_uns[i] != 0) atomicAdd(&unsat[base + i], s_uns[i]);
+        const int mb = base + member_of_slot(i);       // i = word * 32 + bit position
+        if (mb >= b_pad) continue;
+        if (kForward && s_lam[i] != 0) atomicAdd(&lam[mb], s_lam[i]);
+        if (kCheck && s_uns[i] != 0) atomicAdd(&unsat[mb], s_uns[i]);
     }
     if (kLoop) __syncthreads();                       // s_lam / s_uns are reused by the next chunk
     }                                                 // chunk loop
@@ -395,7 +398,8 @@ __global__ void __launch_bounds__(256, SweepShape<kWide>::kMinBlocks) k_sweep(De
                     const int64_t lb = ctrl->best_b - ba.b0;
 #pragma unroll 8
                     for (int32_t v = threadIdx.x; v < ba.extract_n; v += blockDim.x)
-                        ba.best_bits[v] = (uint8_t)((R[(size_t)v * ba.W + (lb >> 5)] >> (lb & 31)) & 1u);
+                        ba.best_bits[v] =
+                            (uint8_t)((R[(size_t)v * ba.W + (lb >> 5)] >> bitpos((int)(lb & 31))) & 1u);
                 }
             }
         }

@@ -8,21 +8,26 @@
 
 namespace galois {
 
-__device__ __forceinline__ uint32_t group8_mask(int lane) { return 0xFFu << (lane & 24); }
+// Member-in-word layout of every bit plane (X, R, E): member i (0..31) of a 32-member word
+// sits at bit 8 (i mod 4) + i / 4, i.e. member j of quad q' (i = 4 q' + j) at bit 8 j + q'.
+// A thread owning quad q' reads its 4 members as (w >> q') & 0x01010101 — already one
+// per byte, ready for SWAR counting — and 8 lanes pack their quads by 4 ballots + 3 PRMT.
+__device__ __forceinline__ int bitpos(int i) { return ((i & 3) << 3) | (i >> 2); }
+__device__ __forceinline__ int member_of_bit(int p) { return ((p & 7) << 2) | (p >> 3); }
+// smem counter index (32-member word, bit position) -> member offset
+__device__ __forceinline__ int member_of_slot(int i) { return (i & ~31) | member_of_bit(i & 31); }
+__device__ __forceinline__ uint32_t quad_bits(uint32_t w, int qp) { return (w >> qp) & 0x01010101u; }
 
-// OR the 4-bit nibbles of the 8 lanes that share one 32-bit word of packed bits.
-__device__ __forceinline__ uint32_t gather_word(uint32_t nib, int lane)
+// The 32-bit word of the 8-lane group of this lane from each lane's 4-bit quad (bit j =
+// member j); mask = the active lanes (whole 8-lane groups).
+__device__ __forceinline__ uint32_t pack_quads(uint32_t nib, int lane, uint32_t mask = 0xffffffffu)
 {
-    const uint32_t mask = group8_mask(lane);
-    uint32_t w = nib << (4 * (lane & 7));
-    w |= __shfl_xor_sync(mask, w, 1);
-    w |= __shfl_xor_sync(mask, w, 2);
-    w |= __shfl_xor_sync(mask, w, 4);
-    return w;
+    const uint32_t b0 = __ballot_sync(mask, nib & 1u), b1 = __ballot_sync(mask, nib & 2u);
+    const uint32_t b2 = __ballot_sync(mask, nib & 4u), b3 = __ballot_sync(mask, nib & 8u);
+    const uint32_t k = (uint32_t)(lane >> 3) & 3u;
+    const uint32_t sel = k | ((k + 4u) << 4);                 // byte k of x, byte k of y
+    return __byte_perm(__byte_perm(b0, b1, sel), __byte_perm(b2, b3, sel), 0x5410);
 }
-
-// 4 bits -> four 8-bit counters (bit i -> byte i).
-__device__ __forceinline__ uint32_t spread4(uint32_t nib) { return (nib * 0x00204081u) & 0x01010101u; }
 
 __device__ __forceinline__ int pinned_bit(const StepParams &p, int32_t v, int64_t b_global)
 {

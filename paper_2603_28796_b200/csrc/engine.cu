@@ -1513,7 +1513,8 @@ extern "C" int galois_engine_get_bits(galois_engine *e, uint8_t *x_next, uint8_t
         ENG_CUDA(e, cudaStreamSynchronize(e->stream));
         for (int32_t b = 0; b < e->b_loc; ++b)
             for (int32_t v = 0; v < n; ++v)
-                outs[a][(size_t)b * n + v] = (uint8_t)((tmp[(size_t)v * e->W + (b >> 5)] >> (b & 31)) & 1u);
+                outs[a][(size_t)b * n + v] =   // member i of a word at bit 8 (i mod 4) + i / 4
+                    (uint8_t)((tmp[(size_t)v * e->W + (b >> 5)] >> (((b & 3) << 3) | ((b & 31) >> 2))) & 1u);
     }
     return GALOIS_OK;
 }

@@ -6,7 +6,8 @@
 //   CSC  code_off[2n+1] int32: occurrences of literal code c are CSC positions
 //        [code_off[c], code_off[c+1]), ascending slot order (stable counting sort)
 //   state z, m, v float [n][b_pad]  (reduced iterate z = theta_1 - theta_0)
-//   bits  X, R uint32 [n][W]        (bit j of word w = member 32w + j)
+//   bits  X, R uint32 [n][W]        (word w holds members 32w..32w+31; member 32w + i at
+//                                    bit 8 (i mod 4) + i / 4 — see device_utils.cuh bitpos)
 //   E     uint32 [L][W] in CSC order (exclusive products of each occurrence); the row of a
 //         NEGATIVE occurrence is stored complemented, so the signed signal of a variable is
 //         (sum of all its row bits) - (number of its negative rows) — one count pass

@@ -112,7 +112,10 @@ __global__ void __launch_bounds__(256) k_update_soft(DevCnf c, StepParams p, flo
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
          i += (uint64_t)gridDim.x * blockDim.x) {
         const int32_t v = (int32_t)(i / (uint32_t)p.b_pad);
-        const int32_t b = (int32_t)(i - (uint64_t)v * p.b_pad);
+        const int32_t slot = (int32_t)(i - (uint64_t)v * p.b_pad);
+        // lane l of a 32-member word handles the member stored at bit l (device_utils.cuh)
+        const int32_t b = (slot & ~31) | member_of_bit(slot & 31);
+        const size_t ii = (size_t)v * p.b_pad + b;
         const int64_t bg = p.b0 + b;
         const int32_t k0 = c.code_off[2 * v], k1 = c.code_off[2 * v + 1], k2 = c.code_off[2 * v + 2];
         float G = 0.0f;
@@ -122,7 +125,7 @@ __global__ void __launch_bounds__(256) k_update_soft(DevCnf c, StepParams p, flo
         const uint4 wx = philox4x32_10(make_uint4((uint32_t)v, (uint32_t)(bg >> 2), (uint32_t)(s + 1), 1u), key);
         const uint32_t wna[4] = {wn.x, wn.y, wn.z, wn.w}, wxa[4] = {wx.x, wx.y, wx.z, wx.w};
         const int pb = soft_pinned_bit(p, v, bg);
-        float zz = z[i], mm = m[i], w2 = vv[i], g1 = 0.0f;
+        float zz = z[ii], mm = m[ii], w2 = vv[ii], g1 = 0.0f;
         if (pb < 0) {
             const float a = (zz + logistic_from_word(wna[bg & 3])) * p.inv_tau;
             const float e = __expf(-fabsf(a));
@@ -136,13 +139,13 @@ __global__ void __launch_bounds__(256) k_update_soft(DevCnf c, StepParams p, flo
                 zz = zz - 2.0f * p.lr * g1;
             }
             bad |= !isfinite(zz);
-            z[i] = zz;
-            m[i] = mm;
-            vv[i] = w2;
+            z[ii] = zz;
+            m[ii] = mm;
+            vv[ii] = w2;
         }
         if (dbg_G) {
-            dbg_G[i] = G;
-            dbg_g1[i] = g1;
+            dbg_G[ii] = G;
+            dbg_g1[ii] = g1;
         }
         const bool rb = pb >= 0 ? pb != 0 : zz >= 0.0f;
         const bool xb = pb >= 0 ? pb != 0 : zz + logistic_from_word(wxa[bg & 3]) >= 0.0f;

@@ -68,7 +68,10 @@ __global__ void __launch_bounds__(256) k_init(StepParams p, float4 *__restrict__
         z4[idx] = make_float4(zz[0], zz[1], zz[2], zz[3]);
         m4[idx] = make_float4(0.f, 0.f, 0.f, 0.f);
         v4[idx] = make_float4(0.f, 0.f, 0.f, 0.f);
-        const uint32_t xw = gather_word(xn, lane), rw = gather_word(rn, lane);
+        // active lanes: whole 8-lane groups with q < QW (QW is a multiple of 8)
+        const uint32_t qb = q & ~31u;
+        const uint32_t act = QW - qb >= 32u ? 0xffffffffu : ((1u << (QW - qb)) - 1u);
+        const uint32_t xw = pack_quads(xn, lane, act), rw = pack_quads(rn, lane, act);
         if ((lane & 7) == 0) {
             X[(size_t)v * p.W + (q >> 3)] = xw;
             R[(size_t)v * p.W + (q >> 3)] = rw;
@@ -100,7 +103,10 @@ __global__ void __launch_bounds__(256) k_resample(StepParams p, const float4 *__
             xn |= (pb >= 0 ? (uint32_t)pb : (zz[j] + ell >= 0.0f ? 1u : 0u)) << j;
             rn |= (pb >= 0 ? (uint32_t)pb : (zz[j] >= 0.0f ? 1u : 0u)) << j;
         }
-        const uint32_t xw = gather_word(xn, lane), rw = gather_word(rn, lane);
+        // active lanes: whole 8-lane groups with q < QW (QW is a multiple of 8)
+        const uint32_t qb = q & ~31u;
+        const uint32_t act = QW - qb >= 32u ? 0xffffffffu : ((1u << (QW - qb)) - 1u);
+        const uint32_t xw = pack_quads(xn, lane, act), rw = pack_quads(rn, lane, act);
         if ((lane & 7) == 0) {
             X[(size_t)v * p.W + (q >> 3)] = xw;
             R[(size_t)v * p.W + (q >> 3)] = rw;
@@ -182,8 +188,9 @@ __global__ void __launch_bounds__(256) k_clauses_st(DevCnf c, int32_t W, int32_t
     __syncthreads();
     const int base = blockIdx.y * 1024;
     for (int i = threadIdx.x; i < 1024; i += blockDim.x) {
-        const int32_t v = s_cnt[i];
-        if (v != 0 && base + i < b_pad) atomicAdd(&cnt[base + i], v);
+        const int32_t v = s_cnt[i];                       // i = word * 32 + bit position
+        const int mb = member_of_slot(i);
+        if (v != 0 && base + mb < b_pad) atomicAdd(&cnt[base + mb], v);
     }
 }
 
@@ -209,7 +216,7 @@ __global__ void k_extract(const uint32_t *__restrict__ R, int32_t n, int32_t W, 
     if (!ctrl->improved) return;
     const int64_t lb = ctrl->best_b - b0;
     for (int32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
-        best_bits[v] = (uint8_t)((R[(size_t)v * W + (lb >> 5)] >> (lb & 31)) & 1u);
+        best_bits[v] = (uint8_t)((R[(size_t)v * W + (lb >> 5)] >> bitpos((int)(lb & 31))) & 1u);
 }
 
 // ------------------------------------------------------------------ launch wrappers

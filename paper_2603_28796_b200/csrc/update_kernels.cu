@@ -43,7 +43,7 @@ constexpr int kTmaSmem = kStages * kStageBytes;
 // occurrences are stored complemented, so sum over all rows = G + (number of negative
 // rows): the callers subtract that count (one pass, no sign split).
 __device__ __forceinline__ void count_bits(const uint32_t *__restrict__ col, int32_t CW, int32_t k0, int32_t k1,
-                                           int sh, int32_t G[4])
+                                           int qp, int32_t G[4])
 {
     const uint32_t *ptr = col + (size_t)k0 * CW;
     int32_t left = k1 - k0;
@@ -57,7 +57,7 @@ __device__ __forceinline__ void count_bits(const uint32_t *__restrict__ col, int
             for (int i = 0; i < kBatch; ++i) e[i] = __ldg(ptr + i * CW);
             ptr += kBatch * CW;
 #pragma unroll
-            for (int i = 0; i < kBatch; ++i) acc += spread4((e[i] >> sh) & 15u);
+            for (int i = 0; i < kBatch; ++i) acc += quad_bits(e[i], qp);
         }
         if (blk > 0) {
             uint32_t e[kBatch - 1];
@@ -65,7 +65,7 @@ __device__ __forceinline__ void count_bits(const uint32_t *__restrict__ col, int
             for (int i = 0; i < kBatch - 1; ++i) e[i] = i < blk ? __ldg(ptr + i * CW) : 0u;
             ptr += blk * CW;
 #pragma unroll
-            for (int i = 0; i < kBatch - 1; ++i) acc += spread4((e[i] >> sh) & 15u);
+            for (int i = 0; i < kBatch - 1; ++i) acc += quad_bits(e[i], qp);
         }
 #pragma unroll
         for (int j = 0; j < 4; ++j) G[j] += (int32_t)((acc >> (8 * j)) & 255u);
@@ -77,11 +77,11 @@ __device__ __forceinline__ void count_bits(const uint32_t *__restrict__ col, int
 #define GALOIS_CNT_UNROLL 8
 #endif
 template <int kUnroll = GALOIS_CNT_UNROLL>
-__device__ __forceinline__ void count_bits_smem(const uint32_t *srow, int32_t n, int sh, int32_t G[4])
+__device__ __forceinline__ void count_bits_smem(const uint32_t *srow, int32_t n, int qp, int32_t G[4])
 {
     uint32_t acc = 0;                     // n <= 128 < 256: no overflow
 #pragma unroll kUnroll
-    for (int32_t k = 0; k < n; ++k) acc += spread4((srow[k * 32] >> sh) & 15u);
+    for (int32_t k = 0; k < n; ++k) acc += quad_bits(srow[k * 32], qp);
 #pragma unroll
     for (int j = 0; j < 4; ++j) G[j] += (int32_t)((acc >> (8 * j)) & 255u);
 }
@@ -94,7 +94,7 @@ __device__ __forceinline__ void count_bits_smem(const uint32_t *srow, int32_t n,
 // row per 4 members. kIn planes hold the per-thread partial (rows/8 < 2^kIn); the sum
 // needs kIn + 3 planes. Adds the 4 counts of this thread's nibble to G.
 template <int kIn>
-__device__ __forceinline__ void count_rows_sliced(const uint32_t *wcol, int32_t n, int sub, int sh, int32_t G[4])
+__device__ __forceinline__ void count_rows_sliced(const uint32_t *wcol, int32_t n, int sub, int qp, int32_t G[4])
 {
     constexpr int kOut = kIn + 3;
     uint32_t P[kOut];
@@ -122,7 +122,7 @@ __device__ __forceinline__ void count_rows_sliced(const uint32_t *wcol, int32_t 
     }
     uint32_t acc = 0;                           // byte j = count of member sh + j (<= 255)
 #pragma unroll
-    for (int k = 0; k < kOut; ++k) acc += spread4((P[k] >> sh) & 15u) << k;
+    for (int k = 0; k < kOut; ++k) acc += quad_bits(P[k], qp) << k;
 #pragma unroll
     for (int j = 0; j < 4; ++j) G[j] += (int32_t)((acc >> (8 * j)) & 255u);
 }
@@ -254,7 +254,7 @@ __global__ void __launch_bounds__(256) k_hub_partial(DevCnf c, int32_t CW, RowMa
         const int32_t split = c.code_off[2 * info.x + 1], end = c.code_off[2 * info.x + 2];
         const int32_t k1 = min(info.y + kHubChunk, end);
         const uint32_t *col = e_column(E, c.L, CW, ip.q);
-        const int sh = 4 * (ip.q & 7);
+        const int sh = ip.q & 7;          // bit offset of this quad's members
         int32_t G[4] = {0, 0, 0, 0};
         count_bits(col, CW, info.y, k1, sh, G);
         const int32_t nneg = k1 - max(split, info.y);
@@ -297,7 +297,7 @@ __global__ void __launch_bounds__(256) k_update_st(DevCnf c, StepParams p, RowMa
             } else {
                 const int32_t k0 = c.code_off[2 * v], k1 = c.code_off[2 * v + 1], k2 = c.code_off[2 * v + 2];
                 const uint32_t *col = e_column(E, c.L, CW, q);
-                const int sh = 4 * (q & 7);
+                const int sh = q & 7;
                 count_bits(col, CW, k0, k2, sh, G);
                 G[0] -= k2 - k1; G[1] -= k2 - k1; G[2] -= k2 - k1; G[3] -= k2 - k1;
             }
@@ -312,7 +312,7 @@ __global__ void __launch_bounds__(256) k_update_st(DevCnf c, StepParams p, RowMa
             }
         }
         // 8 lanes = one 32-bit word; validity is uniform within each group of 8 lanes
-        const uint32_t xw = gather_word(xn, lane), rw = gather_word(rn, lane);
+        const uint32_t xw = pack_quads(xn, lane), rw = pack_quads(rn, lane);
         if (ip.valid && (lane & 7) == 0) {
             X[(size_t)v * p.W + (q >> 3)] = xw;
             R[(size_t)v * p.W + (q >> 3)] = rw;
@@ -406,7 +406,7 @@ __global__ void __launch_bounds__(256 + 32, kTmaCtasPerSm) k_update_tma(DevCnf c
         if (p.clear_a) p.clear_a[i] = 0;
         if (p.clear_b) p.clear_b[i] = 0;
     }
-    const int sh = 4 * (tid & 7);
+    const int sh = tid & 7;
     uint32_t slot = 0;
     for (uint32_t item = blockIdx.x; item < rm.items; item += gridDim.x) {
         float4 z, m, vv;
@@ -459,7 +459,7 @@ __global__ void __launch_bounds__(256 + 32, kTmaCtasPerSm) k_update_tma(DevCnf c
             dbg_G[idx] = make_int4(G[0], G[1], G[2], G[3]);
             dbg_g1[idx] = make_float4(g1o[0], g1o[1], g1o[2], g1o[3]);
         }
-        const uint32_t xw = gather_word(xn, lane), rw = gather_word(rn, lane);
+        const uint32_t xw = pack_quads(xn, lane), rw = pack_quads(rn, lane);
         if ((lane & 7) == 0) {
             X[(size_t)v * p.W + (q >> 3)] = xw;
             R[(size_t)v * p.W + (q >> 3)] = rw;
@@ -514,7 +514,7 @@ __global__ void __launch_bounds__(256 + 32, kTmaCtasPerSm) k_hub_partial_tma(Dev
             }
         }
     } else {
-        const int sh = 4 * (tid & 7);
+        const int sh = tid & 7;
         uint32_t slot = 0;
         for (uint32_t item = blockIdx.x; item < rm.items; item += gridDim.x, ++slot) {
             const int st = (int)(slot % kStages);
