@@ -148,15 +148,18 @@ class ClockSampler:
         self.thread = None
         self.proc = None
 
-    def _nvml_loop(self, nv, h, masks):
-        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+    def _sample(self):
+        nv, h, masks, mx = self.nv
+        try:
+            sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+            r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+            self.rows.append((float(sm), float(mx), [n for n, m in zip(self.NAMES, masks) if r & m]))
+        except Exception:
+            pass
+
+    def _nvml_loop(self):
         while not self.stop_flag.is_set():
-            try:
-                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
-                r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
-                self.rows.append((float(sm), float(mx), [n for n, m in zip(self.NAMES, masks) if r & m]))
-            except Exception:
-                pass
+            self._sample()
             time.sleep(0.002)
 
     def start(self):
@@ -167,8 +170,9 @@ class ClockSampler:
             h = nv.nvmlDeviceGetHandleByIndex(self.index)
             masks = (nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
                      nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap)
+            self.nv = (nv, h, masks, nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
             self.stop_flag = threading.Event()
-            self.thread = threading.Thread(target=self._nvml_loop, args=(nv, h, masks), daemon=True)
+            self.thread = threading.Thread(target=self._nvml_loop, daemon=True)
             self.thread.start()
             return
         except Exception:
@@ -188,6 +192,8 @@ class ClockSampler:
         if self.thread is not None:
             self.stop_flag.set()
             self.thread.join(timeout=5)
+            if not self.rows:               # a region shorter than one poll: sample at its end
+                self._sample()
             src = "nvml 2 ms"
         elif self.proc is not None:
             time.sleep(0.1)
