@@ -355,6 +355,7 @@ __global__ void __launch_bounds__(256 + 32, kTmaCtasPerSm) k_update_tma(DevCnf c
     if (ctrl->stopped) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t QW = rm.QW;
+    const uint32_t full_s = smem_u32(full), empty_s = smem_u32(empty), stage_s = smem_u32(smem);
 
     if (tid == 0) {
         for (int i = 0; i < kStages; ++i) {
@@ -378,22 +379,22 @@ __global__ void __launch_bounds__(256 + 32, kTmaCtasPerSm) k_update_tma(DevCnf c
                 for (int32_t pc = 0; pc < pieces; ++pc, ++slot) {
                     const int st = (int)(slot % kStages);
                     if (slot >= (uint32_t)kStages) {
-                        mbar_wait(&empty[st], ((slot / kStages) - 1u) & 1u);
+                        mbar_wait_s(empty_s + 8u * st, ((slot / kStages) - 1u) & 1u);
                         fence_proxy_async_smem();
                     }
                     const int32_t r0 = hub ? k0 : k0 + pc * kStageRows;
                     const int32_t r1 = hub ? k0 : min(k2, r0 + kStageRows);
                     hdr[st] = StageHdr{(int32_t)v, k1, r0, r1};
                     hflags[st] = (pc == 0 ? 1 : 0) | (pc == pieces - 1 ? 2 : 0) | (hub ? 4 : 0);
-                    uint8_t *sb = smem + st * kStageBytes;
                     const uint32_t ebytes = (uint32_t)(r1 - r0) * 128u;
-                    mbar_arrive_expect_tx(&full[st], (pc == 0 ? 3u * 4096u : 0u) + ebytes);
+                    const uint32_t fb = full_s + 8u * st, sbs = stage_s + (uint32_t)(st * kStageBytes);
+                    mbar_arrive_expect_tx_s(fb, (pc == 0 ? 3u * 4096u : 0u) + ebytes);
                     if (pc == 0) {
-                        bulk_g2s(sb + kStageE, z4 + off, 4096u, &full[st]);
-                        bulk_g2s(sb + kStageE + 4096, m4 + off, 4096u, &full[st]);
-                        bulk_g2s(sb + kStageE + 8192, v4 + off, 4096u, &full[st]);
+                        bulk_g2s_s(sbs + kStageE, z4 + off, 4096u, fb);
+                        bulk_g2s_s(sbs + kStageE + 4096, m4 + off, 4096u, fb);
+                        bulk_g2s_s(sbs + kStageE + 8192, v4 + off, 4096u, fb);
                     }
-                    if (ebytes) bulk_g2s(sb, Ech + (size_t)r0 * 32u, ebytes, &full[st]);
+                    if (ebytes) bulk_g2s_s(sbs, Ech + (size_t)r0 * 32u, ebytes, fb);
                 }
             }
         }
@@ -414,7 +415,7 @@ __global__ void __launch_bounds__(256 + 32, kTmaCtasPerSm) k_update_tma(DevCnf c
         int32_t v = 0, flags = 0;
         do {
             const int st = (int)(slot % kStages);
-            mbar_wait(&full[st], (slot / kStages) & 1u);
+            mbar_wait_s(full_s + 8u * st, (slot / kStages) & 1u);
             ++slot;
             const StageHdr h = hdr[st];
             flags = hflags[st];
@@ -439,7 +440,7 @@ __global__ void __launch_bounds__(256 + 32, kTmaCtasPerSm) k_update_tma(DevCnf c
                 if (nneg > 0) { G[0] -= nneg; G[1] -= nneg; G[2] -= nneg; G[3] -= nneg; }
             }
             __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[st]);   // this warp is done reading the stage
+            if (lane == 0) mbar_arrive_s(empty_s + 8u * st);   // this warp is done reading the stage
         } while (!(flags & 2));
         const uint32_t q = (item - (uint32_t)v * rm.cpr) * 256u + (uint32_t)tid;
         const int64_t bq = p.b0 + 4 * (int64_t)q;
@@ -447,10 +448,15 @@ __global__ void __launch_bounds__(256 + 32, kTmaCtasPerSm) k_update_tma(DevCnf c
         float g1o[4];
         // cube pins (C5: 16 of 100k variables): the pinned code path only where the
         // item's variable is pinned (uniform over the item), the plain one elsewhere
+#ifdef GALOIS_UPD_MEMONLY   // experiment: the data movement of this kernel without its arithmetic
+        xn = (uint32_t)G[0] & 15u; rn = __float_as_uint(z.x) & 15u; (void)bq; (void)g1o;
+        z.x += 1.0f; m.x += 1.0f; vv.x += 1.0f;
+#else
         if (kPins && p.pin_rank[v] >= 0)
             quad_update<kTau1, kAdam, true>(p, ac, v, bq, s, G, z, m, vv, xn, rn, g1o, bad);
         else
             quad_update<kTau1, kAdam, false>(p, ac, v, bq, s, G, z, m, vv, xn, rn, g1o, bad);
+#endif
         const size_t idx = (size_t)v * QW + q;
         z4[idx] = z;
         m4[idx] = m;
