@@ -113,3 +113,28 @@ def test_call_order_and_arguments(G):
     f = O.Cnf(inst.n, inst.offsets, inst.lits)
     assert O.unsat_count(f, first["values"]) == first["unsat"]
     eng.free()
+
+
+def test_graph_replay_equals_plain_launches(G):
+    """run() replays CUDA graphs of 8 captured steps when the budget is long (>= 256 steps
+    left): the result must be bit-identical to enqueueing the same steps one by one
+    (Lambda parity buffers, step counters and the stop flag all live on the device)."""
+    inst = I.random_ksat(60, 420, 3, 11)              # ratio 7: UNSAT, runs the whole budget
+    out = []
+    for mode in ("graph", "plain"):
+        cnf = G.Cnf.from_instance(inst)
+        eng = G.Engine(cnf, 2048, 300, 0.5, 2)
+        if mode == "graph":
+            rc = eng.run()
+        else:
+            eng.enqueue(300)
+            rc = eng.run()                             # nothing left: settles and reports
+        best = eng.best_assignment()
+        counts, _ = eng.unsat_counts()
+        z, _, _, t = eng.get_iterate()
+        out.append((rc, best["unsat"], best["step"], best["global_b"], counts.copy(), z.copy(), t))
+        eng.free()
+    a, b = out
+    assert a[0] == b[0] == G.BUDGET and a[1:4] == b[1:4] and a[6] == b[6] == 300
+    np.testing.assert_array_equal(a[4], b[4])
+    np.testing.assert_array_equal(a[5], b[5])
