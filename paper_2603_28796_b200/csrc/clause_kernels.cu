@@ -44,10 +44,11 @@ __device__ __forceinline__ void count_bits_smem4(int32_t *s_cnt, int vl, uint4 U
     }
 }
 
-__device__ __forceinline__ uint4 lit4(const uint4 *B, int VW, int32_t code)
+// B: this lane's X (or R) vector of row 0; rows are RS uint4 apart (interleaved X/R rows)
+__device__ __forceinline__ uint4 lit4(const uint4 *B, int RS, int32_t code)
 {
     const uint32_t neg = 0u - (uint32_t)(code & 1);
-    uint4 s = B[(size_t)(code >> 1) * VW];
+    uint4 s = B[(size_t)(code >> 1) * RS];
     s.x ^= neg; s.y ^= neg; s.z ^= neg; s.w ^= neg;
     return s;
 }
@@ -82,6 +83,7 @@ __global__ void __launch_bounds__(256) k_clauses_v4(DevCnf c, int32_t W, int32_t
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int VW = W >> 2;                    // 16-B vector words per row
+    const int RS = 2 * VW;                    // uint4 per interleaved X/R row
     const int LPC = VW < 32 ? VW : 32;
     const int CPW = 32 / LPC;
     const int sub = lane / LPC, vl = lane - sub * LPC;
@@ -93,8 +95,8 @@ __global__ void __launch_bounds__(256) k_clauses_v4(DevCnf c, int32_t W, int32_t
     const int CW = W < 32 ? W : 32;
     const int ch = (vw << 2) / CW, wi = (vw << 2) - ch * CW;
     uint32_t *Ecol = kForward ? E + (size_t)ch * c.L * CW + wi : nullptr;
-    const uint4 *BX = reinterpret_cast<const uint4 *>(X) + vw;
-    const uint4 *BR = reinterpret_cast<const uint4 *>(R) + vw;
+    const uint4 *BX = reinterpret_cast<const uint4 *>(X) + 2 * vw;   // interleaved rows: X, R groups alternate
+    const uint4 *BR = reinterpret_cast<const uint4 *>(R) + 2 * vw;
 
     for (int64_t g = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; g < ngroups; g += stride) {
         const int64_t ci = g * CPW + sub;
@@ -111,16 +113,16 @@ __global__ void __launch_bounds__(256) k_clauses_v4(DevCnf c, int32_t W, int32_t
         for (int i = 0; i < kCached; ++i) {
             if (i < width) {
                 if (kForward) {
-                    S[i] = lit4(BX, VW, si[i].x);
+                    S[i] = lit4(BX, RS, si[i].x);
                     acc2(any, two, S[i]);
                 }
-                if (kCheck) or4(anyR, lit4(BR, VW, si[i].x));
+                if (kCheck) or4(anyR, lit4(BR, RS, si[i].x));
             }
         }
         for (int i = kCached; i < width; ++i) {
             const int2 sj = c.slot_info[lo + i];
-            if (kForward) acc2(any, two, lit4(BX, VW, sj.x));
-            if (kCheck) or4(anyR, lit4(BR, VW, sj.x));
+            if (kForward) acc2(any, two, lit4(BX, RS, sj.x));
+            if (kCheck) or4(anyR, lit4(BR, RS, sj.x));
         }
         if (kForward) {
 #pragma unroll
@@ -134,7 +136,7 @@ __global__ void __launch_bounds__(256) k_clauses_v4(DevCnf c, int32_t W, int32_t
                 }
             for (int i = kCached; i < width; ++i) {
                 const int2 sj = c.slot_info[lo + i];
-                const uint4 s = lit4(BX, VW, sj.x);
+                const uint4 s = lit4(BX, RS, sj.x);
                 const uint32_t nm = 0u - (uint32_t)(sj.x & 1);
                 const uint4 e = make_uint4((~any.x | (s.x & ~two.x)) ^ nm, (~any.y | (s.y & ~two.y)) ^ nm,
                                            (~any.z | (s.z & ~two.z)) ^ nm, (~any.w | (s.w & ~two.w)) ^ nm);
@@ -173,7 +175,7 @@ __global__ void __launch_bounds__(256) k_clauses_v4(DevCnf c, int32_t W, int32_t
 #pragma unroll 8
                     for (int32_t v = threadIdx.x; v < ba.extract_n; v += blockDim.x)
                         ba.best_bits[v] =
-                            (uint8_t)((R[(size_t)v * ba.W + (lb >> 5)] >> bitpos((int)(lb & 31))) & 1u);
+                            (uint8_t)((R[xr_at(v, (int32_t)(lb >> 5), ba.W)] >> bitpos((int)(lb & 31))) & 1u);
                 }
             }
         }
@@ -273,6 +275,7 @@ __global__ void __launch_bounds__(256, SweepShape<kWide>::kMinBlocks) k_sweep(De
     const int sub = lane >> 3, vl = lane & 7;
     const uint32_t bm = 0u - (uint32_t)(sub & 1), cm = 0u - (uint32_t)((sub >> 1) & 1);
     const int VW = W >> 2;
+    const int RS = 2 * VW;                            // uint4 per interleaved X/R row
     const int32_t ngroups = (c.m + 3) / 4;
     const int32_t stride = gridDim.x * (blockDim.x >> 5);
     constexpr int kPlanes = SweepShape<kWide>::kPlanes;
@@ -292,8 +295,8 @@ __global__ void __launch_bounds__(256, SweepShape<kWide>::kMinBlocks) k_sweep(De
     __syncthreads();
     const int vw = chunk * 8 + vl;                    // this lane's 16-B vector word of a row
     uint32_t *Ecol = kForward ? E + (size_t)chunk * c.L * 32 + vl * 4 : nullptr;
-    const uint4 *BX = reinterpret_cast<const uint4 *>(X) + vw;
-    const uint4 *BR = reinterpret_cast<const uint4 *>(R) + vw;
+    const uint4 *BX = reinterpret_cast<const uint4 *>(X) + 2 * vw;   // interleaved rows: X, R groups alternate
+    const uint4 *BR = reinterpret_cast<const uint4 *>(R) + 2 * vw;
     int since = 0;
 
     // the offsets of the next group are loaded one iteration ahead (sweep order: no
@@ -328,16 +331,16 @@ __global__ void __launch_bounds__(256, SweepShape<kWide>::kMinBlocks) k_sweep(De
             for (int i = 0; i < kSweepCached; ++i) {
                 if (i < width) {
                     if (kForward) {
-                        S[i] = lit4(BX, VW, si[i].x);
+                        S[i] = lit4(BX, RS, si[i].x);
                         acc2(any, two, S[i]);
                     }
-                    if (kCheck) or4(anyR, lit4(BR, VW, si[i].x));
+                    if (kCheck) or4(anyR, lit4(BR, RS, si[i].x));
                 }
             }
             for (int i = kSweepCached; i < width; ++i) {
                 const int2 sj = c.sweep_slot[lo + i];
-                if (kForward) acc2(any, two, lit4(BX, VW, sj.x));
-                if (kCheck) or4(anyR, lit4(BR, VW, sj.x));
+                if (kForward) acc2(any, two, lit4(BX, RS, sj.x));
+                if (kCheck) or4(anyR, lit4(BR, RS, sj.x));
             }
             if (kForward) {
 #pragma unroll
@@ -351,7 +354,7 @@ __global__ void __launch_bounds__(256, SweepShape<kWide>::kMinBlocks) k_sweep(De
                     }
                 for (int i = kSweepCached; i < width; ++i) {
                     const int2 sj = c.sweep_slot[lo + i];
-                    const uint4 s = lit4(BX, VW, sj.x);
+                    const uint4 s = lit4(BX, RS, sj.x);
                     const uint32_t nm = 0u - (uint32_t)(sj.x & 1);
                     const uint4 e = make_uint4((~any.x | (s.x & ~two.x)) ^ nm, (~any.y | (s.y & ~two.y)) ^ nm,
                                                (~any.z | (s.z & ~two.z)) ^ nm, (~any.w | (s.w & ~two.w)) ^ nm);
@@ -399,7 +402,7 @@ __global__ void __launch_bounds__(256, SweepShape<kWide>::kMinBlocks) k_sweep(De
 #pragma unroll 8
                     for (int32_t v = threadIdx.x; v < ba.extract_n; v += blockDim.x)
                         ba.best_bits[v] =
-                            (uint8_t)((R[(size_t)v * ba.W + (lb >> 5)] >> bitpos((int)(lb & 31))) & 1u);
+                            (uint8_t)((R[xr_at(v, (int32_t)(lb >> 5), ba.W)] >> bitpos((int)(lb & 31))) & 1u);
                 }
             }
         }

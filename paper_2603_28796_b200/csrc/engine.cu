@@ -892,8 +892,7 @@ static int prepare(galois_engine *e)
     slab.add(&e->z, nb);
     slab.add(&e->m, nb);
     slab.add(&e->v, nb);
-    slab.add(&e->X, (size_t)n * e->W);
-    slab.add(&e->R, (size_t)n * e->W);
+    slab.add(&e->X, (size_t)n * 2 * xr_pad(e->W));   // interleaved X/R rows (galois_internal.h)
     slab.add(&e->unsat, (size_t)e->b_pad);
     slab.add(&e->unsat_last, (size_t)e->b_pad);
     slab.add(&e->ctrl, 1);
@@ -920,6 +919,7 @@ static int prepare(galois_engine *e)
     ENG_CUDA(e, use_pool_for_device(e->device));
     ENG_CUDA(e, cudaMallocAsync(&e->slab, slab.total(), e->stream));
     slab.assign(e->slab);
+    e->R = e->X + 4;
     ENG_CUDA(e, cudaMemsetAsync(e->unsat, 0, sizeof(int32_t) * (size_t)e->b_pad, e->stream));
     ENG_CUDA(e, cudaMemsetAsync(e->unsat_last, 0, sizeof(int32_t) * (size_t)e->b_pad, e->stream));
     ENG_CUDA(e, cudaMemsetAsync(e->best_bits, 0, (size_t)n, e->stream));
@@ -1504,17 +1504,17 @@ extern "C" int galois_engine_get_bits(galois_engine *e, uint8_t *x_next, uint8_t
     if (int rc = prepare(e)) return rc;
     WHOLE_SLICE_ONLY(e);
     const int32_t n = e->cnf->n;
-    std::vector<uint32_t> tmp((size_t)n * e->W);
+    std::vector<uint32_t> tmp((size_t)n * 2 * xr_pad(e->W));
+    ENG_CUDA(e, cudaMemcpyAsync(tmp.data(), e->X, tmp.size() * 4, cudaMemcpyDeviceToHost, e->stream));
+    ENG_CUDA(e, cudaStreamSynchronize(e->stream));
     uint8_t *outs[2] = {x_next, r};
-    uint32_t *srcs[2] = {e->X, e->R};
     for (int a = 0; a < 2; ++a) {
         if (!outs[a]) continue;
-        ENG_CUDA(e, cudaMemcpyAsync(tmp.data(), srcs[a], tmp.size() * 4, cudaMemcpyDeviceToHost, e->stream));
-        ENG_CUDA(e, cudaStreamSynchronize(e->stream));
+        const uint32_t *base = tmp.data() + 4 * a;   // R = X + 4 words
         for (int32_t b = 0; b < e->b_loc; ++b)
             for (int32_t v = 0; v < n; ++v)
                 outs[a][(size_t)b * n + v] =   // member i of a word at bit 8 (i mod 4) + i / 4
-                    (uint8_t)((tmp[(size_t)v * e->W + (b >> 5)] >> (((b & 3) << 3) | ((b & 31) >> 2))) & 1u);
+                    (uint8_t)((base[xr_at(v, b >> 5, e->W)] >> (((b & 3) << 3) | ((b & 31) >> 2))) & 1u);
     }
     return GALOIS_OK;
 }

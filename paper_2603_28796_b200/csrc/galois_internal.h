@@ -6,8 +6,11 @@
 //   CSC  code_off[2n+1] int32: occurrences of literal code c are CSC positions
 //        [code_off[c], code_off[c+1]), ascending slot order (stable counting sort)
 //   state z, m, v float [n][b_pad]  (reduced iterate z = theta_1 - theta_0)
-//   bits  X, R uint32 [n][W]        (word w holds members 32w..32w+31; member 32w + i at
-//                                    bit 8 (i mod 4) + i / 4 — see device_utils.cuh bitpos)
+//   bits  X, R interleaved in one array: row v = 2 WP words (WP = W rounded up to 4),
+//         16-byte groups alternating X words 4g..4g+3 and R words 4g..4g+3, R = X + 4 words
+//         (xr_at); a sweep lane's X and R vectors of a literal are one 32-byte sector.
+//         Word w holds members 32w..32w+31; member 32w + i at bit 8 (i mod 4) + i / 4
+//         (device_utils.cuh bitpos)
 //   E     uint32 [L][W] in CSC order (exclusive products of each occurrence); the row of a
 //         NEGATIVE occurrence is stored complemented, so the signed signal of a variable is
 //         (sum of all its row bits) - (number of its negative rows) — one count pass
@@ -21,6 +24,13 @@
 namespace galois {
 
 constexpr int kHubDegree = 256;      // variables with more occurrences use the hub path
+
+// word w of row v of the interleaved X/R array (apply to X for X words, to R = X + 4 for R)
+__host__ __device__ __forceinline__ int32_t xr_pad(int32_t W) { return (W + 3) & ~3; }
+__host__ __device__ __forceinline__ size_t xr_at(int32_t v, int32_t w, int32_t W)
+{
+    return (size_t)v * 2 * (size_t)xr_pad(W) + ((size_t)(w >> 2) << 3) + (size_t)(w & 3);
+}
 constexpr int kHubChunk = 128;       // occurrences per hub partial item (|partial| <= 128: int16)
 
 // Device-side control block (one per engine, device memory).

@@ -152,8 +152,8 @@ __global__ void __launch_bounds__(256) k_update_soft(DevCnf c, StepParams p, flo
         // 32 consecutive members of one row form one word (b_pad is a multiple of 32)
         const uint32_t rw = __ballot_sync(0xffffffffu, rb), xw = __ballot_sync(0xffffffffu, xb);
         if (lane == 0) {
-            R[(size_t)v * p.W + (b >> 5)] = rw;
-            X[(size_t)v * p.W + (b >> 5)] = xw;
+            R[xr_at(v, b >> 5, p.W)] = rw;
+            X[xr_at(v, b >> 5, p.W)] = xw;
         }
     }
     if (bad) atomicOr(&ctrl->nonfinite, 1);

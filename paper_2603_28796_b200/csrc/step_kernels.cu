@@ -73,8 +73,8 @@ __global__ void __launch_bounds__(256) k_init(StepParams p, float4 *__restrict__
         const uint32_t act = QW - qb >= 32u ? 0xffffffffu : ((1u << (QW - qb)) - 1u);
         const uint32_t xw = pack_quads(xn, lane, act), rw = pack_quads(rn, lane, act);
         if ((lane & 7) == 0) {
-            X[(size_t)v * p.W + (q >> 3)] = xw;
-            R[(size_t)v * p.W + (q >> 3)] = rw;
+            X[xr_at(v, (int32_t)(q >> 3), p.W)] = xw;
+            R[xr_at(v, (int32_t)(q >> 3), p.W)] = rw;
         }
     }
 }
@@ -108,8 +108,8 @@ __global__ void __launch_bounds__(256) k_resample(StepParams p, const float4 *__
         const uint32_t act = QW - qb >= 32u ? 0xffffffffu : ((1u << (QW - qb)) - 1u);
         const uint32_t xw = pack_quads(xn, lane, act), rw = pack_quads(rn, lane, act);
         if ((lane & 7) == 0) {
-            X[(size_t)v * p.W + (q >> 3)] = xw;
-            R[(size_t)v * p.W + (q >> 3)] = rw;
+            X[xr_at(v, (int32_t)(q >> 3), p.W)] = xw;
+            R[xr_at(v, (int32_t)(q >> 3), p.W)] = rw;
         }
     }
 }
@@ -148,7 +148,7 @@ __global__ void __launch_bounds__(256) k_clauses_st(DevCnf c, int32_t W, int32_t
         for (int i = 0; i < 8; ++i) {
             if (i < width) {
                 const int2 si = c.slot_info[lo + i];
-                const uint32_t s = bits[(size_t)(si.x >> 1) * W + word] ^ (0u - (uint32_t)(si.x & 1));
+                const uint32_t s = bits[xr_at(si.x >> 1, word, W)] ^ (0u - (uint32_t)(si.x & 1));
                 S[i] = s;
                 two |= any & s;
                 any |= s;
@@ -157,7 +157,7 @@ __global__ void __launch_bounds__(256) k_clauses_st(DevCnf c, int32_t W, int32_t
         for (int i = 8; i < width; ++i) {
             if (!kForward && any == 0xFFFFFFFFu) break;   // every member already satisfied
             const int2 si = c.slot_info[lo + i];
-            const uint32_t s = bits[(size_t)(si.x >> 1) * W + word] ^ (0u - (uint32_t)(si.x & 1));
+            const uint32_t s = bits[xr_at(si.x >> 1, word, W)] ^ (0u - (uint32_t)(si.x & 1));
             two |= any & s;
             any |= s;
         }
@@ -174,7 +174,7 @@ __global__ void __launch_bounds__(256) k_clauses_st(DevCnf c, int32_t W, int32_t
                 }
             for (int i = 8; i < width; ++i) {
                 const int2 si = c.slot_info[lo + i];
-                const uint32_t s = bits[(size_t)(si.x >> 1) * W + word] ^ (0u - (uint32_t)(si.x & 1));
+                const uint32_t s = bits[xr_at(si.x >> 1, word, W)] ^ (0u - (uint32_t)(si.x & 1));
                 Ec[(size_t)si.y * LW] = (~any | (s & ~two)) ^ (0u - (uint32_t)(si.x & 1));
             }
         }
@@ -216,7 +216,7 @@ __global__ void k_extract(const uint32_t *__restrict__ R, int32_t n, int32_t W, 
     if (!ctrl->improved) return;
     const int64_t lb = ctrl->best_b - b0;
     for (int32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
-        best_bits[v] = (uint8_t)((R[(size_t)v * W + (lb >> 5)] >> bitpos((int)(lb & 31))) & 1u);
+        best_bits[v] = (uint8_t)((R[xr_at(v, (int32_t)(lb >> 5), W)] >> bitpos((int)(lb & 31))) & 1u);
 }
 
 // ------------------------------------------------------------------ launch wrappers

@@ -314,8 +314,8 @@ __global__ void __launch_bounds__(256) k_update_st(DevCnf c, StepParams p, RowMa
         // 8 lanes = one 32-bit word; validity is uniform within each group of 8 lanes
         const uint32_t xw = pack_quads(xn, lane), rw = pack_quads(rn, lane);
         if (ip.valid && (lane & 7) == 0) {
-            X[(size_t)v * p.W + (q >> 3)] = xw;
-            R[(size_t)v * p.W + (q >> 3)] = rw;
+            X[xr_at(v, (int32_t)(q >> 3), p.W)] = xw;
+            R[xr_at(v, (int32_t)(q >> 3), p.W)] = rw;
         }
     }
     if (bad) atomicOr(&ctrl->nonfinite, 1);
@@ -467,8 +467,8 @@ __global__ void __launch_bounds__(256 + 32, kTmaCtasPerSm) k_update_tma(DevCnf c
         }
         const uint32_t xw = pack_quads(xn, lane), rw = pack_quads(rn, lane);
         if ((lane & 7) == 0) {
-            X[(size_t)v * p.W + (q >> 3)] = xw;
-            R[(size_t)v * p.W + (q >> 3)] = rw;
+            X[xr_at(v, (int32_t)(q >> 3), p.W)] = xw;
+            R[xr_at(v, (int32_t)(q >> 3), p.W)] = rw;
         }
     }
     if (bad) atomicOr(&ctrl->nonfinite, 1);
