@@ -351,7 +351,7 @@ __global__ void __launch_bounds__(256 + 32, kTmaCtasPerSm) k_update_tma(DevCnf c
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ uint64_t full[kStages], empty[kStages];
     __shared__ StageHdr hdr[kStages];
-    __shared__ int32_t hflags[kStages];    // bit 0 first piece, bit 1 last piece, bit 2 hub
+    __shared__ int32_t hflags[kStages];    // bit 0 first piece, bit 1 last piece, bit 2 hub, bit 3 pinned
     if (ctrl->stopped) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t QW = rm.QW;
@@ -373,6 +373,7 @@ __global__ void __launch_bounds__(256 + 32, kTmaCtasPerSm) k_update_tma(DevCnf c
                 const uint32_t v = div_cpr(rm, item), ch = item - v * rm.cpr;
                 const int32_t k0 = c.code_off[2 * v], k1 = c.code_off[2 * v + 1], k2 = c.code_off[2 * v + 2];
                 const bool hub = c.num_hubs > 0 && c.hub_of_var[v] >= 0;
+                const bool pinned = kPins && p.pin_rank[v] >= 0;   // cube pin: read once, by the producer
                 const int32_t pieces = hub ? 1 : max(1, (k2 - k0 + kStageRows - 1) / kStageRows);
                 const size_t off = (size_t)v * QW + (size_t)ch * 256u;
                 const uint32_t *Ech = E + (size_t)ch * c.L * 32u;
@@ -385,7 +386,7 @@ __global__ void __launch_bounds__(256 + 32, kTmaCtasPerSm) k_update_tma(DevCnf c
                     const int32_t r0 = hub ? k0 : k0 + pc * kStageRows;
                     const int32_t r1 = hub ? k0 : min(k2, r0 + kStageRows);
                     hdr[st] = StageHdr{(int32_t)v, k1, r0, r1};
-                    hflags[st] = (pc == 0 ? 1 : 0) | (pc == pieces - 1 ? 2 : 0) | (hub ? 4 : 0);
+                    hflags[st] = (pc == 0 ? 1 : 0) | (pc == pieces - 1 ? 2 : 0) | (hub ? 4 : 0) | (pinned ? 8 : 0);
                     const uint32_t ebytes = (uint32_t)(r1 - r0) * 128u;
                     const uint32_t fb = full_s + 8u * st, sbs = stage_s + (uint32_t)(st * kStageBytes);
                     mbar_arrive_expect_tx_s(fb, (pc == 0 ? 3u * 4096u : 0u) + ebytes);
@@ -452,7 +453,7 @@ __global__ void __launch_bounds__(256 + 32, kTmaCtasPerSm) k_update_tma(DevCnf c
         xn = (uint32_t)G[0] & 15u; rn = __float_as_uint(z.x) & 15u; (void)bq; (void)g1o;
         z.x += 1.0f; m.x += 1.0f; vv.x += 1.0f;
 #else
-        if (kPins && p.pin_rank[v] >= 0)
+        if (kPins && (flags & 8))
             quad_update<kTau1, kAdam, true>(p, ac, v, bq, s, G, z, m, vv, xn, rn, g1o, bad);
         else
             quad_update<kTau1, kAdam, false>(p, ac, v, bq, s, G, z, m, vv, xn, rn, g1o, bad);
