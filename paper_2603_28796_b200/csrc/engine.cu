@@ -136,16 +136,16 @@ struct galois_cnf {
         int cur = 0;
         cudaGetDevice(&cur);
         cudaSetDevice(device);
-        cudaFree(clause_off);
-        cudaFree(clause_perm);
-        cudaFree(sweep_off);
-        cudaFree(sweep_slot);
-        cudaFree(slot_info);
-        cudaFree(code_off);
-        cudaFree(occ_slot);
-        cudaFree(hub_of_var);
-        cudaFree(hub_chunk_off);
-        cudaFree(hub_chunk);
+        cudaFreeAsync(clause_off, 0);
+        cudaFreeAsync(clause_perm, 0);
+        cudaFreeAsync(sweep_off, 0);
+        cudaFreeAsync(sweep_slot, 0);
+        cudaFreeAsync(slot_info, 0);
+        cudaFreeAsync(code_off, 0);
+        cudaFreeAsync(occ_slot, 0);
+        cudaFreeAsync(hub_of_var, 0);
+        cudaFreeAsync(hub_chunk_off, 0);
+        cudaFreeAsync(hub_chunk, 0);
         cudaSetDevice(cur);
     }
 };
@@ -225,12 +225,15 @@ static cudaError_t use_pool_for_device(int device)
     return e;
 }
 
+// CNF buffers come from the device's stream-ordered pool (cudaMallocAsync on the build
+// stream; freed with cudaFreeAsync): repeated load / normalise / free is a pool hit instead
+// of a driver allocation with an implicit device synchronisation.
 template <typename T>
-static cudaError_t dmalloc(T **p, size_t count)
+static cudaError_t dmalloc(T **p, size_t count, cudaStream_t st)
 {
     *p = nullptr;
     if (count == 0) count = 1;
-    return cudaMalloc((void **)p, count * sizeof(T));
+    return cudaMallocAsync((void **)p, count * sizeof(T), st);
 }
 
 // Build a device CNF from device-resident DIMACS CSR arrays (d_off64 [m+1], d_lits [L]),
@@ -248,11 +251,11 @@ static int cnf_build_device(int dev, int32_t num_vars, int64_t num_clauses, int6
     int32_t *d_err = nullptr;
     void *d_scratch = nullptr;
     auto cleanup = [&]() {
+        cudaFreeAsync(d_off64, st);
+        cudaFreeAsync(d_lits, st);
+        cudaFreeAsync(d_err, st);
+        cudaFreeAsync(d_scratch, st);
         cudaStreamSynchronize(st);
-        cudaFree(d_off64);
-        cudaFree(d_lits);
-        cudaFree(d_err);
-        cudaFree(d_scratch);
     };
     auto bail = [&](int code, const std::string &msg) {
         cleanup();
@@ -267,14 +270,14 @@ static int cnf_build_device(int dev, int32_t num_vars, int64_t num_clauses, int6
                         std::string(#expr) + ": " + cudaGetErrorString(_e));                             \
     } while (0)
 
-    LOAD_TRY(dmalloc(&d_err, 8));
-    LOAD_TRY(dmalloc(&c->clause_off, (size_t)m + 1));
-    LOAD_TRY(dmalloc(&c->clause_perm, (size_t)m));
-    LOAD_TRY(dmalloc(&c->slot_info, (size_t)L));
-    LOAD_TRY(dmalloc(&c->code_off, 2 * (size_t)num_vars + 1));
-    LOAD_TRY(dmalloc(&c->occ_slot, (size_t)L));
+    LOAD_TRY(dmalloc(&d_err, 8, st));
+    LOAD_TRY(dmalloc(&c->clause_off, (size_t)m + 1, st));
+    LOAD_TRY(dmalloc(&c->clause_perm, (size_t)m, st));
+    LOAD_TRY(dmalloc(&c->slot_info, (size_t)L, st));
+    LOAD_TRY(dmalloc(&c->code_off, 2 * (size_t)num_vars + 1, st));
+    LOAD_TRY(dmalloc(&c->occ_slot, (size_t)L, st));
     const size_t scratch = build_cnf_scratch_bytes(num_vars, std::max<int64_t>(L, m));
-    LOAD_TRY(cudaMalloc(&d_scratch, scratch));
+    LOAD_TRY(cudaMallocAsync(&d_scratch, scratch, st));
     const int32_t h_err_init[8] = {0, INT32_MAX, INT32_MAX, INT32_MAX, 0, 0, 0, 0};
     LOAD_TRY(cudaMemcpyAsync(d_err, h_err_init, sizeof(h_err_init), cudaMemcpyHostToDevice, st));
     LOAD_TRY(launch_build_cnf(num_vars, m, L, d_off64, d_lits, c->clause_off, c->slot_info, c->code_off,
@@ -298,14 +301,15 @@ static int cnf_build_device(int dev, int32_t num_vars, int64_t num_clauses, int6
         return bail(GALOIS_E_VAR_RANGE, buf);
     }
     c->max_width = h_err[4];
-    LOAD_TRY(dmalloc(&c->sweep_off, (size_t)m + 1));
-    LOAD_TRY(dmalloc(&c->sweep_slot, (size_t)std::max<int64_t>(L, 1)));
+    LOAD_TRY(dmalloc(&c->sweep_off, (size_t)m + 1, st));
+    LOAD_TRY(dmalloc(&c->sweep_slot, (size_t)std::max<int64_t>(L, 1), st));
     LOAD_TRY(launch_sweep_order(m, c->clause_off, c->clause_perm, c->slot_info, c->sweep_off, c->sweep_slot,
                                 (int32_t *)d_scratch, st));
 
     // hub table: variables with more than kHubDegree occurrences are reduced in chunks
     std::vector<int32_t> code_off(2 * (size_t)num_vars + 1);
-    LOAD_TRY(cudaMemcpy(code_off.data(), c->code_off, code_off.size() * 4, cudaMemcpyDeviceToHost));
+    LOAD_TRY(cudaMemcpyAsync(code_off.data(), c->code_off, code_off.size() * 4, cudaMemcpyDeviceToHost, st));
+    LOAD_TRY(cudaStreamSynchronize(st));
     std::vector<int32_t> hub_of_var(num_vars, -1), hub_chunk_off(1, 0);
     std::vector<int2> hub_chunk;
     for (int32_t v = 0; v < num_vars; ++v) {
@@ -320,12 +324,15 @@ static int cnf_build_device(int dev, int32_t num_vars, int64_t num_clauses, int6
     }
     c->num_hub_chunks = (int32_t)hub_chunk.size();
     if (c->num_hubs > 0) {
-        LOAD_TRY(dmalloc(&c->hub_of_var, (size_t)num_vars));
-        LOAD_TRY(dmalloc(&c->hub_chunk_off, hub_chunk_off.size()));
-        LOAD_TRY(dmalloc(&c->hub_chunk, hub_chunk.size()));
-        LOAD_TRY(cudaMemcpy(c->hub_of_var, hub_of_var.data(), hub_of_var.size() * 4, cudaMemcpyHostToDevice));
-        LOAD_TRY(cudaMemcpy(c->hub_chunk_off, hub_chunk_off.data(), hub_chunk_off.size() * 4, cudaMemcpyHostToDevice));
-        LOAD_TRY(cudaMemcpy(c->hub_chunk, hub_chunk.data(), hub_chunk.size() * sizeof(int2), cudaMemcpyHostToDevice));
+        LOAD_TRY(dmalloc(&c->hub_of_var, (size_t)num_vars, st));
+        LOAD_TRY(dmalloc(&c->hub_chunk_off, hub_chunk_off.size(), st));
+        LOAD_TRY(dmalloc(&c->hub_chunk, hub_chunk.size(), st));
+        LOAD_TRY(cudaMemcpyAsync(c->hub_of_var, hub_of_var.data(), hub_of_var.size() * 4, cudaMemcpyHostToDevice, st));
+        LOAD_TRY(cudaMemcpyAsync(c->hub_chunk_off, hub_chunk_off.data(), hub_chunk_off.size() * 4,
+                                 cudaMemcpyHostToDevice, st));
+        LOAD_TRY(cudaMemcpyAsync(c->hub_chunk, hub_chunk.data(), hub_chunk.size() * sizeof(int2), cudaMemcpyHostToDevice,
+                                 st));
+        LOAD_TRY(cudaStreamSynchronize(st));   // the host vectors go out of scope
     }
 #undef LOAD_TRY
     cleanup();
@@ -350,17 +357,19 @@ extern "C" int galois_cnf_load(int32_t num_vars, int64_t num_clauses, const int6
     cudaStream_t st = nullptr;
     int64_t *d_off64 = nullptr;
     int32_t *d_lits = nullptr;
+    CUDA_TRY(use_pool_for_device(dev));
     CUDA_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-    cudaError_t ce = dmalloc(&d_off64, (size_t)num_clauses + 1);
-    if (ce == cudaSuccess) ce = dmalloc(&d_lits, (size_t)L);
+    cudaError_t ce = dmalloc(&d_off64, (size_t)num_clauses + 1, st);
+    if (ce == cudaSuccess) ce = dmalloc(&d_lits, (size_t)L, st);
     if (ce == cudaSuccess)
         ce = cudaMemcpyAsync(d_off64, clause_offsets, sizeof(int64_t) * (size_t)(num_clauses + 1),
                              cudaMemcpyHostToDevice, st);
     if (ce == cudaSuccess && L > 0)
         ce = cudaMemcpyAsync(d_lits, literals, sizeof(int32_t) * (size_t)L, cudaMemcpyHostToDevice, st);
     if (ce != cudaSuccess) {
-        cudaFree(d_off64);
-        cudaFree(d_lits);
+        cudaFreeAsync(d_off64, st);
+        cudaFreeAsync(d_lits, st);
+        cudaStreamSynchronize(st);
         cudaStreamDestroy(st);
         return fail(ce == cudaErrorMemoryAllocation ? GALOIS_E_OOM : GALOIS_E_CUDA,
                     std::string("cnf upload: ") + cudaGetErrorString(ce));
@@ -391,8 +400,9 @@ extern "C" int galois_cnf_normalize(const galois_cnf *in, int32_t k, galois_cnf 
     cudaError_t ce = launch::tseitin(in->clause_off, in->slot_info, in->m, in->n, k, &d_off, &d_lits, &m2, &aux, st);
     if (ce == cudaSuccess && (int64_t)in->n + aux >= (1 << 30)) ce = cudaErrorInvalidValue;
     if (ce != cudaSuccess) {
-        cudaFree(d_off);
-        cudaFree(d_lits);
+        cudaFreeAsync(d_off, st);
+        cudaFreeAsync(d_lits, st);
+        cudaStreamSynchronize(st);
         cudaStreamDestroy(st);
         return fail(ce == cudaErrorMemoryAllocation ? GALOIS_E_OOM : GALOIS_E_CUDA,
                     std::string("normalize: ") + cudaGetErrorString(ce));

@@ -111,8 +111,8 @@ cudaError_t tseitin(const int32_t *clause_off, const int2 *slot_info, int64_t m,
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     const int64_t m2 = tot[0];
     if (e == cudaSuccess && m2 * (int64_t)k >= INT32_MAX) e = cudaErrorInvalidValue;
-    if (e == cudaSuccess) e = cudaMalloc((void **)d_off_out, sizeof(int64_t) * (size_t)(m2 + 1));
-    if (e == cudaSuccess) e = cudaMalloc((void **)d_lits_out, sizeof(int32_t) * (size_t)(m2 * k > 0 ? m2 * k : 1));
+    if (e == cudaSuccess) e = cudaMallocAsync((void **)d_off_out, sizeof(int64_t) * (size_t)(m2 + 1), st);
+    if (e == cudaSuccess) e = cudaMallocAsync((void **)d_lits_out, sizeof(int32_t) * (size_t)(m2 * k > 0 ? m2 * k : 1), st);
     if (e == cudaSuccess) {
         k_fixed_offsets<<<grid_of(m2 + 1), 256, 0, st>>>(m2, k, *d_off_out);
         if (m > 0) k_tseitin_write<<<grid_of(m), 256, 0, st>>>(clause_off, slot_info, m, n, k, q, a, *d_lits_out);
