@@ -1,21 +1,20 @@
-// step_kernels.cu — rows a3-a8 of SURVEY §8 (straight-through mode, the paper's).
+// step_kernels.cu — rows a3, a5/a8 (small batches) and a8-a9 of SURVEY §8 (straight-
+// through mode, the paper's).
 //
 //   k_init        a3  theta ~ N(0,1) -> z0 = theta_1 - theta_0 (fp64 Box-Muller), first
 //                     sample X_1 and rounding R_0
-//   k_forward_st  a5  clause polynomial on bit-packed samples: U = AND of false-literal
-//                     words, exclusive products E = ~any | (S_i & ~atleast2) written in CSC
-//                     order, Lambda_b = popcount of U per member
-//   k_hub_partial a6  deterministic chunked partial sums of the signal for hub variables
-//   k_update_st   a6+a7 fused: per-variable segmented reduction of the signal G from E
-//                     (no atomics), straight-through gradient, Adam, rounding R_t, next
-//                     sample X_{t+1}
-//   k_check       a8  exact checker on R: per-member unsat counts
+//   k_resample        R_t and X_{t+1} from an injected iterate (set_iterate test hook)
+//   k_clauses_st  a5/a8 the scalar clause sweep for batches whose word count W is not a
+//                     multiple of 4 (b_pad < 1024 padded to 32): U = AND of false-literal
+//                     words, exclusive products E = ~any | (S_i & ~atleast2) in CSC order
+//                     (negative occurrences complemented), per-member counts of U
 //   k_best / k_finalize / k_extract  a8-a9 best tracking and the winner's bits
+// (the sweep for b_pad >= 1024 is k_sweep in clause_kernels.cu, the update in
+// update_kernels.cu)
 //
 // Thread mapping of the per-variable kernels: one thread per QUAD = 4 consecutive members
 // of one variable row (float4 state loads, one Philox call per quad); 8 quads form one
-// 32-bit word of the packed bits. Clause kernels: one lane per (clause, batch word), the
-// lanes of a warp reading consecutive words of the same variable row (128 B coalesced).
+// 32-bit word of the packed bits (member-in-word layout: device_utils.cuh bitpos).
 #include <cuda_runtime.h>
 
 #include <cstdint>

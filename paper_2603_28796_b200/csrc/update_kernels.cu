@@ -2,7 +2,8 @@
 //
 // For every variable v and member b (one thread per QUAD of 4 members):
 //   a6  G_v,b = sum over the occurrences of v of sigma * E   (segmented, CSC order:
-//       positive codes, then negative; integer, no atomics -> deterministic)
+//       positive codes, then negative; integer, no atomics -> deterministic; negative
+//       rows are stored complemented, so G = sum of all row bits - negative row count)
 //   a7  g1 = -G p q / tau (straight-through, Eq.4 text P:160; p q = sigma(a) sigma(-a)),
 //       Adam (App. A) on the reduced iterate z = theta_1 - theta_0, rounding
 //       R_t = [z >= 0], next sample X_{t+1} = [z + ell_{t+1} >= 0] (Eq.3-4).
@@ -37,9 +38,9 @@ constexpr int kStageE = kStageRows * 128;
 constexpr int kStageBytes = kStageE + 3 * 4096;   // E rows + z, m, v of 256 quads
 constexpr int kTmaSmem = kStages * kStageBytes;
 
-// Count the E bits of one quad (bits sh..sh+3 of column `col`, row stride CW words) over
+// Count the E bits of one quad (bits qp + 8j of column `col`, row stride CW words) over
 // occurrences [k0, k1): kBatch independent predicated loads per round trip; four 8-bit
-// counters in one register (spread4), flushed before they can overflow. Rows of negative
+// counters in one register (one bit per byte), flushed before they can overflow. Rows of negative
 // occurrences are stored complemented, so sum over all rows = G + (number of negative
 // rows): the callers subtract that count (one pass, no sign split).
 __device__ __forceinline__ void count_bits(const uint32_t *__restrict__ col, int32_t CW, int32_t k0, int32_t k1,
