@@ -43,10 +43,13 @@ inline PhiloxKeys philox_round_keys(uint64_t seed)
     return pk;
 }
 
+#ifndef GALOIS_PHILOX_ROUNDS_EXPERIMENT
+#define GALOIS_PHILOX_ROUNDS_EXPERIMENT 10   // timing experiment only: results differ from the oracle
+#endif
 __device__ __forceinline__ uint4 philox4x32_10(uint4 c, const PhiloxKeys &pk)
 {
 #pragma unroll
-    for (int r = 0; r < 10; ++r) {
+    for (int r = 0; r < GALOIS_PHILOX_ROUNDS_EXPERIMENT; ++r) {
         const uint64_t p0 = (uint64_t)0xD2511F53u * c.x;
         const uint64_t p1 = (uint64_t)0xCD9E8D57u * c.z;
         c = make_uint4((uint32_t)(p1 >> 32) ^ c.y ^ pk.k0[r], (uint32_t)p1, (uint32_t)(p0 >> 32) ^ c.w ^ pk.k1[r],
