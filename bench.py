@@ -314,6 +314,8 @@ def main():
     ap.add_argument("--tts", default=None, help="only measure time-to-first-SAT on this config's SAT set")
     ap.add_argument("--tts-seeds", type=int, default=10)
     ap.add_argument("--no-tts", action="store_true", help="skip the configs[0] time-to-first-SAT block")
+    ap.add_argument("--check-interval", type=int, default=1,
+                    help="exact check every K steps (SURVEY D.3 also reports K = 10 for C5)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -356,6 +358,7 @@ def main():
     cnf = G.Cnf.from_instance(inst)
     info = cnf.info()
     eng = G.Engine(cnf, B, T, 0.5, 0, cubes=inst.pins, stream=stream.cuda_stream, rank=rank, world=world,
+                   check_interval=args.check_interval,
                    nccl_id=nccl_id)
     eng.enqueue(args.warmup)
     torch.cuda.synchronize(dev)
@@ -406,8 +409,8 @@ def main():
     alg = {
         # E of non-hub occurrences (hubs: int16x4 partials) + z, m, v read/write + X, R + offsets
         "update": (L - L_hub) * W * 4 + hub_chunks * b_pad * 2 + 24 * n * b_pad + 2 * n * W * 4 + 4 * (2 * n + 1),
-        # fused sweep (check interval 1): gather X and R rows per slot, write E, sweep-order index
-        "forward": L * W * 4 * 3 + 8 * L + 4 * (inst.m + 1),
+        # sweep: gather X rows, write E, sweep-order index; every K-th sweep also gathers R
+        "forward": L * W * 4 * 2 + L * W * 4 / args.check_interval + 8 * L + 4 * (inst.m + 1),
         # E rows of hub occurrences read, int16x4 partials written
         "hub_partial": L_hub * W * 4 + hub_chunks * b_pad * 2,
     }
@@ -459,7 +462,7 @@ def main():
             "scaling": "weak", "vs_baseline": None, "dtype": "u32-bits+f32", "data": "synthetic",
             "config": {"workload": args.workload, "instance": WORKLOADS[args.workload]["desc"],
                        "global_batch": B, "batch_per_gpu": per_gpu, "n": n, "m": inst.m, "L": L,
-                       "check_interval": 1, "lr": 0.5, "tau": 1.0, "optimizer": "adam",
+                       "check_interval": args.check_interval, "lr": 0.5, "tau": 1.0, "optimizer": "adam",
                        "l2": l2_note,
                        "parallelism": f"dp{world} (batch sharding, NCCL MIN all-reduce of the best key per step)"},
             "roofline": {"bound": "hbm", "kernel": KNAME[dom],
