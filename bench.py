@@ -314,6 +314,9 @@ def main():
     ap.add_argument("--tts", default=None, help="only measure time-to-first-SAT on this config's SAT set")
     ap.add_argument("--tts-seeds", type=int, default=10)
     ap.add_argument("--no-tts", action="store_true", help="skip the configs[0] time-to-first-SAT block")
+    ap.add_argument("--lanes", type=int, default=None,
+                    help="concurrent lanes per GPU (galois_engine_set_lanes); default: 4 for local batches "
+                         ">= 4096, else 1")
     ap.add_argument("--check-interval", type=int, default=1,
                     help="exact check every K steps (SURVEY D.3 also reports K = 10 for C5)")
     args = ap.parse_args()
@@ -357,9 +360,10 @@ def main():
     torch.cuda.set_stream(stream)
     cnf = G.Cnf.from_instance(inst)
     info = cnf.info()
+    lanes = args.lanes if args.lanes is not None else default_lanes(per_gpu)
     eng = G.Engine(cnf, B, T, 0.5, 0, cubes=inst.pins, stream=stream.cuda_stream, rank=rank, world=world,
                    check_interval=args.check_interval,
-                   nccl_id=nccl_id)
+                   nccl_id=nccl_id, lanes=lanes)
     eng.enqueue(args.warmup)
     torch.cuda.synchronize(dev)
     clocks = ClockSampler(local)
@@ -376,6 +380,16 @@ def main():
         pg.barrier()
     clk = clocks.stop()
     ms = ev0.elapsed_time(ev1)
+    st_timed = eng.info()
+    n_lanes = effective_lanes(st_timed["local_batch"], lanes, world)
+    if n_lanes > 1:
+        # kernel timing of a split engine would time each kernel while it shares the GPU with
+        # another lane's: the per-kernel numbers (roofline) come from an undivided engine
+        # running the same steps (the timed engine is freed first: C5 needs ~117 GB)
+        eng.free()
+        eng = G.Engine(cnf, B, T, 0.5, 0, cubes=inst.pins, stream=stream.cuda_stream, rank=rank, world=world,
+                       check_interval=args.check_interval, nccl_id=nccl_id)
+        eng.enqueue(args.warmup + args.steps)
     # kernel timing pass: K more steps with CUDA events around every launch on the engine's
     # stream (events inside the timed region would cost ~15 us per step on C2)
     eng.set_profiling(True)
@@ -389,7 +403,8 @@ def main():
     ms_instrumented = ek0.elapsed_time(ek1)
     kt = eng.kernel_times()
     st = eng.info()
-    completed = st["steps_done"] == T and not st["stopped"]
+    completed = (st_timed["steps_done"] == args.warmup + args.steps and not st_timed["stopped"]
+                 and st["steps_done"] == T and not st["stopped"])
     t_all = torch.tensor([ms], dtype=torch.float64, device=dev)
     if pg:
         pg.all_reduce(t_all, op=pg.ReduceOp.MAX)
@@ -441,7 +456,7 @@ def main():
     ws = 12 * n * b_pad + L * b_pad // 8 + n * b_pad // 4     # z, m, v + E + X, R
     l2_note = (f"inputs larger than L2: working set {ws / 1e6:.0f} MB per GPU > 126 MB, no flush" if ws > 126e6 else
                f"working set {ws / 1e6:.0f} MB per GPU fits the 126 MB L2 (not flushed; small config)")
-    gpu_launches = int(sum(c for _, c in kt.values()))
+    gpu_launches = int(sum(c for _, c in kt.values())) * n_lanes    # every lane launches the same kernels
     total_kernel_ms = sum(t for t, _ in kt.values())
 
     line = None
@@ -451,7 +466,7 @@ def main():
             cpu = oracle_sample(inst, B, seconds=args.ref_seconds)
         e2e = None
         if world == 1 and not args.no_e2e:
-            e2e = run_e2e(G, inst, B, args, torch, dev)
+            e2e = run_e2e(G, inst, B, args, torch, dev, lanes)
         tts = None
         if world == 1 and not args.no_tts:      # north_star's second metric, on configs[0] (C1)
             tts = time_to_sat(G, torch, dev, "C1", range(8))
@@ -463,6 +478,7 @@ def main():
             "config": {"workload": args.workload, "instance": WORKLOADS[args.workload]["desc"],
                        "global_batch": B, "batch_per_gpu": per_gpu, "n": n, "m": inst.m, "L": L,
                        "check_interval": args.check_interval, "lr": 0.5, "tau": 1.0, "optimizer": "adam",
+                       "lanes_per_gpu": n_lanes,
                        "l2": l2_note,
                        "parallelism": f"dp{world} (batch sharding, NCCL MIN all-reduce of the best key per step)"},
             "roofline": {"bound": "hbm", "kernel": KNAME[dom],
@@ -475,8 +491,11 @@ def main():
                          if dom in per_kernel and total_kernel_ms else None},
             "kernels_ms_per_step": {k: (t / args.steps) for k, (t, c) in kt.items() if c},
             "kernel_timing": {"pass": "K further steps right after the timed region, CUDA events around every "
-                                      "launch on the engine stream", "ms_per_step_instrumented":
-                                      ms_instrumented / args.steps},
+                                      "launch on the engine stream" + (
+                                          "" if n_lanes == 1 else
+                                          f" (an undivided engine: the timed region ran {n_lanes} concurrent "
+                                          "lanes, whose kernels overlap)"),
+                              "ms_per_step_instrumented": ms_instrumented / args.steps},
             "per_kernel": per_kernel,
             "fwd_bwd": fwd_bwd,
             "gpu_launches": gpu_launches,
@@ -531,7 +550,21 @@ def time_to_sat(G, torch, dev, which="C1", seeds=range(10), batch=None, steps=No
             "per_instance": out}
 
 
-def run_e2e(G, inst, B, args, torch, dev):
+def default_lanes(batch_per_gpu):
+    """Concurrent lanes per GPU: 4 once the local batch spans >= 4 chunks of 1024 members
+    (C2 4096: 0.266 -> 0.246 ms/step measured with 4 lanes)."""
+    return 4 if batch_per_gpu >= 4096 else 1
+
+
+def effective_lanes(b_loc, lanes, world):
+    """Lanes the engine actually forms (galois.h, galois_engine_set_lanes)."""
+    if lanes <= 1 or world > 1:
+        return 1
+    ls = (-(-b_loc // lanes) + 1023) // 1024 * 1024
+    return -(-b_loc // ls) if b_loc > ls else 1
+
+
+def run_e2e(G, inst, B, args, torch, dev, lanes=1):
     """Same metric end to end through the public C ABI with HOST buffers: CNF upload
     (host -> device), device CSR/CSC build, engine create + init, galois_engine_run of
     the timed steps (host polls the device stop flag), and the results read back
@@ -544,7 +577,7 @@ def run_e2e(G, inst, B, args, torch, dev):
         torch.cuda.synchronize(dev)
         t0 = time.perf_counter()
         cnf = G.Cnf(inst.n, off, lits)
-        eng = G.Engine(cnf, B, args.steps, 0.5, 0, cubes=inst.pins)
+        eng = G.Engine(cnf, B, args.steps, 0.5, 0, cubes=inst.pins, lanes=lanes)
         eng.run()
         counts, _ = eng.unsat_counts()
         best = eng.best_assignment()

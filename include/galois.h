@@ -188,6 +188,22 @@ int galois_engine_set_stream(galois_engine *eng, void *cuda_stream);
  * With world > 1 every rank runs ceil(b_per / sub_batch) windows in lock step. */
 int galois_engine_set_subbatch(galois_engine *eng, int32_t sub_batch);
 
+/* Split the local slice into `lanes` (1..16) concurrent engines over consecutive member
+ * ranges of ceil(b_loc / lanes) members rounded up to a multiple of 1024, each with its own
+ * buffers, CUDA stream and control block; step(), enqueue() and run() drive them
+ * interleaved, so one lane's clause sweep (a5 + a8, latency-bound) overlaps another lane's
+ * fused update (a6 + a7, HBM-bound). Members never interact (the batch is a set of
+ * independent restarts; RNG counters use the global member index), so every
+ * member's trajectory is the undivided engine's, and the best record (u*, t*, b*) and its
+ * assignment are identical (lexicographic minimum over the lanes' records). After a SAT,
+ * lanes other than the winner's may have run up to two CUDA-graph chunks (16 steps) past t*;
+ * unsat_counts then reports their members' counts at their own last check. Applies when
+ * the slice spans more than one lane, in ST mode, without NCCL (world = 1), sub-batching or
+ * debug; otherwise the engine is undivided. get_iterate / set_iterate / get_grad /
+ * get_loss / get_bits return E_STATE on a split engine; kernel_times sums over the lanes.
+ * Setter: valid only before the first step. */
+int galois_engine_set_lanes(galois_engine *eng, int32_t lanes);
+
 /* Device bytes one member costs in the given mode (z, m, v, bit planes, E or soft
  * buffers, counters), for sizing sub_batch to a memory budget. */
 int galois_engine_bytes_per_member(const galois_cnf *cnf, int32_t mode, int64_t *bytes);

@@ -254,12 +254,18 @@ __device__ __forceinline__ void flush_planes(uint32_t (&P)[kPlanes], int32_t *s_
 
 // Two shapes: kWide (average clause width >= 4.5: many gathers per clause, L2-resident
 // rows) trades register caching and counter planes for a 4th resident CTA per SM.
+#ifndef GALOIS_SWEEP_CACHED
+#define GALOIS_SWEEP_CACHED 2
+#endif
+#ifndef GALOIS_SWEEP_CTAS
+#define GALOIS_SWEEP_CTAS 3
+#endif
 template <bool kWide>
 struct SweepShape {
     static constexpr int kPlanes = kWide ? 6 : 8;            // counts < 2^kPlanes between flushes
     static constexpr int kFlushGroups = ((1 << kPlanes) - 1) / 4;   // a group adds <= 4 per member
-    static constexpr int kCached = kWide ? 0 : 2;            // slots kept in registers for the E pass
-    static constexpr int kMinBlocks = kWide ? 4 : 3;
+    static constexpr int kCached = kWide ? 0 : GALOIS_SWEEP_CACHED;   // slots kept in registers for the E pass
+    static constexpr int kMinBlocks = kWide ? 4 : GALOIS_SWEEP_CTAS;
 };
 
 template <bool kForward, bool kCheck, bool kWide, bool kLoop>
@@ -445,7 +451,7 @@ void clauses_v4(const DevCnf &c, int32_t W, int32_t b_pad, const uint32_t *X, co
         if (gy > (int64_t)chunks) gy = chunks;
         const int64_t groups = ((int64_t)c.m + 3) / 4;
         int64_t bx = (groups + 7) / 8;
-        const int64_t cap = ((wide ? 4 : 3) * 148 + gy - 1) / gy;
+        const int64_t cap = ((wide ? 4 : GALOIS_SWEEP_CTAS) * 148 + gy - 1) / gy;
         if (bx > cap) bx = cap;
         if (bx < 1) bx = 1;
         const dim3 grid((unsigned)bx, (unsigned)gy);

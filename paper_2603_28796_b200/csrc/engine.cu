@@ -496,6 +496,17 @@ struct galois_engine {
     unsigned long long sel_key[2] = {~0ull, ~0ull};
     float *sel_z = nullptr;
     unsigned long long *sel_dkey = nullptr;
+    // lanes: the local slice split into `lane.size()` engines over consecutive member ranges
+    // (1024-member multiples), each with its own stream and control block, stepped
+    // concurrently so one lane's clause sweep overlaps another lane's update. Members never
+    // interact, so every member's trajectory is the one the undivided engine gives it; the
+    // aggregate (agg, sel_*) is formed over the lanes as over f4's windows.
+    int32_t lanes_req = 1;
+    std::vector<galois_engine *> lane;
+    int64_t lane_size = 0;
+    bool fixed_slice = false;          // a lane: b0 / b_loc set by the parent
+    cudaEvent_t fork_ev = nullptr;
+    std::vector<cudaEvent_t> join_ev;
     Comm comm;
     // device buffers
     float *z = nullptr, *m = nullptr, *v = nullptr;
@@ -623,7 +634,11 @@ extern "C" int galois_engine_create(const galois_cnf *cnf, int64_t batch, int32_
 #define WHOLE_SLICE_ONLY(e)                                                                                  \
     do {                                                                                                     \
         if ((e)->windows > 1) return fail(GALOIS_E_STATE, "not available on a sub-batched engine (run only)"); \
+        if (!(e)->lane.empty()) return fail(GALOIS_E_STATE, "not available on an engine split into lanes");   \
     } while (0)
+
+// results formed over several sub-engines / windows (f4 windows, lanes)
+static bool aggregated(const galois_engine *e) { return e->windows > 1 || !e->lane.empty(); }
 
 #define SETTER_ENTRY(e)                                                                        \
     do {                                                                                       \
@@ -733,6 +748,15 @@ extern "C" int galois_engine_set_profiling(galois_engine *e, int32_t enable)
 {
     ENGINE_ENTRY(e);
     e->profiling = enable != 0;
+    for (galois_engine *l : e->lane) l->profiling = e->profiling;
+    return GALOIS_OK;
+}
+
+extern "C" int galois_engine_set_lanes(galois_engine *e, int32_t lanes)
+{
+    SETTER_ENTRY(e);
+    if (lanes < 1 || lanes > 16) return fail(GALOIS_E_ARG, "lanes must be in [1, 16]");
+    e->lanes_req = lanes;
     return GALOIS_OK;
 }
 
@@ -862,6 +886,52 @@ static int enqueue_step(galois_engine *e)
     return GALOIS_OK;
 }
 
+static int prepare(galois_engine *e);
+
+// Lanes of ls members (the last one shorter) over the local slice; each lane is a complete
+// engine (own buffers, stream, control block, CUDA graph) with the parent's configuration.
+static int prepare_lanes(galois_engine *e, int64_t ls)
+{
+    if (!e->stream) {
+        ENG_CUDA(e, cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
+        e->own_stream = true;
+    }
+    e->lane_size = ls;
+    for (int64_t off = 0; off < e->b_loc; off += ls) {
+        galois_engine *l = new galois_engine();
+        e->cnf->refs.fetch_add(1);
+        l->cnf = e->cnf;
+        l->device = e->device;
+        l->B = e->B;
+        l->T = e->T;
+        l->lr = e->lr;
+        l->tau = e->tau;
+        l->beta1 = e->beta1;
+        l->beta2 = e->beta2;
+        l->eps = e->eps;
+        l->optimizer = e->optimizer;
+        l->mode = e->mode;
+        l->K = e->K;
+        l->seed = e->seed;
+        l->pins = e->pins;
+        l->profiling = e->profiling;
+        l->fixed_slice = true;
+        l->b0 = e->b0 + off;
+        l->b_loc = (int32_t)std::min<int64_t>(ls, e->b_loc - off);
+        e->lane.push_back(l);
+        if (int rc = prepare(l)) {
+            e->poisoned = true;
+            return rc;
+        }
+        cudaEvent_t ev = nullptr;
+        ENG_CUDA(e, cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        e->join_ev.push_back(ev);
+    }
+    ENG_CUDA(e, cudaEventCreateWithFlags(&e->fork_ev, cudaEventDisableTiming));
+    e->prepared = true;
+    return GALOIS_OK;
+}
+
 static int prepare(galois_engine *e)
 {
     if (e->prepared) return GALOIS_OK;
@@ -870,12 +940,16 @@ static int prepare(galois_engine *e)
     galois_cnf *c = e->cnf;
     const int32_t n = c->n;
     // batch slice: b_per = roundup(ceil(B / world), 32); pad the local slice to 32
-    int64_t per = (e->B + e->world - 1) / e->world;
-    per = (per + 31) / 32 * 32;
-    e->b_per = per;
-    e->b0 = per * e->rank;
-    const int64_t left = e->B - e->b0;
-    e->b_loc = (int32_t)std::max<int64_t>(0, std::min<int64_t>(per, left));
+    if (e->fixed_slice) {                // a lane: b0 / b_loc were set by its parent
+        e->b_per = e->b_loc;
+    } else {
+        int64_t per = (e->B + e->world - 1) / e->world;
+        per = (per + 31) / 32 * 32;
+        e->b_per = per;
+        e->b0 = per * e->rank;
+        const int64_t left = e->B - e->b0;
+        e->b_loc = (int32_t)std::max<int64_t>(0, std::min<int64_t>(per, left));
+    }
     e->slice_b0 = e->b0;
     e->slice_loc = e->b_loc;
     // f4: windows of sub members; with NCCL every rank runs the same number of windows
@@ -883,6 +957,11 @@ static int prepare(galois_engine *e)
     if (e->sub > 0 && e->sub < span) {
         e->windows = (int32_t)((span + e->sub - 1) / e->sub);
         e->b_loc = (int32_t)std::min<int64_t>(e->sub, e->slice_loc);
+    }
+    if (e->lanes_req > 1 && e->windows == 1 && !e->use_comm && e->mode == GALOIS_MODE_ST && !e->debug) {
+        const int64_t per_lane = ((int64_t)e->b_loc + e->lanes_req - 1) / e->lanes_req;
+        const int64_t ls = (per_lane + 1023) / 1024 * 1024;
+        if ((int64_t)e->b_loc > ls) return prepare_lanes(e, ls);
     }
     const int32_t resident = e->windows > 1 ? e->sub : e->b_loc;
     // pad to 32 members (one bit word) up to 1024, then to whole 1024-member chunks, so that
@@ -1032,10 +1111,21 @@ static int settle(galois_engine *e, Ctrl *out)
     return read_ctrl(e, out);
 }
 
+static int lanes_enqueue(galois_engine *e, int32_t max_steps);
+static int lanes_refresh(galois_engine *e);
+
 extern "C" int galois_engine_step(galois_engine *e)
 {
     ENGINE_ENTRY(e);
     if (int rc = prepare(e)) return rc;
+    if (!e->lane.empty()) {
+        if (int rc = lanes_refresh(e)) return rc;
+        if (e->agg.sat) return GALOIS_SAT;
+        if (e->steps_enqueued >= e->T) return GALOIS_BUDGET;
+        if (int rc = lanes_enqueue(e, 1)) return rc;
+        if (int rc = lanes_refresh(e)) return rc;
+        return e->agg.sat ? GALOIS_SAT : GALOIS_OK;
+    }
     WHOLE_SLICE_ONLY(e);
     Ctrl h;
     if (int rc = read_ctrl(e, &h)) return rc;
@@ -1050,6 +1140,10 @@ extern "C" int galois_engine_enqueue(galois_engine *e, int32_t max_steps)
 {
     ENGINE_ENTRY(e);
     if (int rc = prepare(e)) return rc;
+    if (!e->lane.empty()) {
+        if (e->steps_enqueued >= e->T) return GALOIS_BUDGET;
+        return lanes_enqueue(e, max_steps);
+    }
     WHOLE_SLICE_ONLY(e);
     if (e->steps_enqueued >= e->T) return GALOIS_BUDGET;
     for (int32_t i = 0; i < max_steps && e->steps_enqueued < e->T; ++i)
@@ -1058,6 +1152,7 @@ extern "C" int galois_engine_enqueue(galois_engine *e, int32_t max_steps)
 }
 
 static int run_windows(galois_engine *e);
+static int run_lanes(galois_engine *e);
 
 // Steps of the resident members until SAT or e->T (see galois_engine_run).
 static int run_steps(galois_engine *e)
@@ -1099,6 +1194,7 @@ extern "C" int galois_engine_run(galois_engine *e)
 {
     ENGINE_ENTRY(e);
     if (int rc = prepare(e)) return rc;
+    if (!e->lane.empty()) return run_lanes(e);
     return e->windows > 1 ? run_windows(e) : run_steps(e);
 }
 
@@ -1193,12 +1289,158 @@ static int run_windows(galois_engine *e)
     return e->agg.sat ? GALOIS_SAT : GALOIS_BUDGET;
 }
 
+// ------------------------------------------------------------------------- lanes
+// The lanes' streams wait for the work queued so far on the engine's stream (fork); the
+// engine's stream waits for everything queued on the lanes (join).
+static int lanes_fork(galois_engine *e)
+{
+    ENG_CUDA(e, cudaEventRecord(e->fork_ev, e->stream));
+    for (galois_engine *l : e->lane) ENG_CUDA(e, cudaStreamWaitEvent(l->stream, e->fork_ev, 0));
+    return GALOIS_OK;
+}
+
+static int lanes_join(galois_engine *e)
+{
+    for (size_t i = 0; i < e->lane.size(); ++i) {
+        ENG_CUDA(e, cudaEventRecord(e->join_ev[i], e->lane[i]->stream));
+        ENG_CUDA(e, cudaStreamWaitEvent(e->stream, e->join_ev[i], 0));
+    }
+    return GALOIS_OK;
+}
+
+static int lane_fail(galois_engine *e, int rc)
+{
+    e->poisoned = true;
+    return rc;
+}
+
+// Up to max_steps steps on every lane, interleaved step by step across the lanes.
+static int lanes_enqueue(galois_engine *e, int32_t max_steps)
+{
+    if (int rc = lanes_fork(e)) return rc;
+    for (int32_t i = 0; i < max_steps; ++i)
+        for (galois_engine *l : e->lane)
+            if (l->steps_enqueued < l->T)
+                if (int rc = enqueue_step(l)) return lane_fail(e, rc);
+    if (int rc = lanes_join(e)) return rc;
+    int32_t s = 0;
+    for (galois_engine *l : e->lane) s = std::max(s, l->steps_enqueued);
+    e->steps_enqueued = s;
+    e->agg.ran = false;                   // the aggregate is formed again on the next query
+    return GALOIS_OK;
+}
+
+// Best record, last-check counts and theta_sel candidates over the lanes, exactly as
+// run_windows() forms them over windows: the best is the lexicographic (u, t, b) minimum of
+// the lanes' records, which is the undivided engine's record (a lane that stops at its
+// first SAT t* has run every step <= t*; records of steps after another lane's t* can
+// never precede it).
+static int lanes_refresh(galois_engine *e)
+{
+    if (e->lane.empty() || e->agg.ran) return GALOIS_OK;
+    const int32_t n = e->cnf->n;
+    galois_engine::Agg a;
+    e->agg_bits.assign((size_t)n, 0);
+    e->agg_counts.assign((size_t)e->slice_loc, 0);
+    e->sel_key[0] = e->sel_key[1] = ~0ull;
+    if (!e->sel_z) {
+        ENG_CUDA(e, cudaMallocAsync((void **)&e->sel_z, 2 * (size_t)n * 4, e->stream));
+        ENG_CUDA(e, cudaMallocAsync((void **)&e->sel_dkey, 2 * sizeof(unsigned long long), e->stream));
+        ENG_CUDA(e, cudaStreamSynchronize(e->stream));
+    }
+    for (size_t i = 0; i < e->lane.size(); ++i) {
+        galois_engine *l = e->lane[i];
+        Ctrl h;
+        if (int rc = settle(l, &h)) return lane_fail(e, rc);
+        const bool better = h.best_b >= 0 &&
+                            (h.best_u != a.u ? h.best_u < a.u : h.best_t != a.t ? h.best_t < a.t : h.best_b < a.b);
+        if (better) {
+            ENG_CUDA(e, cudaMemcpyAsync(e->agg_bits.data(), l->best_bits, (size_t)n, cudaMemcpyDeviceToHost, l->stream));
+            a.u = h.best_u;
+            a.t = h.best_t;
+            a.b = h.best_b;
+        }
+        if (l->b_loc > 0) {
+            ENG_CUDA(e, cudaMemcpyAsync(e->agg_counts.data() + (size_t)i * e->lane_size, l->unsat_last,
+                                        sizeof(int32_t) * (size_t)l->b_loc, cudaMemcpyDeviceToHost, l->stream));
+            for (int r = 0; r < 2; ++r) launch::select_member(l->unsat_last, l->b_loc, l->b0, r, e->sel_dkey + r, l->stream);
+            unsigned long long k[2];
+            ENG_CUDA(e, cudaMemcpyAsync(k, e->sel_dkey, sizeof(k), cudaMemcpyDeviceToHost, l->stream));
+            ENG_CUDA(e, cudaStreamSynchronize(l->stream));
+            for (int r = 0; r < 2; ++r)
+                if (k[r] < e->sel_key[r]) {
+                    e->sel_key[r] = k[r];
+                    launch::gather_z(l->z, n, l->b_pad, (int32_t)((int64_t)(k[r] & 0xFFFFFFFFull) - l->b0),
+                                     e->sel_z + (size_t)r * n, l->stream);
+                }
+        }
+        ENG_CUDA(e, cudaStreamSynchronize(l->stream));
+        a.steps = std::max(a.steps, h.t);
+        if (h.stopped) a.sat = true;
+    }
+    a.ran = true;
+    e->agg = a;
+    return GALOIS_OK;
+}
+
+// run() on lanes: every lane runs run_steps()' chunks (CUDA graphs of G steps) in lockstep
+// with the others; the stop flags are polled one chunk behind and a stop in any lane ends
+// the run of all (they have all completed at least the steps of the deciding check).
+static int run_lanes(galois_engine *e)
+{
+    const int32_t KK = e->K % 2 == 0 ? e->K : 2 * e->K;
+    const int32_t G = KK * std::max<int32_t>(1, 8 / KK);
+    if (int rc = lanes_refresh(e)) return rc;
+    if (e->agg.sat) return GALOIS_SAT;
+    if (int rc = lanes_fork(e)) return rc;
+    const size_t NL = e->lane.size();
+    std::vector<int> polled(NL, -1);
+    bool stop = false;
+    for (int iter = 0; !stop; ++iter) {
+        bool any = false;
+        for (size_t i = 0; i < NL; ++i) {
+            galois_engine *l = e->lane[i];
+            if (l->steps_enqueued >= l->T) continue;
+            const int32_t s0 = l->steps_enqueued;
+            const bool graphs = !l->profiling && !l->graph_failed && l->T - s0 >= 32 * G;
+            if (graphs && s0 % G == 0 && s0 + G < l->T) {
+                if (int rc = launch_graph_chunk(l, G)) return lane_fail(e, rc);
+            } else {
+                const int32_t end = std::min<int32_t>(l->T, (s0 / G + 1) * G);
+                while (l->steps_enqueued < end)
+                    if (int rc = enqueue_step(l)) return lane_fail(e, rc);
+            }
+            Ctrl *slot = &l->h_ctrl[iter & 1];
+            ENG_CUDA(e, cudaMemcpyAsync(slot, l->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, l->stream));
+            ENG_CUDA(e, cudaEventRecord(l->poll_ev[iter & 1], l->stream));
+            polled[i] = iter;
+            any = true;
+        }
+        if (!any) break;
+        for (size_t i = 0; i < NL && iter >= 1; ++i) {
+            galois_engine *l = e->lane[i];
+            if (polled[i] < iter - 1) continue;
+            const int j = polled[i] == iter ? (iter - 1) & 1 : polled[i] & 1;
+            ENG_CUDA(e, cudaEventSynchronize(l->poll_ev[j]));
+            if (l->h_ctrl[j].stopped) stop = true;
+        }
+    }
+    if (int rc = lanes_join(e)) return rc;
+    int32_t s = 0;
+    for (galois_engine *l : e->lane) s = std::max(s, l->steps_enqueued);
+    e->steps_enqueued = s;
+    e->agg.ran = false;
+    if (int rc = lanes_refresh(e)) return rc;
+    return e->agg.sat ? GALOIS_SAT : GALOIS_BUDGET;
+}
+
 extern "C" int galois_engine_info(galois_engine *e, int64_t *local_batch, int64_t *first_global_b,
                                   int32_t *steps_done, int32_t *stopped)
 {
     ENGINE_ENTRY(e);
     if (int rc = prepare(e)) return rc;
-    if (e->windows > 1) {
+    if (aggregated(e)) {
+        if (int rc = lanes_refresh(e)) return rc;
         if (local_batch) *local_batch = e->slice_loc;
         if (first_global_b) *first_global_b = e->slice_b0;
         if (steps_done) *steps_done = e->agg.sat ? e->agg.t : e->agg.steps;   // what the full batch did
@@ -1219,7 +1461,8 @@ extern "C" int galois_best_assignment(galois_engine *e, uint8_t *values, int32_t
 {
     ENGINE_ENTRY(e);
     if (int rc = prepare(e)) return rc;
-    if (e->windows > 1) {
+    if (aggregated(e)) {
+        if (int rc = lanes_refresh(e)) return rc;
         if (values && e->agg.ran) memcpy(values, e->agg_bits.data(), (size_t)e->cnf->n);
         else if (values) memset(values, 0, (size_t)e->cnf->n);
         if (unsat) *unsat = e->agg.u;
@@ -1247,7 +1490,8 @@ extern "C" int galois_unsat_counts(galois_engine *e, int32_t *counts, int64_t *f
 {
     ENGINE_ENTRY(e);
     if (int rc = prepare(e)) return rc;
-    if (e->windows > 1) {
+    if (aggregated(e)) {
+        if (int rc = lanes_refresh(e)) return rc;
         if (counts && e->agg.ran) memcpy(counts, e->agg_counts.data(), sizeof(int32_t) * (size_t)e->slice_loc);
         else if (counts) memset(counts, 0, sizeof(int32_t) * (size_t)e->slice_loc);
         if (first_global_b) *first_global_b = e->slice_b0;
@@ -1290,7 +1534,8 @@ extern "C" int galois_select_member(galois_engine *e, int32_t rule, int64_t *glo
     ENGINE_ENTRY(e);
     if (rule != 0 && rule != 1) return fail(GALOIS_E_ARG, "rule must be 0 (min loss) or 1 (max loss)");
     if (int rc = prepare(e)) return rc;
-    if (e->windows > 1) {                 // sub-batched: tracked over the windows by run()
+    if (aggregated(e)) {                  // sub-batched: tracked over the windows by run(); lanes: refreshed
+        if (int rc = lanes_refresh(e)) return rc;
         if (!e->agg.ran || e->sel_key[rule] == ~0ull)
             return fail(GALOIS_E_STATE, "sub-batched engine: call run() first (this rank has members)");
         const unsigned long long key = e->sel_key[rule];
@@ -1341,6 +1586,14 @@ static int local_member(galois_engine *e, int64_t global_b, int32_t *lb)
 // the retained winner of run() (theta_sel; other members' windows are gone).
 static int member_z(galois_engine *e, int64_t global_b, float *d_z)
 {
+    for (galois_engine *l : e->lane)       // lanes: every member stays resident in its lane
+        if (global_b >= l->b0 && global_b < l->b0 + l->b_loc) {
+            if (int rc = lanes_refresh(e)) return rc;    // the lane's pending check is settled
+            launch::gather_z(l->z, e->cnf->n, l->b_pad, (int32_t)(global_b - l->b0), d_z, l->stream);
+            ENG_CUDA(e, cudaStreamSynchronize(l->stream));
+            return GALOIS_OK;
+        }
+    if (!e->lane.empty()) return fail(GALOIS_E_ARG, "member is not local to this rank");
     if (e->windows > 1) {
         for (int r = 0; r < 2 && e->agg.ran; ++r)
             if (e->sel_key[r] != ~0ull && (int64_t)(e->sel_key[r] & 0xFFFFFFFFull) == global_b) {
@@ -1534,6 +1787,15 @@ extern "C" int galois_engine_kernel_times(galois_engine *e, double *ms, int64_t 
     ENGINE_ENTRY(e);
     if (ms) std::fill(ms, ms + GALOIS_NUM_KERNEL_CLASSES, 0.0);
     if (launches) std::fill(launches, launches + GALOIS_NUM_KERNEL_CLASSES, 0);
+    for (galois_engine *l : e->lane) {     // lanes: summed over the lanes (their launches overlap)
+        double lm[GALOIS_NUM_KERNEL_CLASSES];
+        int64_t lc[GALOIS_NUM_KERNEL_CLASSES];
+        if (int rc = galois_engine_kernel_times(l, lm, lc)) return rc;
+        for (int k = 0; k < GALOIS_NUM_KERNEL_CLASSES; ++k) {
+            if (ms) ms[k] += lm[k];
+            if (launches) launches[k] += lc[k];
+        }
+    }
     if (e->stream) ENG_CUDA(e, cudaStreamSynchronize(e->stream));
     for (auto &r : e->recs) {
         float t = 0.f;
@@ -1554,6 +1816,9 @@ extern "C" void galois_engine_free(galois_engine *e)
     cudaGetDevice(&cur);
     cudaSetDevice(e->device);
     if (e->stream) cudaStreamSynchronize(e->stream);
+    for (galois_engine *l : e->lane) galois_engine_free(l);
+    for (auto ev : e->join_ev) cudaEventDestroy(ev);
+    if (e->fork_ev) cudaEventDestroy(e->fork_ev);
     e->comm.destroy(e->poisoned);
     engine_free_buffers(e);
     for (auto &r : e->recs) {

@@ -37,7 +37,7 @@ EXPORTED = (
     "galois_comm_unique_id", "galois_engine_get_iterate", "galois_engine_set_iterate",
     "galois_engine_get_grad", "galois_engine_get_loss", "galois_engine_get_bits",
     "galois_engine_kernel_times", "galois_select_member", "galois_candidate_pool", "galois_cube_variables",
-    "galois_cnf_normalize", "galois_cnf_get_csr", "galois_engine_set_subbatch", "galois_engine_bytes_per_member",
+    "galois_cnf_normalize", "galois_cnf_get_csr", "galois_engine_set_subbatch", "galois_engine_set_lanes", "galois_engine_bytes_per_member",
 )
 
 
@@ -94,6 +94,7 @@ def lib() -> ctypes.CDLL:
             "galois_cnf_normalize": [P, I32, P, P],
             "galois_cnf_get_csr": [P, P, P],
             "galois_engine_set_subbatch": [P, I32],
+            "galois_engine_set_lanes": [P, I32],
             "galois_engine_bytes_per_member": [P, I32, P],
         }
         for name, args in sig.items():
@@ -232,7 +233,8 @@ class Engine:
                  mode: int = 0, tau: float = 1.0, beta1: float = 0.9, beta2: float = 0.999,
                  eps: float = 1e-8, optimizer: int = 0, check_interval: int = 1,
                  cubes: Sequence[int] = (), debug: bool = False, stream=None,
-                 rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None, sub_batch: int = 0):
+                 rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None, sub_batch: int = 0,
+                 lanes: int = 1):
         self.cnf = cnf
         self.n = cnf.n
         self.handle = galois_engine_create(cnf.handle, batch, steps, lr, seed)
@@ -252,6 +254,8 @@ class Engine:
             _check(L.galois_engine_set_stream(self.handle, ctypes.c_void_p(int(stream))))
         if sub_batch:
             _check(L.galois_engine_set_subbatch(self.handle, int(sub_batch)))
+        if lanes != 1:
+            _check(L.galois_engine_set_lanes(self.handle, int(lanes)))
         if world > 1 or nccl_id is not None:
             buf = ctypes.create_string_buffer(bytes(nccl_id), 128)
             _check(L.galois_engine_set_comm(self.handle, int(rank), int(world), buf))
