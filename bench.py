@@ -344,13 +344,16 @@ def main():
         return 0
     pg = None
     nccl_id = None
+    def new_nccl_id():
+        obj = [G.galois_comm_unique_id() if rank == 0 else None]
+        pg.broadcast_object_list(obj, src=0)
+        return obj[0]
+
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
         pg = dist
-        obj = [G.galois_comm_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        nccl_id = obj[0]
+        nccl_id = new_nccl_id()
 
     inst = make_instance(args.workload)
     per_gpu = WORKLOADS[args.workload]["batch"]
@@ -388,7 +391,7 @@ def main():
         # running the same steps (the timed engine is freed first: C5 needs ~117 GB)
         eng.free()
         eng = G.Engine(cnf, B, T, 0.5, 0, cubes=inst.pins, stream=stream.cuda_stream, rank=rank, world=world,
-                       check_interval=args.check_interval, nccl_id=nccl_id)
+                       check_interval=args.check_interval, nccl_id=new_nccl_id() if pg else None)
         eng.enqueue(args.warmup + args.steps)
     # kernel timing pass: K more steps with CUDA events around every launch on the engine's
     # stream (events inside the timed region would cost ~15 us per step on C2)
@@ -558,9 +561,9 @@ def default_lanes(batch_per_gpu):
 
 def effective_lanes(b_loc, lanes, world):
     """Lanes the engine actually forms (galois.h, galois_engine_set_lanes)."""
-    if lanes <= 1 or world > 1:
+    if lanes <= 1:
         return 1
-    ls = (-(-b_loc // lanes) + 1023) // 1024 * 1024
+    ls = (-(-b_loc // lanes) + 1023) // 1024 * 1024     # (ranks hold equal slices in the bench)
     return -(-b_loc // ls) if b_loc > ls else 1
 
 

@@ -890,14 +890,18 @@ static int prepare(galois_engine *e);
 
 // Lanes of ls members (the last one shorter) over the local slice; each lane is a complete
 // engine (own buffers, stream, control block, CUDA graph) with the parent's configuration.
-static int prepare_lanes(galois_engine *e, int64_t ls)
+static int prepare_lanes(galois_engine *e, int64_t ls, int64_t lspan)
 {
     if (!e->stream) {
         ENG_CUDA(e, cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
         e->own_stream = true;
     }
+    if (e->use_comm) {                   // one communicator per lane, split from the engine's
+        std::string why;
+        if (!e->comm.init(e->rank, e->world, e->nccl_id, &why)) return poison(e, GALOIS_E_NCCL, why);
+    }
     e->lane_size = ls;
-    for (int64_t off = 0; off < e->b_loc; off += ls) {
+    for (int64_t off = 0; off < lspan; off += ls) {
         galois_engine *l = new galois_engine();
         e->cnf->refs.fetch_add(1);
         l->cnf = e->cnf;
@@ -917,8 +921,16 @@ static int prepare_lanes(galois_engine *e, int64_t ls)
         l->profiling = e->profiling;
         l->fixed_slice = true;
         l->b0 = e->b0 + off;
-        l->b_loc = (int32_t)std::min<int64_t>(ls, e->b_loc - off);
+        l->b_loc = (int32_t)std::max<int64_t>(0, std::min<int64_t>(ls, e->b_loc - off));
+        l->b_per = e->b_per;             // rank stride of the global member index (winner's owner)
+        l->use_comm = e->use_comm;
+        l->rank = e->rank;
+        l->world = e->world;
         e->lane.push_back(l);
+        if (e->use_comm) {
+            std::string why;
+            if (!l->comm.dup_from(e->comm, &why)) return poison(e, GALOIS_E_NCCL, why);
+        }
         if (int rc = prepare(l)) {
             e->poisoned = true;
             return rc;
@@ -940,8 +952,8 @@ static int prepare(galois_engine *e)
     galois_cnf *c = e->cnf;
     const int32_t n = c->n;
     // batch slice: b_per = roundup(ceil(B / world), 32); pad the local slice to 32
-    if (e->fixed_slice) {                // a lane: b0 / b_loc were set by its parent
-        e->b_per = e->b_loc;
+    if (e->fixed_slice) {                // a lane: b0 / b_loc (/ b_per) were set by its parent
+        if (!e->b_per) e->b_per = e->b_loc;
     } else {
         int64_t per = (e->B + e->world - 1) / e->world;
         per = (per + 31) / 32 * 32;
@@ -958,10 +970,12 @@ static int prepare(galois_engine *e)
         e->windows = (int32_t)((span + e->sub - 1) / e->sub);
         e->b_loc = (int32_t)std::min<int64_t>(e->sub, e->slice_loc);
     }
-    if (e->lanes_req > 1 && e->windows == 1 && !e->use_comm && e->mode == GALOIS_MODE_ST && !e->debug) {
-        const int64_t per_lane = ((int64_t)e->b_loc + e->lanes_req - 1) / e->lanes_req;
+    if (e->lanes_req > 1 && e->windows == 1 && e->mode == GALOIS_MODE_ST && !e->debug) {
+        // with NCCL every rank forms the same lanes (from b_per; the last rank's may be short or empty)
+        const int64_t lspan = e->use_comm ? e->b_per : e->b_loc;
+        const int64_t per_lane = (lspan + e->lanes_req - 1) / e->lanes_req;
         const int64_t ls = (per_lane + 1023) / 1024 * 1024;
-        if ((int64_t)e->b_loc > ls) return prepare_lanes(e, ls);
+        if (lspan > ls) return prepare_lanes(e, ls, lspan);
     }
     const int32_t resident = e->windows > 1 ? e->sub : e->b_loc;
     // pad to 32 members (one bit word) up to 1024, then to whole 1024-member chunks, so that
@@ -1040,7 +1054,7 @@ static int prepare(galois_engine *e)
     ENG_CUDA(e, cudaMemcpyAsync(e->ctrl, &e->h_ctrl[0], sizeof(Ctrl), cudaMemcpyHostToDevice, e->stream));
     ENG_CUDA(e, cudaStreamSynchronize(e->stream));   // h_ctrl[0] is reused below
     for (auto &ev : e->poll_ev) ENG_CUDA(e, cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-    if (e->use_comm) {
+    if (e->use_comm && !e->comm.comm) {  // (a lane's communicator is split from its parent's)
         std::string why;
         if (!e->comm.init(e->rank, e->world, e->nccl_id, &why)) return poison(e, GALOIS_E_NCCL, why);
     }
@@ -1355,6 +1369,11 @@ static int lanes_refresh(galois_engine *e)
         const bool better = h.best_b >= 0 &&
                             (h.best_u != a.u ? h.best_u < a.u : h.best_t != a.t ? h.best_t < a.t : h.best_b < a.b);
         if (better) {
+            if (e->use_comm) {            // the winner's bits from its owner (collective on the lane's comm)
+                std::string why;
+                if (!l->comm.broadcast_bytes(l->best_bits, (size_t)n, (int)(h.best_b / e->b_per), l->stream, &why))
+                    return poison(e, GALOIS_E_NCCL, why);
+            }
             ENG_CUDA(e, cudaMemcpyAsync(e->agg_bits.data(), l->best_bits, (size_t)n, cudaMemcpyDeviceToHost, l->stream));
             a.u = h.best_u;
             a.t = h.best_t;

@@ -168,3 +168,22 @@ def test_lanes_gating_and_kernel_times(G):
     assert kt["forward"][1] == 2 * 3 and kt["update"][1] == 2 * 3
     eng.free()
     cnf.free()
+
+
+@pytest.mark.parametrize("K", [1, 3])
+def test_lanes_over_nccl(G, K):
+    """Lanes with the NCCL path (a 1-rank communicator; each lane's communicator is split
+    from the engine's): best, its bits (broadcast from the owner) and the counts equal the
+    undivided engine's, with and without SAT."""
+    inst = I.random_ksat(300, 1290, 3, 5)
+    full = _solve(G, inst, 3000, 40, 7, check_interval=K)
+    comm = _solve(G, inst, 3000, 40, 7, check_interval=K, lanes=3, nccl_id=G.galois_comm_unique_id())
+    assert full[1] == comm[1]
+    np.testing.assert_array_equal(full[2], comm[2])
+    np.testing.assert_array_equal(full[3], comm[3])
+    assert full[4] == comm[4]
+    sat = I.random_ksat(50, 213, 3, 0)
+    f2 = _solve(G, sat, 4096, 100, 0)
+    c2 = _solve(G, sat, 4096, 100, 0, lanes=2, nccl_id=G.galois_comm_unique_id())
+    assert f2[0] == c2[0] == G.SAT and f2[1] == c2[1]
+    np.testing.assert_array_equal(f2[2], c2[2])
