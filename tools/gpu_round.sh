@@ -30,7 +30,7 @@ if has launches; then
     for W in C2 C4; do
         timeout 600 $NCU --metrics gpu__time_duration.sum --clock-control none --csv \
             --log-file "$OUT/launches_$W.csv" python bench.py --workload $W --steps 4 --warmup 3 \
-            --no-cpu-baseline --no-e2e > "$OUT/launches_$W.log" 2>&1
+            --no-cpu-baseline --no-e2e --no-tts > "$OUT/launches_$W.log" 2>&1
         echo "launches $W rc=$?"
     done
 fi
@@ -38,7 +38,7 @@ if has full; then
     for W in C2 C4; do
         for K in k_update_tma k_sweep k_hub_partial_tma; do
             timeout 900 $NCU --set full --clock-control none --import-source on -k regex:$K -s 20 -c 1 \
-                -o "$OUT/full_${W}_$K" python bench.py --workload $W --steps 24 --warmup 3 --no-cpu-baseline \
+                -o "$OUT/full_${W}_$K" python bench.py --workload $W --steps 24 --warmup 3 --lanes 1 --no-cpu-baseline \
                 --no-e2e > "$OUT/full_${W}_$K.log" 2>&1
             echo "full $W $K rc=$?"
         done
