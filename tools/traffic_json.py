@@ -41,7 +41,7 @@ def main():
     src = sys.argv[1]
     tag = sys.argv[2] if len(sys.argv) > 2 else os.path.basename(src.rstrip("/"))
     out = {"_source": f"ncu --set full --clock-control none --import-source on (one launch after 20, cold cache, "
-                      f"replayed) of `python bench.py --workload W --steps 24 --warmup 3 --no-cpu-baseline --no-e2e` "
+                      f"replayed) of `python bench.py --workload W --steps 24 --warmup 3 --lanes 1 --no-cpu-baseline --no-e2e` "
                       f"on one B200, {tag}; dram__bytes_read.sum + dram__bytes_write.sum of that launch"}
     for rep in sorted(glob.glob(os.path.join(src, "full_*_*.ncu-rep"))):
         name = os.path.basename(rep)[len("full_"):-len(".ncu-rep")]
