@@ -34,7 +34,9 @@ WORKLOADS = {
     "C3a": dict(desc="random 5-SAT n=2000 m=42000 (ratio 21), seed 0", batch=16384),
     "C3b": dict(desc="random 7-SAT n=500 m=43895 (ratio 87.79), seed 0", batch=16384),
     "C4": dict(desc="industrial-like n=1M m=4.2M widths 2-30 power-law occurrences, seed 0", batch=1024),
-    "C5": dict(desc="cube-split random 3-SAT n=100k m=426k, 16 cube pins, seed 0", batch=65536),
+    # C5's batch is GLOBAL (configs[4]: "batch=65536 sharded over 2/4/8 B200"; alpha = b mod
+    # 2^16 covers every cube once): strong scaling, B / P members per GPU
+    "C5": dict(desc="cube-split random 3-SAT n=100k m=426k, 16 cube pins, seed 0", batch=65536, strong=True),
     # the paper's own GPU-stage configuration (App. A) on the C4 instance:
     # Tseitin k = 3 on the device, B = 3000, 10 epochs, lr 0.5, tau 1, then theta_sel, the
     # N = 100 candidate pool and the top 0.05 % confident literals (f1 + f2 + f4)
@@ -265,6 +267,15 @@ def oracle_sample(inst, batch, seconds=12.0, rank_b0=0):
             "cpu_model": cpu_model()}
 
 
+def batch_of(workload, world):
+    """(global batch, per-GPU batch, scaling): per-GPU batch fixed (weak) except C5, whose
+    global batch is fixed and sharded (strong)."""
+    w = WORKLOADS[workload]
+    if w.get("strong"):
+        return w["batch"], -(-w["batch"] // world), "strong"
+    return w["batch"] * world, w["batch"], "weak"
+
+
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -278,8 +289,7 @@ def run_reference(args):
     if rank != 0:
         return 0
     inst = make_instance(args.workload)
-    per_gpu = WORKLOADS[args.workload]["batch"]
-    B = per_gpu * args.gpus
+    B, per_gpu, scaling = batch_of(args.workload, args.gpus)
     samples = []
     # each step is a bounded sample: the whole --steps K --warmup W run stays within ~3 min
     per_step = max(0.25, min(args.ref_seconds, 180.0 / (args.warmup + args.steps)))
@@ -292,7 +302,7 @@ def run_reference(args):
     cb["value"] = value
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": args.workload, "instance": WORKLOADS[args.workload]["desc"],
                        "global_batch": B, "n": inst.n, "m": inst.m, "L": inst.L},
             "cpu_baseline": cb,
@@ -338,10 +348,6 @@ def main():
         if rank == 0:
             print(json.dumps(paper_pipeline(G, torch, dev, args)), flush=True)
         return 0
-    if args.tts:
-        print(json.dumps({"time_to_first_sat": time_to_sat(G, torch, dev, args.tts, range(args.tts_seeds))}),
-              flush=True)
-        return 0
     pg = None
     nccl_id = None
     def new_nccl_id():
@@ -353,11 +359,20 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
         pg = dist
+    if args.tts:
+        tts = time_to_sat(G, torch, dev, args.tts, range(args.tts_seeds),
+                          dist=(pg, rank, world, new_nccl_id) if pg else None)
+        if rank == 0:
+            print(json.dumps({"time_to_first_sat": tts}), flush=True)
+        if pg:
+            pg.barrier()
+            pg.destroy_process_group()
+        return 0
+    if pg:
         nccl_id = new_nccl_id()
 
     inst = make_instance(args.workload)
-    per_gpu = WORKLOADS[args.workload]["batch"]
-    B = per_gpu * world
+    B, per_gpu, scaling = batch_of(args.workload, world)
     T = args.warmup + 2 * args.steps         # warm-up, timed region, kernel timing pass
     stream = torch.cuda.Stream(dev)          # a real stream (not the legacy default one)
     torch.cuda.set_stream(stream)
@@ -477,7 +492,7 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u32-bits+f32", "data": "synthetic",
+            "scaling": scaling, "vs_baseline": None, "dtype": "u32-bits+f32", "data": "synthetic",
             "config": {"workload": args.workload, "instance": WORKLOADS[args.workload]["desc"],
                        "global_batch": B, "batch_per_gpu": per_gpu, "n": n, "m": inst.m, "L": L,
                        "check_interval": args.check_interval, "lr": 0.5, "tau": 1.0, "optimizer": "adam",
@@ -518,11 +533,13 @@ def main():
     return 0
 
 
-def time_to_sat(G, torch, dev, which="C1", seeds=range(10), batch=None, steps=None):
+def time_to_sat(G, torch, dev, which="C1", seeds=range(10), batch=None, steps=None, dist=None):
     """Time-to-first-SAT through the public API (galois_engine_run; host wall clock
     bracketed by device syncs; CNF already loaded, engine create + init included),
     per instance: SAT-set instances of the config's shape (C1: G1(50, 213, 3, seed);
-    C2: planted G2(10000, 42000, 3, seed); C4: planted G3)."""
+    C2: planted G2(10000, 42000, 3, seed); C4: planted G3). Under torchrun (dist =
+    (process group, rank, world, id factory)) the config's batch is the GLOBAL batch,
+    sharded over the ranks with the NCCL MIN exchange; each time is the max over ranks."""
     from paper_2603_28796_b200 import instances as I
     make = {"C1": lambda s: I.random_ksat(50, 213, 3, s),
             "C2": lambda s: I.random_ksat(10_000, 42_000, 3, s, planted=True),
@@ -530,24 +547,35 @@ def time_to_sat(G, torch, dev, which="C1", seeds=range(10), batch=None, steps=No
             "C4": lambda s: I.industrial(1_000_000, 4_200_000, s, planted=True)}[which]
     B = batch or WORKLOADS[which]["batch"]
     T = steps or (100 if which == "C1" else 200)
+    pg, rank, world, new_id = dist if dist else (None, 0, 1, None)
+    lanes = default_lanes(-(-B // world))
     out = []
     for s in seeds:
         inst = make(s)
         cnf = G.Cnf.from_instance(inst)
         for rep in range(2):               # the first repetition warms up
+            kw = dict(rank=rank, world=world, nccl_id=new_id()) if pg else {}
             torch.cuda.synchronize(dev)
+            if pg:
+                pg.barrier()
             t0 = time.perf_counter()
-            eng = G.Engine(cnf, B, T, 0.5, 0)
+            eng = G.Engine(cnf, B, T, 0.5, 0, lanes=lanes, **kw)
             rc = eng.run()
             best = eng.best_assignment()
             torch.cuda.synchronize(dev)
             el = time.perf_counter() - t0
+            if pg:
+                t = torch.tensor([el], dtype=torch.float64, device=dev)
+                pg.all_reduce(t, op=pg.ReduceOp.MAX)
+                el = float(t.item())
             eng.free()
         out.append({"seed": s, "sat": rc == G.SAT, "seconds": el, "step": best["step"], "member": best["global_b"],
                     "best_unsat": best["unsat"]})
         cnf.free()
     solved = [o for o in out if o["sat"]]
-    return {"instances": which, "batch": B, "steps_budget": T, "n": len(out), "solved": len(solved),
+    return {"instances": which, "batch": B, "n_gpus": world,
+            "lanes_per_gpu": effective_lanes(-(-B // world), lanes, world), "steps_budget": T,
+            "n": len(out), "solved": len(solved),
             "median_seconds_solved": statistics.median(o["seconds"] for o in solved) if solved else None,
             "median_step_solved": statistics.median(o["step"] for o in solved) if solved else None,
             "per_instance": out}
