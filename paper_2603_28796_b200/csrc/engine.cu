@@ -31,6 +31,10 @@ bool clauses(const DevCnf &c, int32_t W, int32_t b_pad, const uint32_t *X, const
              int32_t *lam, int32_t *unsat, Ctrl *ctrl, const BestArgs &ba, cudaStream_t st);
 void hub_partial(const DevCnf &c, int32_t W, int32_t b_pad, const uint32_t *E, short4 *partial,
                  const Ctrl *ctrl, cudaStream_t st);
+size_t small_run_smem(int32_t n, int32_t L);
+void small_run(const DevCnf &c, const StepParams &p, int32_t T, int32_t K, bool pending, float *z, float *m, float *v,
+               uint32_t *X, uint32_t *R, int32_t *unsat_last, int32_t *lam, SmallScratch *gs, void *recs,
+               uint8_t *snap, uint8_t *best_bits, Ctrl *ctrl, cudaStream_t st);
 void update_st(const DevCnf &c, const StepParams &p, float *z, float *m, float *v, uint32_t *X, uint32_t *R,
                const uint32_t *E, const short4 *partial, Ctrl *ctrl, int32_t *dbg_G, float *dbg_g1,
                cudaStream_t st);
@@ -62,6 +66,7 @@ using namespace galois;
 
 // ------------------------------------------------------------------------ errors
 static thread_local std::string g_last_error;
+constexpr size_t kSmallRunSmem = 200 * 1024;   // dynamic shared memory of one k_small_run CTA (max)
 
 static int fail(int code, const std::string &msg)
 {
@@ -516,6 +521,10 @@ struct galois_engine {
     int32_t *lam = nullptr, *unsat = nullptr, *unsat_last = nullptr;   // lam: 2 x b_pad (step parity)
     Ctrl *ctrl = nullptr;
     uint8_t *best_bits = nullptr;
+    // single-launch run of small instances (k_small_run): scratch, per-CTA records, snapshots
+    SmallScratch *small_gs = nullptr;
+    unsigned long long *small_recs = nullptr;
+    uint8_t *small_snap = nullptr;
     int8_t *pin_rank = nullptr;
     float2 *adam_consts = nullptr;
     int32_t *dbg_G = nullptr;
@@ -1002,6 +1011,11 @@ static int prepare(galois_engine *e)
     slab.add(&e->best_bits, (size_t)n);
     slab.add(&e->adam_consts, (size_t)e->T + 2);
     if (!e->pins.empty()) slab.add(&e->pin_rank, (size_t)n);
+    if (e->mode == GALOIS_MODE_ST && launch::small_run_smem(n, (int32_t)c->L) <= kSmallRunSmem) {
+        slab.add(&e->small_gs, 1);
+        slab.add(&e->small_recs, 2 * (size_t)e->W);
+        slab.add(&e->small_snap, (size_t)e->W * (size_t)n);
+    }
     if (e->mode == GALOIS_MODE_ST) {
         slab.add(&e->E, (size_t)c->L * e->W);
         slab.add(&e->lam, 2 * (size_t)e->b_pad);
@@ -1027,6 +1041,10 @@ static int prepare(galois_engine *e)
     ENG_CUDA(e, cudaMemsetAsync(e->unsat_last, 0, sizeof(int32_t) * (size_t)e->b_pad, e->stream));
     ENG_CUDA(e, cudaMemsetAsync(e->best_bits, 0, (size_t)n, e->stream));
     if (e->lam) ENG_CUDA(e, cudaMemsetAsync(e->lam, 0, 2 * sizeof(int32_t) * (size_t)e->b_pad, e->stream));
+    if (e->small_gs) {                   // {tstar = "no SAT", done = 0}; k_small_run's last CTA resets it
+        ENG_CUDA(e, cudaMemsetAsync(&e->small_gs->tstar, 0x7f, sizeof(int32_t), e->stream));
+        ENG_CUDA(e, cudaMemsetAsync(&e->small_gs->done, 0, sizeof(uint32_t), e->stream));
+    }
     // Adam step constants in fp64, per step index: 2 lr / (1 - beta1^t), 1 / sqrt(1 - beta2^t)
     // (the factor 2: z = theta_1 - theta_0 moves by twice the per-logit step)
     std::vector<float2> consts((size_t)e->T + 2);
@@ -1168,9 +1186,32 @@ extern "C" int galois_engine_enqueue(galois_engine *e, int32_t max_steps)
 static int run_windows(galois_engine *e);
 static int run_lanes(galois_engine *e);
 
+// Small instances: the remaining steps of run() as ONE launch of k_small_run (state in
+// shared memory, one CTA per 32 members; update_kernels.cu). Bypassed while profiling (its
+// per-kernel records need the per-step kernels), in debug mode and with NCCL.
+static bool small_run_ok(const galois_engine *e)
+{
+    return e->small_gs && e->mode == GALOIS_MODE_ST && !e->use_comm && e->windows == 1 && e->lane.empty() &&
+           !e->debug && !e->profiling && e->steps_enqueued < e->T;
+}
+
+static int run_small(galois_engine *e)
+{
+    Ctrl h;
+    const StepParams p = e->params();     // (a stopped engine: the kernel returns at once)
+    launch::small_run(e->cnf->view(), p, e->T, e->K, e->pending_check, e->z, e->m, e->v, e->X, e->R, e->unsat_last,
+                      e->lam, e->small_gs, e->small_recs, e->small_snap, e->best_bits, e->ctrl, e->stream);
+    ENG_CUDA(e, cudaGetLastError());
+    e->steps_enqueued = e->T;
+    e->pending_check = false;
+    if (int rc = read_ctrl(e, &h)) return rc;
+    return h.stopped ? GALOIS_SAT : GALOIS_BUDGET;
+}
+
 // Steps of the resident members until SAT or e->T (see galois_engine_run).
 static int run_steps(galois_engine *e)
 {
+    if (small_run_ok(e)) return run_small(e);
     // chunks of G steps (G even and a multiple of K, so every chunk that starts at a
     // multiple of G has the same kernel sequence and Lambda parity): replayed as one CUDA
     // graph; the stop flag of chunk i-1 is polled while chunk i is queued

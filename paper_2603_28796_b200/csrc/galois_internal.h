@@ -102,6 +102,15 @@ struct StepParams {
     int32_t *clear_b;
 };
 
+// Scratch of one single-launch small-instance run (k_small_run): the earliest SAT step
+// over the CTAs and the count of finished CTAs ({0x7f7f7f7f, 0}: set at prepare, reset by
+// the last CTA of every run).
+struct SmallScratch {
+    int32_t tstar;
+    uint32_t done;
+};
+constexpr size_t kSmallRecBytes = 16;   // per-CTA record {u, t, b}
+
 // Best tracking done by the last CTA of a checking clause sweep.
 struct BestArgs {
     int32_t *unsat_last;   // copy of the counts of this check

@@ -543,6 +543,241 @@ __global__ void __launch_bounds__(256 + 32, kTmaCtasPerSm) k_hub_partial_tma(Dev
     }
 }
 
+// ------------------------------------ small instances: a whole run() in ONE launch (a3-a8)
+// One CTA per 32-member word keeps its members' whole state in shared memory — z, m, v
+// (n x 32 fp32 each), the X and R words of every variable and one E word per literal slot
+// — and runs the steps itself: the clause pass (forward of X_s into E, Lambda, and the
+// exact check of R_{s-1}), then the fused update of every (variable, quad) with the SAME
+// quad_update() as k_update_tma, so every member's trajectory is bit-identical to the
+// per-step kernels'. Members never interact, so CTAs need no grid barrier: each keeps its
+// own best record (lexicographic (u, t, b); the winner's bits snapshotted on improvement),
+// and a SAT found at step t* (global atomicMin) stops every CTA once it has checked R_{t*}
+// (a CTA that is ahead may have run past t*; its records after t* cannot precede the
+// winner's). The last CTA merges the records into the control block. Used by run() when
+// the state fits shared memory (C1-sized instances, which the per-step path runs at ~12 us
+// per step of launch latency).
+struct SmallRec {
+    int32_t u, t;
+    int64_t b;
+};
+
+template <bool kTau1, bool kAdam, bool kPins>
+__global__ void __launch_bounds__(512) k_small_run(DevCnf c, StepParams p, int32_t T, int32_t K, int32_t pending0,
+                                                   float4 *__restrict__ z4, float4 *__restrict__ m4,
+                                                   float4 *__restrict__ v4, uint32_t *__restrict__ X,
+                                                   uint32_t *__restrict__ R, int32_t *__restrict__ unsat_last,
+                                                   int32_t *__restrict__ lam, SmallScratch *__restrict__ gs,
+                                                   SmallRec *__restrict__ recs, uint8_t *__restrict__ snap,
+                                                   uint8_t *__restrict__ best_bits, Ctrl *__restrict__ ctrl)
+{
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ int32_t cntU[32], cntL[32];
+    __shared__ int32_t s_bu, s_bt, s_flag, s_improved;
+    __shared__ int64_t s_bb;
+    if (ctrl->stopped) return;
+    const int32_t n = c.n;
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int w = blockIdx.x;                           // this CTA's 32-member word
+    const uint32_t QW = (uint32_t)p.b_pad / 4u;
+    const int64_t bw = p.b0 + 32 * (int64_t)w;         // global index of the word's member 0
+    const int32_t nvalid = min(32, p.b_loc - 32 * w);   // existing members of the word
+    float4 *sz = reinterpret_cast<float4 *>(smem);
+    float4 *sm = sz + (size_t)n * 8;
+    float4 *sv = sm + (size_t)n * 8;
+    uint32_t *sX = reinterpret_cast<uint32_t *>(sv + (size_t)n * 8);
+    uint32_t *sR = sX + n;
+    uint32_t *sE = sR + n;                              // [L] in CSC order, plain (not complemented)
+    for (int32_t i = tid; i < n * 8; i += blockDim.x) {
+        const size_t idx = (size_t)(i >> 3) * QW + (size_t)w * 8 + (i & 7);
+        sz[i] = z4[idx];
+        sm[i] = m4[idx];
+        sv[i] = v4[idx];
+    }
+    for (int32_t v = tid; v < n; v += blockDim.x) {
+        sX[v] = X[xr_at(v, w, p.W)];
+        sR[v] = R[xr_at(v, w, p.W)];
+    }
+    if (tid == 0) {
+        s_bu = INT32_MAX;
+        s_bt = -1;
+        s_bb = -1;
+    }
+    const int32_t t0 = ctrl->t;
+    bool pending = pending0 != 0, bad = false;
+    int32_t s = t0 + 1;
+    for (;;) {
+        const bool fwd = s <= T;
+        if (!fwd && !pending) break;
+        if (tid < 32) {
+            cntU[tid] = 0;
+            cntL[tid] = 0;
+        }
+        __syncthreads();
+        // clause pass: thread per clause (sweep order); lane p of a warp then owns bit p
+        int32_t myU = 0, myL = 0;
+        for (int32_t base = 0; base < c.m; base += blockDim.x) {
+            const int32_t ci = base + tid;
+            uint32_t U = 0, UR = 0;
+            if (ci < c.m) {
+                const int32_t lo = c.sweep_off[ci], hi = c.sweep_off[ci + 1];
+                uint32_t any = 0, two = 0, anyR = 0;
+                for (int32_t k = lo; k < hi; ++k) {
+                    const int2 si = c.sweep_slot[k];
+                    const uint32_t neg = 0u - (uint32_t)(si.x & 1);
+                    if (fwd) {
+                        const uint32_t sl = sX[si.x >> 1] ^ neg;
+                        two |= any & sl;
+                        any |= sl;
+                    }
+                    if (pending) anyR |= sR[si.x >> 1] ^ neg;
+                }
+                if (fwd) {
+                    for (int32_t k = lo; k < hi; ++k) {       // E_i = no OTHER literal true
+                        const int2 si = c.sweep_slot[k];
+                        const uint32_t sl = sX[si.x >> 1] ^ (0u - (uint32_t)(si.x & 1));
+                        sE[si.y] = ~any | (sl & ~two);
+                    }
+                    U = ~any;
+                }
+                if (pending) UR = ~anyR;
+            }
+            for (int b = 0; b < 32; ++b) {
+                if (fwd) {
+                    const uint32_t bl = __ballot_sync(0xffffffffu, (U >> b) & 1u);
+                    if (lane == b) myL += __popc(bl);
+                }
+                if (pending) {
+                    const uint32_t bl = __ballot_sync(0xffffffffu, (UR >> b) & 1u);
+                    if (lane == b) myU += __popc(bl);
+                }
+            }
+        }
+        if (fwd && myL) atomicAdd(&cntL[lane], myL);
+        if (pending && myU) atomicAdd(&cntU[lane], myU);
+        __syncthreads();
+        if (pending) {                                   // exact check of R_{s-1}
+            if (tid < 32) {
+                const int32_t u = cntU[bitpos(tid)];
+                if (tid < nvalid) unsat_last[32 * w + tid] = u;
+                unsigned long long key = tid < nvalid ? ((unsigned long long)(uint32_t)u << 32) |
+                                                            (unsigned long long)(bw + tid)
+                                                      : ~0ull;
+#pragma unroll
+                for (int d = 16; d > 0; d >>= 1) {
+                    const unsigned long long o = __shfl_xor_sync(0xffffffffu, key, d);
+                    key = o < key ? o : key;
+                }
+                if (tid == 0) {
+                    s_improved = 0;
+                    if (key != ~0ull && (int64_t)(key >> 32) < (int64_t)s_bu) {
+                        s_bu = (int32_t)(key >> 32);
+                        s_bt = s - 1;
+                        s_bb = (int64_t)(key & 0xFFFFFFFFull);
+                        s_improved = 1;
+                        if (s_bu == 0) atomicMin(&gs->tstar, s - 1);
+                    }
+                }
+            }
+            __syncthreads();
+            if (s_improved) {                           // the new best member's rounding
+                const int jb = bitpos((int)(s_bb - bw));
+                for (int32_t v = tid; v < n; v += blockDim.x) snap[(size_t)w * n + v] = (uint8_t)((sR[v] >> jb) & 1u);
+            }
+        }
+        if (!fwd) break;
+        if (tid < nvalid) lam[(size_t)(s & 1) * p.b_pad + 32 * w + tid] = cntL[bitpos(tid)];
+        if (tid == 0) s_flag = s_bu == 0 || *(volatile int32_t *)&gs->tstar <= s - 1;
+        __syncthreads();
+        if (s_flag) break;                              // the engine stops before update(s)
+        // fused update of step s: signal, gradient, Adam, R_s, X_{s+1}
+        const float2 ac = p.adam_consts[s];
+        for (int32_t base = 0; base < n * 8; base += blockDim.x) {
+            const int32_t i = base + tid;
+            const bool valid = i < n * 8;
+            uint32_t xn = 0, rn = 0;
+            if (valid) {
+                const int32_t v = i >> 3, q = i & 7;
+                const int32_t k0 = c.code_off[2 * v], k1 = c.code_off[2 * v + 1], k2 = c.code_off[2 * v + 2];
+                int32_t G[4] = {0, 0, 0, 0};
+                for (int32_t k = k0; k < k2; ++k) {
+                    const uint32_t b = quad_bits(sE[k], q);
+                    const int32_t sg = k < k1 ? 1 : -1;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) G[j] += sg * (int32_t)((b >> (8 * j)) & 1u);
+                }
+                const int64_t bq = p.b0 + 4 * ((int64_t)w * 8 + q);
+                float4 z = sz[i], m = sm[i], vv = sv[i];
+                float g1o[4];
+                quad_update<kTau1, kAdam, kPins>(p, ac, v, bq, s, G, z, m, vv, xn, rn, g1o, bad);
+                sz[i] = z;
+                sm[i] = m;
+                sv[i] = vv;
+            }
+            const uint32_t xw = pack_quads(xn, lane), rw = pack_quads(rn, lane);
+            if (valid && (lane & 7) == 0) {
+                sX[i >> 3] = xw;
+                sR[i >> 3] = rw;
+            }
+        }
+        __syncthreads();
+        pending = (s % K) == 0 || s == T;
+        ++s;
+    }
+    if (bad) atomicOr(&ctrl->nonfinite, 1);
+    __syncthreads();
+    for (int32_t i = tid; i < n * 8; i += blockDim.x) {
+        const size_t idx = (size_t)(i >> 3) * QW + (size_t)w * 8 + (i & 7);
+        z4[idx] = sz[i];
+        m4[idx] = sm[i];
+        v4[idx] = sv[i];
+    }
+    for (int32_t v = tid; v < n; v += blockDim.x) {
+        X[xr_at(v, w, p.W)] = sX[v];
+        R[xr_at(v, w, p.W)] = sR[v];
+    }
+    // the last CTA merges the records (lexicographic (u, t, b), with the record of earlier runs)
+    if (tid == 0) {
+        recs[w] = SmallRec{s_bu, s_bt, s_bb};
+        __threadfence();
+        s_flag = atomicAdd(&gs->done, 1u) == gridDim.x - 1u;
+    }
+    __syncthreads();
+    if (!s_flag) return;
+    __threadfence();
+    if (tid == 0) {
+        int32_t bu = ctrl->best_u, bt = ctrl->best_t;
+        int64_t bb = ctrl->best_b;
+        int win = -1;
+        for (int k = 0; k < (int)gridDim.x; ++k) {
+            SmallRec r;                                  // written by other CTAs: bypass L1
+            r.u = __ldcg(&recs[k].u);
+            r.t = __ldcg(&recs[k].t);
+            r.b = __ldcg(&recs[k].b);
+            if (r.b < 0) continue;
+            if (r.u < bu || (r.u == bu && (r.t < bt || (r.t == bt && r.b < bb)))) {
+                bu = r.u;
+                bt = r.t;
+                bb = r.b;
+                win = k;
+            }
+        }
+        ctrl->improved = win >= 0 ? 1 : 0;
+        ctrl->best_u = bu;
+        ctrl->best_t = bt;
+        ctrl->best_b = bb;
+        const int32_t tstar = *(volatile int32_t *)&gs->tstar;
+        ctrl->stopped = bu == 0 ? 1 : 0;
+        ctrl->t = bu == 0 ? tstar : T;
+        ctrl->last_check_t = ctrl->t;
+        gs->tstar = 0x7f7f7f7f;                         // ready for the next run
+        gs->done = 0;
+        s_bu = win;
+    }
+    __syncthreads();
+    if (s_bu >= 0)
+        for (int32_t v = tid; v < n; v += blockDim.x) best_bits[v] = snap[(size_t)s_bu * n + v];
+}
+
 // ------------------------------------------------------------------ launch wrappers
 namespace launch {
 
@@ -616,6 +851,26 @@ bool use_tma_update(int32_t W) { return W % 32 == 0; }
 
 // Function attributes (dynamic shared memory of the TMA kernels) for the current device;
 // called once per engine before any launch (and so never during CUDA-graph capture).
+size_t small_run_smem(int32_t n, int32_t L) { return (size_t)n * 8 * 16 * 3 + (size_t)n * 8 + (size_t)L * 4; }
+
+void small_run(const DevCnf &c, const StepParams &p, int32_t T, int32_t K, bool pending, float *z, float *m, float *v,
+               uint32_t *X, uint32_t *R, int32_t *unsat_last, int32_t *lam, SmallScratch *gs, void *recs,
+               uint8_t *snap, uint8_t *best_bits, Ctrl *ctrl, cudaStream_t st)
+{
+    using K_t = void (*)(DevCnf, StepParams, int32_t, int32_t, int32_t, float4 *, float4 *, float4 *, uint32_t *,
+                         uint32_t *, int32_t *, int32_t *, SmallScratch *, SmallRec *, uint8_t *, uint8_t *, Ctrl *);
+    static const K_t ks[8] = {k_small_run<false, false, false>, k_small_run<false, false, true>,
+                              k_small_run<false, true, false>,  k_small_run<false, true, true>,
+                              k_small_run<true, false, false>,  k_small_run<true, false, true>,
+                              k_small_run<true, true, false>,   k_small_run<true, true, true>};
+    const int variant = (p.inv_tau == 1.0f ? 4 : 0) | (p.optimizer == 0 ? 2 : 0) | (p.pin_rank ? 1 : 0);
+    const K_t k = ks[variant];
+    const size_t smem = small_run_smem(c.n, c.L);
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k<<<p.b_pad / 32, 512, smem, st>>>(c, p, T, K, pending ? 1 : 0, (float4 *)z, (float4 *)m, (float4 *)v, X, R,
+                                      unsat_last, lam, gs, (SmallRec *)recs, snap, best_bits, ctrl);
+}
+
 cudaError_t configure_kernels()
 {
     static std::atomic<uint64_t> done{0};
