@@ -114,7 +114,13 @@ int galois_engine_step(galois_engine *eng);
 
 /* Run steps until SAT (GALOIS_SAT) or until the budget is spent (GALOIS_BUDGET). The
  * host polls an 8-byte device flag once per chunk of steps; kernels of steps enqueued
- * after the stop are no-ops, so the recorded best and step count are exact. */
+ * after the stop are no-ops, so the recorded best and step count are exact.
+ * Small instances (32 members' z, m, v, bit planes and one E word per slot within 200 KB
+ * of shared memory, ST mode, no NCCL / sub-batching / lanes / debug / profiling) run all
+ * remaining steps in ONE kernel launch, one CTA per 32 members, with the same arithmetic
+ * (bit-identical iterates, best record and counts). After a SAT at step t* the best
+ * record, its assignment and the step count are exact; CTAs that were ahead may have run
+ * past t*, so their members' iterates and last-check counts can be of later steps. */
 int galois_engine_run(galois_engine *eng);
 
 /* Like run, but enqueues at most max_steps further steps and does not synchronise the
