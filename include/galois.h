@@ -118,9 +118,9 @@ int galois_engine_step(galois_engine *eng);
  * Small instances (32 members' z, m, v, bit planes and one E word per slot within 200 KB
  * of shared memory, ST mode, no NCCL / sub-batching / lanes / debug / profiling) run all
  * remaining steps in ONE kernel launch, one CTA per 32 members, with the same arithmetic
- * (bit-identical iterates, best record and counts). After a SAT at step t* the best
- * record, its assignment and the step count are exact; CTAs that were ahead may have run
- * past t*, so their members' iterates and last-check counts can be of later steps. */
+ * (bit-identical iterates, best record and counts; a grid barrier at each check stops
+ * every CTA exactly where the per-step engine stops). Needs all W CTAs co-resident
+ * (cooperative launch); otherwise the per-step path runs. */
 int galois_engine_run(galois_engine *eng);
 
 /* Like run, but enqueues at most max_steps further steps and does not synchronise the

@@ -32,9 +32,9 @@ bool clauses(const DevCnf &c, int32_t W, int32_t b_pad, const uint32_t *X, const
 void hub_partial(const DevCnf &c, int32_t W, int32_t b_pad, const uint32_t *E, short4 *partial,
                  const Ctrl *ctrl, cudaStream_t st);
 size_t small_run_smem(int32_t n, int32_t L);
-void small_run(const DevCnf &c, const StepParams &p, int32_t T, int32_t K, bool pending, float *z, float *m, float *v,
-               uint32_t *X, uint32_t *R, int32_t *unsat_last, int32_t *lam, SmallScratch *gs, void *recs,
-               uint8_t *snap, uint8_t *best_bits, Ctrl *ctrl, cudaStream_t st);
+cudaError_t small_run(const DevCnf &c, const StepParams &p, int32_t T, int32_t K, bool pending, float *z, float *m,
+                      float *v, uint32_t *X, uint32_t *R, int32_t *unsat_last, int32_t *lam, SmallScratch *gs,
+                      void *recs, uint8_t *snap, uint8_t *best_bits, Ctrl *ctrl, cudaStream_t st);
 void update_st(const DevCnf &c, const StepParams &p, float *z, float *m, float *v, uint32_t *X, uint32_t *R,
                const uint32_t *E, const short4 *partial, Ctrl *ctrl, int32_t *dbg_G, float *dbg_g1,
                cudaStream_t st);
@@ -1041,9 +1041,9 @@ static int prepare(galois_engine *e)
     ENG_CUDA(e, cudaMemsetAsync(e->unsat_last, 0, sizeof(int32_t) * (size_t)e->b_pad, e->stream));
     ENG_CUDA(e, cudaMemsetAsync(e->best_bits, 0, (size_t)n, e->stream));
     if (e->lam) ENG_CUDA(e, cudaMemsetAsync(e->lam, 0, 2 * sizeof(int32_t) * (size_t)e->b_pad, e->stream));
-    if (e->small_gs) {                   // {tstar = "no SAT", done = 0}; k_small_run's last CTA resets it
+    if (e->small_gs) {                   // {tstar = "no SAT", done = 0, arrive = 0}; the last CTA resets them
+        ENG_CUDA(e, cudaMemsetAsync(e->small_gs, 0, sizeof(SmallScratch), e->stream));
         ENG_CUDA(e, cudaMemsetAsync(&e->small_gs->tstar, 0x7f, sizeof(int32_t), e->stream));
-        ENG_CUDA(e, cudaMemsetAsync(&e->small_gs->done, 0, sizeof(uint32_t), e->stream));
     }
     // Adam step constants in fp64, per step index: 2 lr / (1 - beta1^t), 1 / sqrt(1 - beta2^t)
     // (the factor 2: z = theta_1 - theta_0 moves by twice the per-logit step)
@@ -1195,13 +1195,21 @@ static bool small_run_ok(const galois_engine *e)
            !e->debug && !e->profiling && e->steps_enqueued < e->T;
 }
 
+static int run_steps(galois_engine *e);
+
 static int run_small(galois_engine *e)
 {
     Ctrl h;
     const StepParams p = e->params();     // (a stopped engine: the kernel returns at once)
-    launch::small_run(e->cnf->view(), p, e->T, e->K, e->pending_check, e->z, e->m, e->v, e->X, e->R, e->unsat_last,
-                      e->lam, e->small_gs, e->small_recs, e->small_snap, e->best_bits, e->ctrl, e->stream);
-    ENG_CUDA(e, cudaGetLastError());
+    const cudaError_t le = launch::small_run(e->cnf->view(), p, e->T, e->K, e->pending_check, e->z, e->m, e->v, e->X,
+                                             e->R, e->unsat_last, e->lam, e->small_gs, e->small_recs, e->small_snap,
+                                             e->best_bits, e->ctrl, e->stream);
+    if (le == cudaErrorCooperativeLaunchTooLarge) {   // not all CTAs fit at once: per-step path
+        cudaGetLastError();
+        e->small_gs = nullptr;
+        return run_steps(e);
+    }
+    ENG_CUDA(e, le);
     e->steps_enqueued = e->T;
     e->pending_check = false;
     if (int rc = read_ctrl(e, &h)) return rc;

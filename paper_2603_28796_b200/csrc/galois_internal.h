@@ -108,6 +108,8 @@ struct StepParams {
 struct SmallScratch {
     int32_t tstar;
     uint32_t done;
+    uint32_t arrive;        // grid-barrier arrivals of the cooperative launch (0 between runs)
+    uint32_t pad;
 };
 constexpr size_t kSmallRecBytes = 16;   // per-CTA record {u, t, b}
 

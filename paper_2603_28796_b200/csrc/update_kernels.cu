@@ -74,14 +74,10 @@ __device__ __forceinline__ void count_bits(const uint32_t *__restrict__ col, int
 }
 
 // Same count over rows staged in shared memory (row = 32 words = 128 B).
-#ifndef GALOIS_CNT_UNROLL
-#define GALOIS_CNT_UNROLL 8
-#endif
-template <int kUnroll = GALOIS_CNT_UNROLL>
 __device__ __forceinline__ void count_bits_smem(const uint32_t *srow, int32_t n, int qp, int32_t G[4])
 {
     uint32_t acc = 0;                     // n <= 128 < 256: no overflow
-#pragma unroll kUnroll
+#pragma unroll 8
     for (int32_t k = 0; k < n; ++k) acc += quad_bits(srow[k * 32], qp);
 #pragma unroll
     for (int j = 0; j < 4; ++j) G[j] += (int32_t)((acc >> (8 * j)) & 255u);
@@ -126,6 +122,56 @@ __device__ __forceinline__ void count_rows_sliced(const uint32_t *wcol, int32_t 
     for (int k = 0; k < kOut; ++k) acc += quad_bits(P[k], qp) << k;
 #pragma unroll
     for (int j = 0; j < 4; ++j) G[j] += (int32_t)((acc >> (8 * j)) & 255u);
+}
+
+// The same bit-sliced count split in two, for a variable whose E rows arrive in several
+// pieces: sliced_add() adds one piece's rows (thread `sub` of the 8 sharing a word takes
+// rows sub, sub + 8, ...) into kIn planes that persist across the pieces, and
+// sliced_finish() runs the butterfly ONCE per variable and adds this thread's 4 counts to
+// G. For degree <= 256 a thread adds <= 32 rows: kIn = 6 planes, 9 after the butterfly.
+template <int kIn>
+__device__ __forceinline__ void sliced_add(uint32_t (&P)[kIn], const uint32_t *wcol, int32_t n, int sub)
+{
+    for (int32_t r = sub; r < n; r += 8) {
+        uint32_t c = wcol[r * 32];
+#pragma unroll
+        for (int k = 0; k < kIn; ++k) {
+            const uint32_t t = P[k] & c;
+            P[k] ^= c;
+            c = t;
+        }
+    }
+}
+
+template <int kIn>
+__device__ __forceinline__ void sliced_finish(const uint32_t (&Pin)[kIn], int qp, int32_t G[4])
+{
+    constexpr int kOut = kIn + 3;
+    uint32_t P[kOut];
+#pragma unroll
+    for (int k = 0; k < kOut; ++k) P[k] = k < kIn ? Pin[k] : 0u;
+#pragma unroll
+    for (int d = 1; d < 8; d <<= 1) {           // lanes 8w .. 8w+7 hold the same word
+        uint32_t carry = 0;
+#pragma unroll
+        for (int k = 0; k < kOut; ++k) {
+            const uint32_t o = __shfl_xor_sync(0xffffffffu, P[k], d);
+            const uint32_t sum = P[k] ^ o ^ carry;
+            carry = (P[k] & o) | (carry & (P[k] ^ o));
+            P[k] = sum;
+        }
+    }
+    uint32_t acc = 0;                           // planes 0..7: byte j = count mod 256 of member j
+#pragma unroll
+    for (int k = 0; k < kOut && k < 8; ++k) acc += quad_bits(P[k], qp) << k;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) G[j] += (int32_t)((acc >> (8 * j)) & 255u);
+#pragma unroll
+    for (int k = 8; k < kOut; ++k) {
+        const uint32_t b = quad_bits(P[k], qp);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) G[j] += (int32_t)((b >> (8 * j)) & 1u) << k;
+    }
 }
 
 struct ItemPos {
@@ -334,6 +380,19 @@ __global__ void __launch_bounds__(256) k_update_st(DevCnf c, StepParams p, RowMa
 // through `empty` (one arrive per warp). No CTA-wide barrier in the loop. Hub variables
 // (degree > kHubDegree) take one stage for z, m, v and read their partial sums.
 constexpr int kConsumerWarps = 8;
+// variables of at least this degree count their E rows bit-sliced across all their pieces
+// (~1.6 instructions per row and thread + one ~170-instruction butterfly) instead of ~4.1
+// per row and thread; kHubDegree bounds a thread's rows at 32 (6 planes)
+#ifndef GALOIS_SLICED_MIN_DEGREE
+#define GALOIS_SLICED_MIN_DEGREE 64
+#endif
+constexpr int kSlicedMinDegree = GALOIS_SLICED_MIN_DEGREE;
+constexpr int kSlicedPlanes = 6;
+#ifndef GALOIS_SLICED_MIN_AVG_DEGREE
+#define GALOIS_SLICED_MIN_AVG_DEGREE 48
+#endif
+constexpr int kSlicedMinAvgDegree = GALOIS_SLICED_MIN_AVG_DEGREE;   // L / n at which update_st picks kSliced
+static_assert(kHubDegree <= 8 * ((1 << kSlicedPlanes) - 1) + 8, "rows per thread must fit the planes");
 
 struct StageHdr {
     int32_t v;       // variable
@@ -341,7 +400,7 @@ struct StageHdr {
     int32_t r0, r1;  // CSC rows staged in this piece
 };
 
-template <bool kDebug, bool kTau1, bool kAdam, bool kPins>
+template <bool kDebug, bool kTau1, bool kAdam, bool kPins, bool kSliced>
 __global__ void __launch_bounds__(256 + 32, kTmaCtasPerSm) k_update_tma(DevCnf c, StepParams p, RowMap rm, float4 *__restrict__ z4,
                                                          float4 *__restrict__ m4, float4 *__restrict__ v4,
                                                          uint32_t *__restrict__ X, uint32_t *__restrict__ R,
@@ -375,6 +434,7 @@ __global__ void __launch_bounds__(256 + 32, kTmaCtasPerSm) k_update_tma(DevCnf c
                 const int32_t k0 = c.code_off[2 * v], k1 = c.code_off[2 * v + 1], k2 = c.code_off[2 * v + 2];
                 const bool hub = c.num_hubs > 0 && c.hub_of_var[v] >= 0;
                 const bool pinned = kPins && p.pin_rank[v] >= 0;   // cube pin: read once, by the producer
+                const bool sliced = kSliced && !hub && k2 - k0 >= kSlicedMinDegree;
                 const int32_t pieces = hub ? 1 : max(1, (k2 - k0 + kStageRows - 1) / kStageRows);
                 const size_t off = (size_t)v * QW + (size_t)ch * 256u;
                 const uint32_t *Ech = E + (size_t)ch * c.L * 32u;
@@ -387,7 +447,8 @@ __global__ void __launch_bounds__(256 + 32, kTmaCtasPerSm) k_update_tma(DevCnf c
                     const int32_t r0 = hub ? k0 : k0 + pc * kStageRows;
                     const int32_t r1 = hub ? k0 : min(k2, r0 + kStageRows);
                     hdr[st] = StageHdr{(int32_t)v, k1, r0, r1};
-                    hflags[st] = (pc == 0 ? 1 : 0) | (pc == pieces - 1 ? 2 : 0) | (hub ? 4 : 0) | (pinned ? 8 : 0);
+                    hflags[st] = (pc == 0 ? 1 : 0) | (pc == pieces - 1 ? 2 : 0) | (hub ? 4 : 0) | (pinned ? 8 : 0) |
+                                 (sliced ? 16 : 0);
                     const uint32_t ebytes = (uint32_t)(r1 - r0) * 128u;
                     const uint32_t fb = full_s + 8u * st, sbs = stage_s + (uint32_t)(st * kStageBytes);
                     mbar_arrive_expect_tx_s(fb, (pc == 0 ? 3u * 4096u : 0u) + ebytes);
@@ -413,8 +474,15 @@ __global__ void __launch_bounds__(256 + 32, kTmaCtasPerSm) k_update_tma(DevCnf c
     uint32_t slot = 0;
     for (uint32_t item = blockIdx.x; item < rm.items; item += gridDim.x) {
         float4 z, m, vv;
+        int32_t v = 0, flags = 0, negs = 0;
         int32_t G[4] = {0, 0, 0, 0};
-        int32_t v = 0, flags = 0;
+        // kSliced (high average degree): counts carried across an item's pieces in SWAR bytes
+        // (degree < kSlicedMinDegree: a byte cannot overflow) or bit-sliced planes (flag 16),
+        // G formed after the last piece. Otherwise each piece adds its counts to G.
+        uint32_t acc = 0;
+        uint32_t PS[kSlicedPlanes];
+#pragma unroll
+        for (int k = 0; k < kSlicedPlanes; ++k) PS[k] = 0;
         do {
             const int st = (int)(slot % kStages);
             mbar_wait_s(full_s + 8u * st, (slot / kStages) & 1u);
@@ -429,22 +497,45 @@ __global__ void __launch_bounds__(256 + 32, kTmaCtasPerSm) k_update_tma(DevCnf c
                 vv = reinterpret_cast<const float4 *>(sb + kStageE + 8192)[tid];
             }
             if (flags & 4) {
-                const uint32_t q = (item - (uint32_t)v * rm.cpr) * 256u + (uint32_t)tid;
-                hub_signal(c, partial, QW, c.hub_of_var[v], q, G);
+                if (!kSliced) {
+                    const uint32_t q = (item - (uint32_t)v * rm.cpr) * 256u + (uint32_t)tid;
+                    hub_signal(c, partial, QW, c.hub_of_var[v], q, G);
+                }
             } else {
                 // rows [r0, r1): negative ones (from k1 on) are stored complemented
                 const uint32_t *srow = reinterpret_cast<const uint32_t *>(sb) + (tid >> 3);
-                const int32_t nneg = h.r1 - max(h.k1, h.r0), nrows = h.r1 - h.r0;
-                if (nrows >= 16)                    // uniform over the CTA: a long piece
-                    count_rows_sliced<3>(srow, nrows, tid & 7, sh, G);   // <= 4 rows per thread
-                else
-                    count_bits_smem(srow, nrows, sh, G);
-                if (nneg > 0) { G[0] -= nneg; G[1] -= nneg; G[2] -= nneg; G[3] -= nneg; }
+                const int32_t nrows = h.r1 - h.r0, nneg = h.r1 - max(h.k1, h.r0);
+                if (kSliced) {
+                    negs += max(0, nneg);
+                    if (flags & 16) {               // uniform over the CTA: a high-degree variable
+                        sliced_add(PS, srow, nrows, tid & 7);
+                    } else {
+#pragma unroll 8
+                        for (int32_t k = 0; k < nrows; ++k) acc += quad_bits(srow[k * 32], sh);
+                    }
+                } else {
+                    if (nrows >= 16)                // uniform over the CTA: a long piece
+                        count_rows_sliced<3>(srow, nrows, tid & 7, sh, G);   // <= 4 rows per thread
+                    else
+                        count_bits_smem(srow, nrows, sh, G);
+                    if (nneg > 0) { G[0] -= nneg; G[1] -= nneg; G[2] -= nneg; G[3] -= nneg; }
+                }
             }
             __syncwarp();
             if (lane == 0) mbar_arrive_s(empty_s + 8u * st);   // this warp is done reading the stage
         } while (!(flags & 2));
         const uint32_t q = (item - (uint32_t)v * rm.cpr) * 256u + (uint32_t)tid;
+        if (kSliced && (flags & 4)) {
+            hub_signal(c, partial, QW, c.hub_of_var[v], q, G);
+        } else if (kSliced) {
+            if (flags & 16)
+                sliced_finish(PS, sh, G);           // one butterfly per variable
+            else
+#pragma unroll
+                for (int j = 0; j < 4; ++j) G[j] = (int32_t)((acc >> (8 * j)) & 255u);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) G[j] -= negs;
+        }
         const int64_t bq = p.b0 + 4 * (int64_t)q;
         uint32_t xn, rn;
         float g1o[4];
@@ -549,17 +640,35 @@ __global__ void __launch_bounds__(256 + 32, kTmaCtasPerSm) k_hub_partial_tma(Dev
 // — and runs the steps itself: the clause pass (forward of X_s into E, Lambda, and the
 // exact check of R_{s-1}), then the fused update of every (variable, quad) with the SAME
 // quad_update() as k_update_tma, so every member's trajectory is bit-identical to the
-// per-step kernels'. Members never interact, so CTAs need no grid barrier: each keeps its
-// own best record (lexicographic (u, t, b); the winner's bits snapshotted on improvement),
-// and a SAT found at step t* (global atomicMin) stops every CTA once it has checked R_{t*}
-// (a CTA that is ahead may have run past t*; its records after t* cannot precede the
-// winner's). The last CTA merges the records into the control block. Used by run() when
-// the state fits shared memory (C1-sized instances, which the per-step path runs at ~12 us
-// per step of launch latency).
+// per-step kernels'. Members never interact, so CTAs meet only at check steps: each keeps
+// its own best record (lexicographic (u, t, b); the winner's bits snapshotted on
+// improvement), publishes a SAT at t* by atomicMin, and after a grid barrier (cooperative
+// launch: all CTAs co-resident) every CTA stops before update(t* + 1), exactly where the
+// per-step engine stops. The last CTA merges the records into the control block. Used by
+// run() when the state fits shared memory (C1-sized instances, which the per-step path
+// runs at ~12 us per step of launch latency).
 struct SmallRec {
     int32_t u, t;
     int64_t b;
 };
+
+// Grid-wide barrier of a cooperative launch (all CTAs co-resident): a monotonic arrival
+// counter, release add + acquire polls; the k-th barrier waits for k * gridDim.x arrivals
+// (the last CTA zeroes the counter after the run).
+__device__ __forceinline__ void grid_barrier(SmallScratch *gs, uint32_t target)
+{
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(&gs->arrive) : "memory");
+        uint32_t seen;
+        for (;;) {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(&gs->arrive) : "memory");
+            if (seen >= target) break;
+            __nanosleep(8);
+        }
+    }
+    __syncthreads();
+}
 
 template <bool kTau1, bool kAdam, bool kPins>
 __global__ void __launch_bounds__(512) k_small_run(DevCnf c, StepParams p, int32_t T, int32_t K, int32_t pending0,
@@ -605,6 +714,7 @@ __global__ void __launch_bounds__(512) k_small_run(DevCnf c, StepParams p, int32
     const int32_t t0 = ctrl->t;
     bool pending = pending0 != 0, bad = false;
     int32_t s = t0 + 1;
+    uint32_t barriers = 0;                              // arrivals the next barrier waits for
     for (;;) {
         const bool fwd = s <= T;
         if (!fwd && !pending) break;
@@ -686,9 +796,15 @@ __global__ void __launch_bounds__(512) k_small_run(DevCnf c, StepParams p, int32
         }
         if (!fwd) break;
         if (tid < nvalid) lam[(size_t)(s & 1) * p.b_pad + 32 * w + tid] = cntL[bitpos(tid)];
-        if (tid == 0) s_flag = s_bu == 0 || *(volatile int32_t *)&gs->tstar <= s - 1;
-        __syncthreads();
-        if (s_flag) break;                              // the engine stops before update(s)
+        if (pending) {
+            // every CTA has checked R_{s-1}: a SAT anywhere stops all of them before update(s),
+            // exactly where the per-step engine stops
+            barriers += gridDim.x;
+            grid_barrier(gs, barriers);
+            if (tid == 0) s_flag = __ldcg(&gs->tstar) <= s - 1;
+            __syncthreads();
+            if (s_flag) break;
+        }
         // fused update of step s: signal, gradient, Adam, R_s, X_{s+1}
         const float2 ac = p.adam_consts[s];
         for (int32_t base = 0; base < n * 8; base += blockDim.x) {
@@ -771,6 +887,7 @@ __global__ void __launch_bounds__(512) k_small_run(DevCnf c, StepParams p, int32
         ctrl->last_check_t = ctrl->t;
         gs->tstar = 0x7f7f7f7f;                         // ready for the next run
         gs->done = 0;
+        gs->arrive = 0;
         s_bu = win;
     }
     __syncthreads();
@@ -844,8 +961,14 @@ struct SelGeneric {
 };
 template <bool a, bool b, bool c, bool d>
 struct SelTma {
-    static constexpr UpdKernel k = k_update_tma<a, b, c, d>;
+    static constexpr UpdKernel k = k_update_tma<a, b, c, d, false>;
 };
+template <bool a, bool b, bool c, bool d>
+struct SelTmaSliced {
+    static constexpr UpdKernel k = k_update_tma<a, b, c, d, true>;
+};
+// high average degree (5-SAT-like): E rows counted bit-sliced across a variable's pieces
+static bool use_sliced(const DevCnf &c) { return (int64_t)c.L >= (int64_t)kSlicedMinAvgDegree * c.n; }
 
 bool use_tma_update(int32_t W) { return W % 32 == 0; }
 
@@ -853,9 +976,9 @@ bool use_tma_update(int32_t W) { return W % 32 == 0; }
 // called once per engine before any launch (and so never during CUDA-graph capture).
 size_t small_run_smem(int32_t n, int32_t L) { return (size_t)n * 8 * 16 * 3 + (size_t)n * 8 + (size_t)L * 4; }
 
-void small_run(const DevCnf &c, const StepParams &p, int32_t T, int32_t K, bool pending, float *z, float *m, float *v,
-               uint32_t *X, uint32_t *R, int32_t *unsat_last, int32_t *lam, SmallScratch *gs, void *recs,
-               uint8_t *snap, uint8_t *best_bits, Ctrl *ctrl, cudaStream_t st)
+cudaError_t small_run(const DevCnf &c, const StepParams &p, int32_t T, int32_t K, bool pending, float *z, float *m,
+                      float *v, uint32_t *X, uint32_t *R, int32_t *unsat_last, int32_t *lam, SmallScratch *gs,
+                      void *recs, uint8_t *snap, uint8_t *best_bits, Ctrl *ctrl, cudaStream_t st)
 {
     using K_t = void (*)(DevCnf, StepParams, int32_t, int32_t, int32_t, float4 *, float4 *, float4 *, uint32_t *,
                          uint32_t *, int32_t *, int32_t *, SmallScratch *, SmallRec *, uint8_t *, uint8_t *, Ctrl *);
@@ -866,9 +989,24 @@ void small_run(const DevCnf &c, const StepParams &p, int32_t T, int32_t K, bool 
     const int variant = (p.inv_tau == 1.0f ? 4 : 0) | (p.optimizer == 0 ? 2 : 0) | (p.pin_rank ? 1 : 0);
     const K_t k = ks[variant];
     const size_t smem = small_run_smem(c.n, c.L);
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k<<<p.b_pad / 32, 512, smem, st>>>(c, p, T, K, pending ? 1 : 0, (float4 *)z, (float4 *)m, (float4 *)v, X, R,
-                                      unsat_last, lam, gs, (SmallRec *)recs, snap, best_bits, ctrl);
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    // cooperative launch: every CTA must be resident for the grid barrier (else the caller
+    // takes the per-step path)
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 512, smem);
+    if (e != cudaSuccess) return e;
+    const unsigned grid = (unsigned)(p.b_pad / 32);
+    if ((int64_t)per_sm * sms < (int64_t)grid) return cudaErrorCooperativeLaunchTooLarge;
+    int32_t pend = pending ? 1 : 0;
+    float4 *z4 = (float4 *)z, *m4 = (float4 *)m, *v4 = (float4 *)v;
+    SmallRec *rc = (SmallRec *)recs;
+    DevCnf cc = c;
+    StepParams pp = p;
+    void *args[] = {&cc, &pp, &T, &K, &pend, &z4, &m4, &v4, &X, &R, &unsat_last, &lam, &gs, &rc, &snap, &best_bits, &ctrl};
+    return cudaLaunchCooperativeKernel((const void *)k, dim3(grid), dim3(512), args, smem, st);
 }
 
 cudaError_t configure_kernels()
@@ -880,6 +1018,9 @@ cudaError_t configure_kernels()
     if (dev < 64 && (done.load() >> dev) & 1ull) return cudaSuccess;
     for (int v = 0; v < 16; ++v) {
         e = cudaFuncSetAttribute((const void *)pick<SelTma>(v), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 kTmaSmem);
+        if (e != cudaSuccess) return e;
+        e = cudaFuncSetAttribute((const void *)pick<SelTmaSliced>(v), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  kTmaSmem);
         if (e != cudaSuccess) return e;
     }
@@ -898,7 +1039,8 @@ void update_st(const DevCnf &c, const StepParams &p, float *z, float *m, float *
     const int variant = (dbg_G ? 8 : 0) | (p.inv_tau == 1.0f ? 4 : 0) | (p.optimizer == 0 ? 2 : 0) |
                         (p.pin_rank ? 1 : 0);
     if (use_tma_update(p.W)) {
-        const UpdKernel k = pick<SelTma>(variant);   // smem attribute set by configure_kernels()
+        // smem attribute set by configure_kernels()
+        const UpdKernel k = use_sliced(c) ? pick<SelTmaSliced>(variant) : pick<SelTma>(variant);
         k<<<item_grid(rm, kTmaCtasPerSm), 256 + 32, kTmaSmem, st>>>(c, p, rm, (float4 *)z, (float4 *)m, (float4 *)v, X, R, E,
                                                    partial, ctrl, (int4 *)dbg_G, (float4 *)dbg_g1);
     } else {

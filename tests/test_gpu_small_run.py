@@ -3,8 +3,8 @@
 
 The per-step path is forced by turning profiling on (its per-kernel records need the
 per-step kernels). Both run the same quad_update(), so the iterates, best record, bits,
-counts and losses must be bit-identical; after a SAT only the winner's record and the
-step count are compared (CTAs that are ahead may have run past t*, as documented)."""
+counts and losses must be bit-identical — also after a SAT, where a grid barrier at each
+check stops every CTA exactly where the per-step engine stops."""
 import numpy as np
 import pytest
 
@@ -91,14 +91,12 @@ def test_small_run_variants(G, variant):
 @pytest.mark.parametrize("seed", [0, 2, 3])
 def test_small_run_first_sat(G, seed):
     """C1 shape: the first satisfying (step, member), its bits (a model of the CNF, checked
-    by the oracle) and the step count equal the per-step engine's."""
+    by the oracle), the step count, every member's iterate and last-check count equal the
+    per-step engine's."""
     inst = I.random_ksat(50, 213, 3, seed)
-    a = _run(G, inst, 1024, 100, 0, per_step=True, state=False)
-    b = _run(G, inst, 1024, 100, 0, per_step=False, state=False)
-    assert a["rc"] == b["rc"]
-    assert a["best"] == b["best"]
-    np.testing.assert_array_equal(a["values"], b["values"])
-    assert a["info"] == b["info"]
+    a = _run(G, inst, 1024, 100, 0, per_step=True)
+    b = _run(G, inst, 1024, 100, 0, per_step=False)
+    _same(a, b)                                   # iterates and counts too: the stop is exact
     f = O.Cnf(inst.n, inst.offsets, inst.lits)
     assert O.unsat_count(f, b["values"]) == b["best"][0]
     if b["rc"] == G.SAT:
@@ -112,3 +110,13 @@ def test_small_run_not_used_when_large(G):
     a = _run(G, inst, 64, 10, 0, per_step=True)
     b = _run(G, inst, 64, 10, 0, per_step=False)
     _same(a, b)
+
+
+def test_small_run_planted_sat_k_interval(G):
+    """A planted instance solved mid-run with a check interval: stop step, record and state
+    identical (the barrier sits only at check steps)."""
+    inst = I.random_ksat(60, 255, 3, 13, planted=True)
+    for K in (1, 3):
+        a = _run(G, inst, 2048, 40, 21, per_step=True, check_interval=K)
+        b = _run(G, inst, 2048, 40, 21, per_step=False, check_interval=K)
+        _same(a, b)
