@@ -38,3 +38,22 @@ def test_reference_arm_json_line():
 def test_reference_arm_other_ranks_exit_quietly():
     out = _run({"RANK": "1", "WORLD_SIZE": "2", "LOCAL_RANK": "1"}, "--gpus", "2")
     assert out == ""
+
+
+def test_batch_sharding_and_lanes_rules():
+    """Host rules of the bench: weak scaling keeps the per-GPU batch (C2: 4096 per GPU),
+    C5's global batch of 65536 is sharded (strong); the lanes the engine forms (galois.h
+    galois_engine_set_lanes: ceil(b_loc / lanes) rounded up to 1024 members)."""
+    sys.path.insert(0, ROOT)
+    import bench
+    assert bench.batch_of("C2", 1) == (4096, 4096, "weak")
+    assert bench.batch_of("C2", 8) == (32768, 4096, "weak")
+    assert bench.batch_of("C5", 1) == (65536, 65536, "strong")
+    assert bench.batch_of("C5", 8) == (65536, 8192, "strong")
+    assert bench.default_lanes(4096) == 4 and bench.default_lanes(1024) == 1
+    assert bench.effective_lanes(4096, 4, 1) == 4
+    assert bench.effective_lanes(3000, 4, 1) == 3          # 1024 + 1024 + 952
+    assert bench.effective_lanes(16384, 4, 1) == 4
+    assert bench.effective_lanes(2100, 2, 8) == 2          # 2048 + 52
+    assert bench.effective_lanes(1024, 4, 1) == 1
+    assert bench.effective_lanes(8192, 1, 1) == 1
