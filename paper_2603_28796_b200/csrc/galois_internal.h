@@ -31,7 +31,10 @@ __host__ __device__ __forceinline__ size_t xr_at(int32_t v, int32_t w, int32_t W
 {
     return (size_t)v * 2 * (size_t)xr_pad(W) + ((size_t)(w >> 2) << 3) + (size_t)(w & 3);
 }
-constexpr int kHubChunk = 128;       // occurrences per hub partial item (|partial| <= 128: int16)
+#ifndef GALOIS_HUB_CHUNK
+#define GALOIS_HUB_CHUNK 128
+#endif
+constexpr int kHubChunk = GALOIS_HUB_CHUNK;   // occurrences per hub partial item (|partial| <= 256: int16)
 
 // Device-side control block (one per engine, device memory).
 struct Ctrl {

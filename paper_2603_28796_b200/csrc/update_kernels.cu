@@ -117,11 +117,17 @@ __device__ __forceinline__ void count_rows_sliced(const uint32_t *wcol, int32_t 
             P[k] = sum;
         }
     }
-    uint32_t acc = 0;                           // byte j = count of member sh + j (<= 255)
+    uint32_t acc = 0;                           // planes 0..7: byte j = count mod 256 of member j
 #pragma unroll
-    for (int k = 0; k < kOut; ++k) acc += quad_bits(P[k], qp) << k;
+    for (int k = 0; k < kOut && k < 8; ++k) acc += quad_bits(P[k], qp) << k;
 #pragma unroll
     for (int j = 0; j < 4; ++j) G[j] += (int32_t)((acc >> (8 * j)) & 255u);
+#pragma unroll
+    for (int k = 8; k < kOut; ++k) {            // (a 256-row hub chunk can count 256)
+        const uint32_t b = quad_bits(P[k], qp);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) G[j] += (int32_t)((b >> (8 * j)) & 1u) << k;
+    }
 }
 
 // The same bit-sliced count split in two, for a variable whose E rows arrive in several
@@ -573,6 +579,8 @@ __global__ void __launch_bounds__(256 + 32, kTmaCtasPerSm) k_update_tma(DevCnf c
 // Item = (hub chunk of <= kHubChunk occurrences, 1024-member chunk): the chunk's E rows
 // (<= 16 KB, contiguous) arrive by one bulk copy; per quad the signed count (|.| <= 128).
 constexpr int kHubStageBytes = kHubChunk * 128;
+constexpr int kHubCtasPerSm = kStages * kHubStageBytes * kTmaCtasPerSm <= 200 * 1024 ? kTmaCtasPerSm
+                                                                                    : (200 * 1024) / (kStages * kHubStageBytes);
 
 __global__ void __launch_bounds__(256 + 32, kTmaCtasPerSm) k_hub_partial_tma(DevCnf c, RowMap rm,
                                                                            const uint32_t *__restrict__ E,
@@ -621,8 +629,8 @@ __global__ void __launch_bounds__(256 + 32, kTmaCtasPerSm) k_hub_partial_tma(Dev
             const int4 h = hdr[st];
             const uint32_t *srow = reinterpret_cast<const uint32_t *>(smem + st * kHubStageBytes) + (tid >> 3);
             int32_t G[4] = {0, 0, 0, 0};
-            // h.z <= 128 rows (the last h.z - h.y negative): per-thread share <= 16 < 2^5
-            count_rows_sliced<5>(reinterpret_cast<const uint32_t *>(smem + st * kHubStageBytes) + (tid >> 3), h.z,
+            // h.z <= kHubChunk rows (the last h.z - h.y negative): per-thread share <= kHubChunk / 8
+            count_rows_sliced<kHubChunk <= 248 ? 5 : 6>(reinterpret_cast<const uint32_t *>(smem + st * kHubStageBytes) + (tid >> 3), h.z,
                                  tid & 7, sh, G);
             const int32_t nneg = h.z - h.y;
             G[0] -= nneg; G[1] -= nneg; G[2] -= nneg; G[3] -= nneg;
@@ -932,7 +940,7 @@ void hub_partial(const DevCnf &c, int32_t W, int32_t b_pad, const uint32_t *E, s
     if (c.num_hub_chunks == 0) return;
     const RowMap rm = make_rowmap((uint32_t)c.num_hub_chunks, (uint32_t)b_pad);
     if (W % 32 == 0)
-        k_hub_partial_tma<<<item_grid(rm, kTmaCtasPerSm), 256 + 32, kStages * kHubStageBytes, st>>>(c, rm, E, partial,
+        k_hub_partial_tma<<<item_grid(rm, kHubCtasPerSm), 256 + 32, kStages * kHubStageBytes, st>>>(c, rm, E, partial,
                                                                                                    ctrl);
     else
         k_hub_partial<<<item_grid(rm, 8), 256, 0, st>>>(c, W < 32 ? W : 32, rm, E, partial, ctrl);

@@ -64,7 +64,7 @@ t4, _ = table(c4)
 m = {k: sum(v) / len(v) for k, v in agg2.items()}
 lane = [m.get(f"{k} [lane, 1024 members]", 0) for k in main]
 und = [m.get(f"{k} [undivided, 4096 members]", 0) for k in main]
-md = f"""# Round {RND[1:]} — launch lists (ncu gpu__time_duration.sum, --clock-control none)
+md = f"""# Round {int(RND[1:])} — launch lists (ncu gpu__time_duration.sum, --clock-control none)
 
 Command: `ncu --metrics gpu__time_duration.sum --clock-control none --csv python bench.py --workload W --steps 4 --warmup 3 --no-cpu-baseline --no-e2e --no-tts` — the bench's own command (cold-cache, serialised per launch: compare shares, not absolutes). Raw CSVs: {RND}_c2_launches.csv, {RND}_c4_launches.csv. Source: gpurun_out/{TAG}.
 
