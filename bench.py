@@ -24,6 +24,7 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+HUB_CHUNK = 256                 # occurrences per hub partial item (galois_internal.h kHubChunk)
 METRIC = "literal-evals/sec"
 UNIT = "literal-evals/s"
 
@@ -438,7 +439,7 @@ def main():
     deg = np.bincount(np.abs(inst.lits.astype(np.int64)) - 1, minlength=n)
     hubs = deg > 256
     L_hub = int(deg[hubs].sum())
-    hub_chunks = int(((deg[hubs] + 127) // 128).sum())
+    hub_chunks = int(((deg[hubs] + HUB_CHUNK - 1) // HUB_CHUNK).sum())   # galois_internal.h kHubChunk
     alg = {
         # E of non-hub occurrences (hubs: int16x4 partials) + z, m, v read/write + X, R + offsets
         "update": (L - L_hub) * W * 4 + hub_chunks * b_pad * 2 + 24 * n * b_pad + 2 * n * W * 4 + 4 * (2 * n + 1),

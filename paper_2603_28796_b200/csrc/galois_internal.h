@@ -32,7 +32,7 @@ __host__ __device__ __forceinline__ size_t xr_at(int32_t v, int32_t w, int32_t W
     return (size_t)v * 2 * (size_t)xr_pad(W) + ((size_t)(w >> 2) << 3) + (size_t)(w & 3);
 }
 #ifndef GALOIS_HUB_CHUNK
-#define GALOIS_HUB_CHUNK 128
+#define GALOIS_HUB_CHUNK 256
 #endif
 constexpr int kHubChunk = GALOIS_HUB_CHUNK;   // occurrences per hub partial item (|partial| <= 256: int16)
 
