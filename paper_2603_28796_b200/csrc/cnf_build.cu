@@ -208,6 +208,23 @@ __global__ void k_width_keys(int64_t m, const int32_t *__restrict__ clause_off, 
     }
 }
 
+// Locality key of the sweep order: width bucket (8 bits) above the clause's lowest
+// variable scaled to 24 bits, so that within a width class consecutive clause groups share
+// their lowest variable's X/R row (and its E rows are written close together).
+__global__ void k_width_minvar_keys(int64_t m, int32_t n, const int32_t *__restrict__ clause_off,
+                                    const int32_t *__restrict__ lits, uint32_t *__restrict__ keys,
+                                    int32_t *__restrict__ vals)
+{
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < m; c += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t a = clause_off[c], b = clause_off[c + 1], w = b - a;
+        int32_t mv = n;
+        for (int32_t k = a; k < b; ++k) mv = min(mv, abs(lits[k]) - 1);
+        const uint32_t bucket = (uint32_t)(((uint64_t)(mv < 0 ? 0 : mv) << 24) / (uint64_t)(n > 0 ? n : 1));
+        keys[c] = ((uint32_t)(w < 0 ? 0 : (w > 255 ? 255 : w)) << 24) | (bucket & 0xFFFFFFu);
+        vals[c] = (int32_t)c;
+    }
+}
+
 __global__ void k_code_hist(const uint32_t *__restrict__ keys, int64_t L, int32_t *__restrict__ cnt)
 {
     for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < L;
@@ -291,6 +308,9 @@ size_t build_cnf_scratch_bytes(int32_t n, int64_t L)
     return bytes + 256;
 }
 
+#ifndef GALOIS_SWEEP_LOCALITY
+#define GALOIS_SWEEP_LOCALITY 1
+#endif
 cudaError_t launch_build_cnf(int32_t n, int64_t m, int64_t L, const int64_t *d_off64,
                              const int32_t *d_lits, int32_t *d_clause_off, int2 *d_slot_info,
                              int32_t *d_code_off, int32_t *d_occ_slot, int32_t *d_err,
@@ -340,7 +360,21 @@ cudaError_t launch_build_cnf(int32_t n, int64_t m, int64_t L, const int64_t *d_o
     // clause processing order: stable sort of the clauses by width (one 8-bit radix pass;
     // widths >= 255 share the last bucket) so that the clauses a warp handles together
     // have similar widths — no divergence on mixed-width (industrial) CNFs
-    if (m > 0) {
+    if (m > 0 && GALOIS_SWEEP_LOCALITY) {
+        // (width, lowest variable): four stable 8-bit passes, LSD first
+        const int64_t mt = (m + kTile - 1) / kTile;
+        k_width_minvar_keys<<<grid_for(m), kThreads, 0, st>>>(m, n, d_clause_off, d_lits, keys_a, vals_b);
+        uint32_t *kin = keys_a, *kout = keys_b;
+        int32_t *vin = vals_b, *vout = d_clause_perm;
+        for (int ps = 0; ps < 4; ++ps) {
+            k_radix_hist<<<(unsigned)mt, kThreads, 0, st>>>(kin, m, 8 * ps, mt, hist);
+            exclusive_scan(hist, hist, 256 * mt, scan_scratch, st);
+            k_radix_scatter<<<(unsigned)mt, kThreads, 0, st>>>(kin, vin, kout, vout, m, 8 * ps, mt, hist);
+            uint32_t *tk = kin; kin = kout; kout = tk;
+            int32_t *tv = vin; vin = vout; vout = tv;
+        }
+        if (vin != d_clause_perm) cudaMemcpyAsync(d_clause_perm, vin, (size_t)m * 4, cudaMemcpyDeviceToDevice, st);
+    } else if (m > 0) {
         const int64_t mt = (m + kTile - 1) / kTile;
         k_width_keys<<<grid_for(m), kThreads, 0, st>>>(m, d_clause_off, keys_a, vals_b);
         k_radix_hist<<<(unsigned)mt, kThreads, 0, st>>>(keys_a, m, 0, mt, hist);
