@@ -583,8 +583,11 @@ def time_to_sat(G, torch, dev, which="C1", seeds=range(10), batch=None, steps=No
 
 
 def default_lanes(batch_per_gpu):
-    """Concurrent lanes per GPU: 4 once the local batch spans >= 4 chunks of 1024 members
-    (C2 4096: 0.266 -> 0.246 ms/step measured with 4 lanes)."""
+    """Concurrent lanes per GPU: 4 for local batches of 4096-8192 members
+    (C2: 0.266 -> 0.247 ms/step), 2 from 16384 on (C3b: 0.493 -> 0.484 ms with 2 instead of
+    4 lanes; C3a and C5 within 1 %), none below 4096."""
+    if batch_per_gpu >= 16384:
+        return 2
     return 4 if batch_per_gpu >= 4096 else 1
 
 

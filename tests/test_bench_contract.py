@@ -51,6 +51,7 @@ def test_batch_sharding_and_lanes_rules():
     assert bench.batch_of("C5", 1) == (65536, 65536, "strong")
     assert bench.batch_of("C5", 8) == (65536, 8192, "strong")
     assert bench.default_lanes(4096) == 4 and bench.default_lanes(1024) == 1
+    assert bench.default_lanes(16384) == 2 and bench.default_lanes(65536) == 2
     assert bench.effective_lanes(4096, 4, 1) == 4
     assert bench.effective_lanes(3000, 4, 1) == 3          # 1024 + 1024 + 952
     assert bench.effective_lanes(16384, 4, 1) == 4
