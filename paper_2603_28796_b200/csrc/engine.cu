@@ -1069,8 +1069,9 @@ static int prepare(galois_engine *e)
     h.best_b = -1;
     ENG_CUDA(e, pinned_ctrl_acquire(&e->h_ctrl));
     e->h_ctrl[0] = h;
+    // (no sync: later D2H copies into h_ctrl are ordered after this one on the stream, and
+    // the host writes h_ctrl[0] again only after a stream synchronisation)
     ENG_CUDA(e, cudaMemcpyAsync(e->ctrl, &e->h_ctrl[0], sizeof(Ctrl), cudaMemcpyHostToDevice, e->stream));
-    ENG_CUDA(e, cudaStreamSynchronize(e->stream));   // h_ctrl[0] is reused below
     for (auto &ev : e->poll_ev) ENG_CUDA(e, cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
     if (e->use_comm && !e->comm.comm) {  // (a lane's communicator is split from its parent's)
         std::string why;
@@ -1539,15 +1540,26 @@ extern "C" int galois_best_assignment(galois_engine *e, uint8_t *values, int32_t
         return GALOIS_OK;
     }
     Ctrl h;
-    if (int rc = settle(e, &h)) return rc;
-    if (e->use_comm && h.best_b >= 0) {
-        const int root = (int)(h.best_b / e->b_per);
-        std::string why;
-        if (!e->comm.broadcast_bytes(e->best_bits, (size_t)e->cnf->n, root, e->stream, &why))
-            return poison(e, GALOIS_E_NCCL, why);
+    if (!e->use_comm) {                   // one round trip: the control block and the bits together
+        if (int rc = flush_check(e)) return rc;
+        ENG_CUDA(e, cudaMemcpyAsync(&e->h_ctrl[0], e->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, e->stream));
+        if (values)
+            ENG_CUDA(e, cudaMemcpyAsync(values, e->best_bits, (size_t)e->cnf->n, cudaMemcpyDeviceToHost, e->stream));
+        ENG_CUDA(e, cudaStreamSynchronize(e->stream));
+        h = e->h_ctrl[0];
+        if (h.nonfinite) return poison(e, GALOIS_E_NONFINITE, "an iterate became NaN/Inf");
+    } else {
+        if (int rc = settle(e, &h)) return rc;
+        if (h.best_b >= 0) {
+            const int root = (int)(h.best_b / e->b_per);
+            std::string why;
+            if (!e->comm.broadcast_bytes(e->best_bits, (size_t)e->cnf->n, root, e->stream, &why))
+                return poison(e, GALOIS_E_NCCL, why);
+        }
+        if (values)
+            ENG_CUDA(e, cudaMemcpyAsync(values, e->best_bits, (size_t)e->cnf->n, cudaMemcpyDeviceToHost, e->stream));
+        ENG_CUDA(e, cudaStreamSynchronize(e->stream));
     }
-    if (values) ENG_CUDA(e, cudaMemcpyAsync(values, e->best_bits, (size_t)e->cnf->n, cudaMemcpyDeviceToHost, e->stream));
-    ENG_CUDA(e, cudaStreamSynchronize(e->stream));
     if (unsat) *unsat = h.best_u;
     if (global_b) *global_b = h.best_b;
     if (step) *step = h.best_t;
