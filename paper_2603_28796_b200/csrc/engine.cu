@@ -187,6 +187,46 @@ struct Slab {
 
 // Pinned host mirrors of the control block (2 slots per engine) come from one process-wide
 // pinned page: page-locking memory costs ~ms, an engine should not pay it.
+
+// Non-blocking streams are reused across engines and CNF loads (creating one costs ~50 us,
+// as much as the rest of an engine's preparation): released streams are synchronised and
+// parked per device, up to 64.
+static std::mutex g_stream_mu;
+static std::vector<std::pair<int, cudaStream_t>> g_stream_pool;
+
+static cudaError_t stream_acquire(cudaStream_t *out)
+{
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    {
+        std::lock_guard<std::mutex> lock(g_stream_mu);
+        for (size_t i = 0; i < g_stream_pool.size(); ++i)
+            if (g_stream_pool[i].first == dev) {
+                *out = g_stream_pool[i].second;
+                g_stream_pool.erase(g_stream_pool.begin() + (std::ptrdiff_t)i);
+                return cudaSuccess;
+            }
+    }
+    return cudaStreamCreateWithFlags(out, cudaStreamNonBlocking);
+}
+
+static void stream_release(cudaStream_t s)
+{
+    if (!s) return;
+    int dev = 0;
+    if (cudaStreamSynchronize(s) != cudaSuccess || cudaGetDevice(&dev) != cudaSuccess) {
+        cudaGetLastError();
+        cudaStreamDestroy(s);
+        return;
+    }
+    std::lock_guard<std::mutex> lock(g_stream_mu);
+    if (g_stream_pool.size() < 64)
+        g_stream_pool.emplace_back(dev, s);
+    else
+        cudaStreamDestroy(s);
+}
+
 static std::mutex g_pin_mu;
 static Ctrl *g_pin_base = nullptr;
 static std::vector<int> g_pin_free;
@@ -363,7 +403,7 @@ extern "C" int galois_cnf_load(int32_t num_vars, int64_t num_clauses, const int6
     int64_t *d_off64 = nullptr;
     int32_t *d_lits = nullptr;
     CUDA_TRY(use_pool_for_device(dev));
-    CUDA_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    CUDA_TRY(stream_acquire(&st));
     cudaError_t ce = dmalloc(&d_off64, (size_t)num_clauses + 1, st);
     if (ce == cudaSuccess) ce = dmalloc(&d_lits, (size_t)L, st);
     if (ce == cudaSuccess)
@@ -375,12 +415,12 @@ extern "C" int galois_cnf_load(int32_t num_vars, int64_t num_clauses, const int6
         cudaFreeAsync(d_off64, st);
         cudaFreeAsync(d_lits, st);
         cudaStreamSynchronize(st);
-        cudaStreamDestroy(st);
+        stream_release(st);
         return fail(ce == cudaErrorMemoryAllocation ? GALOIS_E_OOM : GALOIS_E_CUDA,
                     std::string("cnf upload: ") + cudaGetErrorString(ce));
     }
     const int rc = cnf_build_device(dev, num_vars, num_clauses, L, d_off64, d_lits, st, out);
-    cudaStreamDestroy(st);
+    stream_release(st);
     return rc;
 }
 
@@ -399,7 +439,7 @@ extern "C" int galois_cnf_normalize(const galois_cnf *in, int32_t k, galois_cnf 
     if (k < 3 || k > 32) return fail(GALOIS_E_ARG, "k must be in [3, 32]");
     CUDA_TRY(cudaSetDevice(in->device));
     cudaStream_t st = nullptr;
-    CUDA_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    CUDA_TRY(stream_acquire(&st));
     int64_t *d_off = nullptr, m2 = 0;
     int32_t *d_lits = nullptr, aux = 0;
     cudaError_t ce = launch::tseitin(in->clause_off, in->slot_info, in->m, in->n, k, &d_off, &d_lits, &m2, &aux, st);
@@ -408,13 +448,13 @@ extern "C" int galois_cnf_normalize(const galois_cnf *in, int32_t k, galois_cnf 
         cudaFreeAsync(d_off, st);
         cudaFreeAsync(d_lits, st);
         cudaStreamSynchronize(st);
-        cudaStreamDestroy(st);
+        stream_release(st);
         return fail(ce == cudaErrorMemoryAllocation ? GALOIS_E_OOM : GALOIS_E_CUDA,
                     std::string("normalize: ") + cudaGetErrorString(ce));
     }
     if (num_aux) *num_aux = aux;
     const int rc = cnf_build_device(in->device, in->n + aux, m2, m2 * k, d_off, d_lits, st, out);
-    cudaStreamDestroy(st);
+    stream_release(st);
     return rc;
 }
 
@@ -902,7 +942,7 @@ static int prepare(galois_engine *e);
 static int prepare_lanes(galois_engine *e, int64_t ls, int64_t lspan)
 {
     if (!e->stream) {
-        ENG_CUDA(e, cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
+        ENG_CUDA(e, stream_acquire(&e->stream));
         e->own_stream = true;
     }
     if (e->use_comm) {                   // one communicator per lane, split from the engine's
@@ -994,7 +1034,7 @@ static int prepare(galois_engine *e)
     if ((uint64_t)n * (uint64_t)e->b_pad / 4 >= (1ull << 40))
         return poison(e, GALOIS_E_ARG, "n * local batch too large");
     if (!e->stream) {
-        ENG_CUDA(e, cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
+        ENG_CUDA(e, stream_acquire(&e->stream));
         e->own_stream = true;
     }
     const size_t nb = (size_t)n * (size_t)e->b_pad;
@@ -1909,7 +1949,7 @@ extern "C" void galois_engine_free(galois_engine *e)
     for (auto ev : e->poll_ev)
         if (ev) cudaEventDestroy(ev);
     if (e->graph) cudaGraphExecDestroy(e->graph);
-    if (e->own_stream && e->stream) cudaStreamDestroy(e->stream);
+    if (e->own_stream && e->stream) stream_release(e->stream);
     cnf_release(e->cnf);
     cudaSetDevice(cur);
     delete e;
