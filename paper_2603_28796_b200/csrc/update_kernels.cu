@@ -90,6 +90,73 @@ __device__ __forceinline__ void count_bits_smem(const uint32_t *srow, int32_t n,
 // back out of the planes: ~11 instructions per row per 32 members instead of ~5.5 per
 // row per 4 members. kIn planes hold the per-thread partial (rows/8 < 2^kIn); the sum
 // needs kIn + 3 planes. Adds the 4 counts of this thread's nibble to G.
+#ifndef GALOIS_HARLEY_SEAL
+#define GALOIS_HARLEY_SEAL 1
+#endif
+// Carry-save adder (one LOP3 each for the sum and the majority).
+__device__ __forceinline__ void csa(uint32_t &h, uint32_t &l, uint32_t a, uint32_t b, uint32_t c)
+{
+    const uint32_t u = a ^ b;
+    h = (a & b) | (u & c);
+    l = u ^ c;
+}
+
+// Add bit-rows sub, sub + 8, ... (< n) of a word column into the vertical counter P[0..kIn)
+// (P[k] = bit k of each lane's count). Harley-Seal: 8 rows cost 7 carry-save adders (14
+// LOP3) plus one carry rippled into P[3..], 4 rows 3 adders plus a carry into P[2..];
+// single rows ripple (2 ops per plane) — instead of 2 kIn ops per row.
+template <int kIn, int kMaxRows>
+__device__ __forceinline__ void add_rows(uint32_t (&P)[kIn], const uint32_t *wcol, int32_t n, int sub)
+{
+    int32_t r = sub;
+    if (kIn >= 4 && kMaxRows >= 8) {
+        for (; r + 56 < n; r += 64) {
+            uint32_t d[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) d[i] = wcol[(r + 8 * i) * 32];
+            uint32_t tA, tB, fA, fB, e;
+            csa(tA, P[0], P[0], d[0], d[1]);
+            csa(tB, P[0], P[0], d[2], d[3]);
+            csa(fA, P[1], P[1], tA, tB);
+            csa(tA, P[0], P[0], d[4], d[5]);
+            csa(tB, P[0], P[0], d[6], d[7]);
+            csa(fB, P[1], P[1], tA, tB);
+            csa(e, P[2], P[2], fA, fB);
+#pragma unroll
+            for (int k = 3; k < kIn; ++k) {
+                const uint32_t t = P[k] & e;
+                P[k] ^= e;
+                e = t;
+            }
+        }
+    }
+    if (kIn >= 3 && kMaxRows >= 4) {
+        for (; r + 24 < n; r += 32) {
+            const uint32_t d0 = wcol[r * 32], d1 = wcol[(r + 8) * 32], d2 = wcol[(r + 16) * 32],
+                           d3 = wcol[(r + 24) * 32];
+            uint32_t tA, tB, f;
+            csa(tA, P[0], P[0], d0, d1);
+            csa(tB, P[0], P[0], d2, d3);
+            csa(f, P[1], P[1], tA, tB);
+#pragma unroll
+            for (int k = 2; k < kIn; ++k) {
+                const uint32_t t = P[k] & f;
+                P[k] ^= f;
+                f = t;
+            }
+        }
+    }
+    for (; r < n; r += 8) {
+        uint32_t c = wcol[r * 32];
+#pragma unroll
+        for (int k = 0; k < kIn; ++k) {
+            const uint32_t t = P[k] & c;
+            P[k] ^= c;
+            c = t;
+        }
+    }
+}
+
 template <int kIn>
 __device__ __forceinline__ void count_rows_sliced(const uint32_t *wcol, int32_t n, int sub, int qp, int32_t G[4])
 {
@@ -97,6 +164,16 @@ __device__ __forceinline__ void count_rows_sliced(const uint32_t *wcol, int32_t 
     uint32_t P[kOut];
 #pragma unroll
     for (int k = 0; k < kOut; ++k) P[k] = 0;
+#if GALOIS_HARLEY_SEAL
+    if (kIn >= 5) {                             // hub chunks (<= 32 rows per thread); the
+        uint32_t Q[kIn];                        // update's short pieces keep the ripple below
+#pragma unroll
+        for (int k = 0; k < kIn; ++k) Q[k] = 0;
+        add_rows<kIn, (1 << kIn) - 1>(Q, wcol, n, sub);
+#pragma unroll
+        for (int k = 0; k < kIn; ++k) P[k] = Q[k];
+    } else
+#endif
     for (int32_t r = sub; r < n; r += 8) {
         uint32_t c = wcol[r * 32];
 #pragma unroll
@@ -138,6 +215,10 @@ __device__ __forceinline__ void count_rows_sliced(const uint32_t *wcol, int32_t 
 template <int kIn>
 __device__ __forceinline__ void sliced_add(uint32_t (&P)[kIn], const uint32_t *wcol, int32_t n, int sub)
 {
+#if GALOIS_HARLEY_SEAL
+    add_rows<kIn, 4>(P, wcol, n, sub);          // a piece has <= 32 rows: <= 4 per thread
+    return;
+#endif
     for (int32_t r = sub; r < n; r += 8) {
         uint32_t c = wcol[r * 32];
 #pragma unroll
