@@ -90,6 +90,9 @@ __device__ __forceinline__ void count_bits_smem(const uint32_t *srow, int32_t n,
 // back out of the planes: ~11 instructions per row per 32 members instead of ~5.5 per
 // row per 4 members. kIn planes hold the per-thread partial (rows/8 < 2^kIn); the sum
 // needs kIn + 3 planes. Adds the 4 counts of this thread's nibble to G.
+#ifndef GALOIS_HUB_CF
+#define GALOIS_HUB_CF 1
+#endif
 #ifndef GALOIS_HARLEY_SEAL
 #define GALOIS_HARLEY_SEAL 1
 #endif
@@ -707,6 +710,46 @@ __global__ void __launch_bounds__(256 + 32, kTmaCtasPerSm) k_hub_partial_tma(Dev
     } else {
         const int sh = tid & 7;
         uint32_t slot = 0;
+#if GALOIS_HUB_CF
+        // Row pass with lane = word and warp = row subset (rows warp, warp + 8, ...): the 32
+        // lanes of an LDS read 32 different banks (the quad mapping below would put the 8
+        // row-sharing lanes of a word on one bank: 8-way conflicts). The 8 warps' partial
+        // counters meet in shared memory (double-buffered by item parity, one named barrier
+        // of the 256 consumer threads per item); thread (word tid / 8, quad tid % 8) sums
+        // its 4 members' counts over them.
+        constexpr int kHP = kHubChunk <= 248 ? 5 : 6;
+        __shared__ uint32_t sP[2][kConsumerWarps][kHP][32];
+        for (uint32_t item = blockIdx.x; item < rm.items; item += gridDim.x, ++slot) {
+            const int st = (int)(slot % kStages);
+            mbar_wait(&full[st], (slot / kStages) & 1u);
+            const int4 h = hdr[st];
+            uint32_t Q[kHP];
+#pragma unroll
+            for (int k = 0; k < kHP; ++k) Q[k] = 0;
+            add_rows<kHP, (1 << kHP) - 1>(Q, reinterpret_cast<const uint32_t *>(smem + st * kHubStageBytes) + lane, h.z,
+                                         warp);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[st]);            // this warp is done with the stage
+            const int pb = (int)(slot & 1u);
+#pragma unroll
+            for (int k = 0; k < kHP; ++k) sP[pb][warp][k][lane] = Q[k];
+            asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32) : "memory");
+            int32_t G[4] = {0, 0, 0, 0};
+            const int w2 = tid >> 3;
+#pragma unroll
+            for (int k = 0; k < kHP; ++k) {
+                uint32_t acc = 0;                               // bytes: <= 8 per member
+#pragma unroll
+                for (int wp = 0; wp < kConsumerWarps; ++wp) acc += quad_bits(sP[pb][wp][k][w2], sh);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) G[j] += (int32_t)((acc >> (8 * j)) & 255u) << k;
+            }
+            const int32_t nneg = h.z - h.y;
+            G[0] -= nneg; G[1] -= nneg; G[2] -= nneg; G[3] -= nneg;
+            const uint32_t ch = item - (uint32_t)h.w * rm.cpr;
+            partial[(size_t)h.w * rm.QW + ch * 256u + tid] = make_short4((short)G[0], (short)G[1], (short)G[2], (short)G[3]);
+        }
+#else
         for (uint32_t item = blockIdx.x; item < rm.items; item += gridDim.x, ++slot) {
             const int st = (int)(slot % kStages);
             mbar_wait(&full[st], (slot / kStages) & 1u);
@@ -723,6 +766,7 @@ __global__ void __launch_bounds__(256 + 32, kTmaCtasPerSm) k_hub_partial_tma(Dev
             const uint32_t ch = item - (uint32_t)h.w * rm.cpr;
             partial[(size_t)h.w * rm.QW + ch * 256u + tid] = make_short4((short)G[0], (short)G[1], (short)G[2], (short)G[3]);
         }
+#endif
     }
 }
 
