@@ -83,7 +83,7 @@ __device__ __forceinline__ void count_bits_smem(const uint32_t *srow, int32_t n,
     for (int j = 0; j < 4; ++j) G[j] += (int32_t)((acc >> (8 * j)) & 255u);
 }
 
-// Long segments (hub chunks of up to 128 rows): the 8 threads sharing a 32-member word
+// Long segments (32-row pieces of the update): the 8 threads sharing a 32-member word
 // split the rows (thread i takes rows i, i+8, ...) and add FULL words into a bit-sliced
 // counter (one half adder per plane), then sum the 8 partial counters by a 3-round
 // shuffle butterfly (one full adder per plane) and each thread reads its nibble's counts
