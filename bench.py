@@ -8,8 +8,8 @@ A "step" is one pass of the whole hot path over the batch: sample, clause forwar
 straight-through signal + Adam update + rounding (fused), exact check, best tracking
 (and the NCCL MIN all-reduce of the best key when N > 1). Metric: literal-evaluations/s
 (L x B x steps / time, one "literal evaluation" = one (slot, member) pair of one step),
-whole job over all ranks; weak scaling (B = 4096 per GPU for C2). Prints ONE JSON line
-on rank 0.
+whole job over all ranks; weak scaling (default workload C4 = configs[3], the north_star
+instance: 1M variables, 4.2M clauses, B = 1024 per GPU). Prints ONE JSON line on rank 0.
 """
 from __future__ import annotations
 
@@ -317,7 +317,8 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--workload", default="C2", choices=sorted(WORKLOADS))
+    # default: the north_star instance (configs[3], 1M variables, 4.2M clauses)
+    ap.add_argument("--workload", default="C4", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--ref-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -615,7 +616,8 @@ def run_e2e(G, inst, B, args, torch, dev, lanes=1):
         torch.cuda.synchronize(dev)
         t0 = time.perf_counter()
         cnf = G.Cnf(inst.n, off, lits)
-        eng = G.Engine(cnf, B, args.steps, 0.5, 0, cubes=inst.pins, lanes=lanes)
+        eng = G.Engine(cnf, B, args.steps, 0.5, 0, cubes=inst.pins, lanes=lanes,
+                       check_interval=args.check_interval)
         eng.run()
         counts, _ = eng.unsat_counts()
         best = eng.best_assignment()
@@ -627,7 +629,9 @@ def run_e2e(G, inst, B, args, torch, dev, lanes=1):
         results.append((el, done))
     el, done = sorted(results[-5:])[2]
     h2d = off.nbytes + lits.nbytes + 8 * (args.steps + 2) + 64
-    polls = (args.steps + 3) // 4 + 2
+    K = args.check_interval                      # run(): one 64-byte poll per chunk of G steps
+    KK = K if K % 2 == 0 else 2 * K
+    polls = -(-args.steps // (KK * max(1, 8 // KK))) + 2
     d2h = 64 * polls + 4 * B + inst.n
     return {"value": inst.L * B * done / el, "unit": UNIT, "steps": done,
             "h2d_bytes_per_step": h2d / max(done, 1), "d2h_bytes_per_step": d2h / max(done, 1),

@@ -93,6 +93,11 @@ int galois_cnf_normalize(const galois_cnf *cnf, int32_t k, galois_cnf **out, int
 /* Copy the CSR back in DIMACS form (test hook): offsets m+1 int64, literals L int32. */
 int galois_cnf_get_csr(const galois_cnf *cnf, int64_t *clause_offsets, int32_t *literals);
 
+/* Variables of the CNF before normalisation (= num_vars unless made by galois_cnf_normalize,
+ * whose auxiliaries f_j are variables n_orig+1 ..; P:214 excludes them from the candidate
+ * literals, and cubes branch on original variables only). */
+int galois_cnf_original_vars(const galois_cnf *cnf, int32_t *n_orig);
+
 /* Drop the caller's reference (engines hold their own). NULL is a no-op. */
 void galois_cnf_free(galois_cnf *cnf);
 
@@ -102,7 +107,8 @@ void galois_cnf_free(galois_cnf *cnf);
  * steps >= 0 optimiser steps ("epochs", one full-batch step each), learning
  * rate lr > 0 (paper 0.5) and RNG seed. Defaults: ST mode, tau = 1, Adam (0.9, 0.999,
  * 1e-8), check interval 1, no cubes, world = 1. Device memory is allocated and the
- * logits initialised lazily at the first step/run/get (so setters may follow create). */
+ * logits initialised lazily at the first step/run/get (so setters may follow create);
+ * a local slice b_per >= 2^31 - 1024 members is rejected there (E_ARG). */
 int galois_engine_create(const galois_cnf *cnf, int64_t batch, int32_t steps, double lr,
                          uint64_t seed, galois_engine **out);
 
@@ -171,7 +177,16 @@ int galois_engine_set_cubes(galois_engine *eng, int32_t d, const int32_t *vars);
 
 /* Join an NCCL communicator of `world` ranks (one per GPU) created from a 128-byte
  * ncclUniqueId produced by galois_comm_unique_id on one rank and shared by the caller.
- * The communicator is initialised (collectively) at the first step. */
+ * The communicator is initialised (collectively) at the first step.
+ * Exchange (row a9; mechanism ours, the paper's 2 -> 8 GPU split is Table 3):
+ * every rank keeps its own best record and the winner's bits exactly as on one rank; after
+ * each check an 8-byte MIN all-reduce of (u << 32 | global member) and the global record
+ * update run on an engine-owned exchange stream, overlapping the update of the same step;
+ * the main stream joins it before the next sweep. The global record (u*, t*, b*), its bits
+ * (broadcast from the owner rank, b* / b_per), the unsat counts and steps_done are exactly
+ * the single-GPU result; a rank that did not hold the SAT member may run one update past t*
+ * (its iterate then is one step ahead; no further check runs). All ranks must make the same
+ * sequence of step / enqueue / run / best_assignment calls. */
 int galois_engine_set_comm(galois_engine *eng, int32_t rank, int32_t world, const void *nccl_unique_id);
 
 /* Use the caller's CUDA stream (a cudaStream_t, e.g. torch.cuda.current_stream()). */
@@ -203,12 +218,19 @@ int galois_engine_set_subbatch(galois_engine *eng, int32_t sub_batch);
  * member's trajectory is the undivided engine's, and the best record (u*, t*, b*) and its
  * assignment are identical (lexicographic minimum over the lanes' records). After a SAT,
  * lanes other than the winner's may have run up to two CUDA-graph chunks (16 steps) past t*;
- * unsat_counts then reports their members' counts at their own last check. Applies when
- * the slice spans more than one lane, in ST mode, without NCCL (world = 1), sub-batching or
- * debug; otherwise the engine is undivided. get_iterate / set_iterate / get_grad /
- * get_loss / get_bits return E_STATE on a split engine; kernel_times sums over the lanes.
+ * unsat_counts then reports their members' counts at their own last check. Applies only
+ * when the slice spans more than one lane, in ST mode, WITHOUT an NCCL communicator
+ * (set_comm: concurrent collectives on several communicators of one device are not
+ * guaranteed to progress), without sub-batching or debug; otherwise the engine is
+ * undivided. get_iterate / set_iterate / get_loss / get_bits / get_member act on every lane
+ * (set_iterate: each lane from the same step t); kernel_times sums over the lanes.
  * Setter: valid only before the first step. */
 int galois_engine_set_lanes(galois_engine *eng, int32_t lanes);
+
+/* CUDA graphs for run(): -1 never, 0 automatic (graphs of 8-step chunks when the run has
+ * >= 32 chunks left), 1 always (also bypasses the single-launch small-instance run). The
+ * result is identical in every mode (kernels read the step index from the device). */
+int galois_engine_set_graphs(galois_engine *eng, int32_t mode);
 
 /* Device bytes one member costs in the given mode (z, m, v, bit planes, E or soft
  * buffers, counters), for sizing sub_batch to a memory budget. */
@@ -232,21 +254,26 @@ int galois_comm_unique_id(void *out128);
  * z_v = theta_{v,1} - theta_{v,0} (n floats, host). Local to this rank. */
 int galois_select_member(galois_engine *eng, int32_t rule, int64_t *global_b, int32_t *unsat, float *z);
 
+/* |S| = max(1, ceil(rho * n_orig)) of galois_candidate_pool (Eq.11), for sizing
+ * its units array. E_ARG unless 0 < rho <= 1. */
+int galois_candidate_pool_size(const galois_cnf *cnf, double rho, int32_t *S);
+
 /* Candidate pool (Eq.10) of member `global_b` (local to this rank): N samples
  * x^(k)_v = [z_v + ell^(k)_v >= 0] with fresh logistic noise (Philox counter (v, k/4, 0, 2),
- * word k mod 4, key pool_seed) and confidences c^(k)_v = max(y_0, y_1) = sigma(|z_v + ell|/tau);
- * and per candidate the S = max(1, ceil(rho * n)) most confident variables (Eq.11,
- * P:221-237; paper rho = 0.0005) as DIMACS unit literals (+v if x = 1, else -v),
- * ordered by descending confidence, ties to the lower index.
+ * word k mod 4, key pool_seed) and confidences c^(k)_v = max(y_0, y_1) = sigma(|z_v + ell|/tau)
+ * over all n variables; and per candidate the S = max(1, ceil(rho * n_orig)) most confident
+ * ORIGINAL variables (Eq.11, auxiliaries excluded as P:214 states; paper
+ * rho = 0.0005) as DIMACS unit literals (+v if x = 1, else -v), ordered by descending
+ * confidence, ties to the lower index.
  *   values [N][n] uint8 (may be NULL), confidence [N][n] float (may be NULL),
  *   units [N][S] int32 (may be NULL; S <= 4096), *S_out = S. E_ARG on bad sizes. */
 int galois_candidate_pool(galois_engine *eng, int64_t global_b, int32_t N, double rho, uint64_t pool_seed,
                           uint8_t *values, float *confidence, int32_t *units, int32_t *S_out);
 
 /* Confidence-guided branching (Lemma 1: "identify d variables with the lowest
- * confidence"): the d variables of member global_b with the lowest noise-free confidence
- * sigma(|z_v|/tau) (= smallest |z_v|), ties to the lower index, 1-based ascending — ready
- * for galois_engine_set_cubes. 1 <= d <= min(n, 4096). */
+ * confidence"): the d original variables (1..n_orig) of member global_b with the lowest
+ * noise-free confidence sigma(|z_v|/tau) (= smallest |z_v|), ties to the lower index,
+ * 1-based ascending — ready for galois_engine_set_cubes. 1 <= d <= min(n_orig, 4096). */
 int galois_cube_variables(galois_engine *eng, int64_t global_b, int32_t d, int32_t *vars);
 
 /* ------------------------------------------------------ test hooks (parity / resume) */
@@ -259,6 +286,17 @@ int galois_engine_get_iterate(galois_engine *eng, float *z, float *m, float *v, 
  * and the next sample X_{t+1}; clears the stop flag (the best record is kept). */
 int galois_engine_set_iterate(galois_engine *eng, const float *z, const float *m, const float *v,
                               int32_t t);
+
+/* One member's state, read in place on the device (works on lanes and at full size) and
+ * WITHOUT running a pending check (unlike unsat_counts): reduced iterate z, m, v (n floats
+ * each), the sample bits X_{t+1} the next forward uses and the rounding R_t (n bytes 0/1
+ * each), with set_debug(1) the last step's signal G (n int32) and g1 (n floats); t = the
+ * steps of the engine (or lane) holding the member; unsat = its count at the last check
+ * that ran, check_t = that check's step. Any output may be NULL. E_ARG if global_b is not
+ * local; E_STATE on a sub-batched engine. */
+int galois_engine_get_member(galois_engine *eng, int64_t global_b, float *z, float *m, float *v,
+                             uint8_t *x_next, uint8_t *r, int32_t *G, float *g1, int32_t *t,
+                             int32_t *unsat, int32_t *check_t);
 
 /* Of the last step (requires set_debug(1) before the first step): the clause signal
  * G = sum over occurrences of sigma * E (int32; ST mode) and dL/dtheta_1 = -G p q / tau

@@ -51,6 +51,9 @@ def _compile(src: str, verbose: bool) -> str:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    if any(f.startswith("-DGALOIS_PARITY_BREAKING_EXPERIMENT") for f in EXTRA) and LIB == os.path.join(PKG, "libgalois.so"):
+        raise RuntimeError("parity-breaking experiment builds must go to their own GALOIS_LIB_OUT, "
+                           "never to the product libgalois.so")
     os.makedirs(OBJ, exist_ok=True)
     todo = [s for s in SOURCES if force or _stale(os.path.join(OBJ, s + ".o"), os.path.join(CSRC, s))]
     with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:

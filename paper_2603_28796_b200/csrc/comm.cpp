@@ -30,7 +30,6 @@ struct NcclApi {
     ncclResult_t (*Broadcast)(const void *, void *, size_t, ncclDataType_t, int, ncclComm_t,
                               cudaStream_t) = nullptr;
     const char *(*GetErrorString)(ncclResult_t) = nullptr;
-    ncclResult_t (*CommSplit)(ncclComm_t, int, int, ncclComm_t *, ncclConfig_t *) = nullptr;   // NCCL >= 2.18
 };
 
 NcclApi g_api;
@@ -65,7 +64,6 @@ bool nccl_load(std::string *why)
             g_api.why = "libnccl.so.2 lacks a required symbol";
         } else {
             g_api.ok = true;
-            sym(h, "ncclCommSplit", g_api.CommSplit);     // optional: lanes over NCCL
         }
     }
     if (!g_api.ok && why) *why = g_api.why;
@@ -103,25 +101,6 @@ bool Comm::init(int rank_, int world_, const unsigned char *id128, std::string *
     if (r != ncclSuccess) {
         comm = nullptr;
         if (why) *why = nccl_err("ncclCommInitRank", r);
-        return false;
-    }
-    return true;
-}
-
-// A communicator over the same ranks (ncclCommSplit with one color; collective: every rank
-// calls it in the same order), for an engine lane with its own stream.
-bool Comm::dup_from(const Comm &parent, std::string *why)
-{
-    rank = parent.rank;
-    world = parent.world;
-    if (!g_api.CommSplit) {
-        if (why) *why = "libnccl.so.2 lacks ncclCommSplit (NCCL < 2.18)";
-        return false;
-    }
-    ncclResult_t r = g_api.CommSplit(parent.comm, 0, parent.rank, &comm, nullptr);
-    if (r != ncclSuccess) {
-        comm = nullptr;
-        if (why) *why = nccl_err("ncclCommSplit", r);
         return false;
     }
     return true;

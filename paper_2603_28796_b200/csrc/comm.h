@@ -16,7 +16,6 @@ struct Comm {
     ncclComm_t comm = nullptr;
 
     bool init(int rank, int world, const unsigned char *id128, std::string *why);
-    bool dup_from(const Comm &parent, std::string *why);
     bool allreduce_min_u64(const unsigned long long *send, unsigned long long *recv, cudaStream_t st,
                            std::string *why);
     bool broadcast_bytes(void *buf, size_t bytes, int root, cudaStream_t st, std::string *why);

@@ -40,9 +40,10 @@ void update_st(const DevCnf &c, const StepParams &p, float *z, float *m, float *
                cudaStream_t st);
 void best(const int32_t *unsat, int32_t *unsat_last, int32_t b_loc, int64_t b0, Ctrl *ctrl, bool finalize,
           cudaStream_t st);
-void finalize(Ctrl *ctrl, int64_t b0, int32_t b_loc, cudaStream_t st);
+void gfinalize(Ctrl *ctrl, cudaStream_t st);
 void extract(const uint32_t *R, int32_t n, int32_t W, int64_t b0, const Ctrl *ctrl, uint8_t *best_bits,
              cudaStream_t st);
+void member_bits(const uint32_t *X, int32_t n, int32_t W, int32_t lb, uint8_t *x_out, uint8_t *r_out, cudaStream_t st);
 // SOFT mode (soft_kernels.cu)
 void forward_soft(const DevCnf &c, const StepParams &p, const float *z, float *P, float *Es, float *lam,
                   Ctrl *ctrl, cudaStream_t st);
@@ -56,7 +57,8 @@ void select_member(const int32_t *counts, int32_t b_loc, int64_t b0, int32_t rul
 void gather_z(const float *z, int32_t n, int32_t b_pad, int32_t lb, float *out, cudaStream_t st);
 void pool(const float *zsel, int32_t n, int32_t N, float inv_tau, uint64_t pool_seed, uint8_t *x, float *conf,
           cudaStream_t st);
-void topk(const uint8_t *x, const float *conf, int32_t n, int32_t N, int32_t S, int32_t *units, cudaStream_t st);
+void topk(const uint8_t *x, const float *conf, int32_t n, int32_t n_sel, int32_t N, int32_t S, int32_t *units,
+          cudaStream_t st);
 void lowconf(const float *zsel, int32_t n, int32_t d, int32_t *vars, cudaStream_t st);
 int max_sorted();
 }  // namespace launch
@@ -99,6 +101,7 @@ struct galois_cnf {
     std::atomic<int> refs{1};
     int device = 0;
     int32_t n = 0;
+    int32_t n_orig = 0;      // variables of the CNF before normalisation (= n unless normalised)
     int64_t m = 0;
     int64_t L = 0;
     int32_t max_width = 0;
@@ -290,6 +293,7 @@ static int cnf_build_device(int dev, int32_t num_vars, int64_t num_clauses, int6
     galois_cnf *c = new galois_cnf();
     c->device = dev;
     c->n = num_vars;
+    c->n_orig = num_vars;
     c->m = num_clauses;
     c->L = L;
     const int64_t m = num_clauses;
@@ -454,6 +458,7 @@ extern "C" int galois_cnf_normalize(const galois_cnf *in, int32_t k, galois_cnf 
     }
     if (num_aux) *num_aux = aux;
     const int rc = cnf_build_device(in->device, in->n + aux, m2, m2 * k, d_off, d_lits, st, out);
+    if (rc == GALOIS_OK) (*out)->n_orig = in->n_orig;   // auxiliaries are not candidates
     stream_release(st);
     return rc;
 }
@@ -491,6 +496,27 @@ extern "C" int galois_cnf_info(const galois_cnf *c, int32_t *n, int64_t *m, int6
     return GALOIS_OK;
 }
 
+extern "C" int galois_cnf_original_vars(const galois_cnf *c, int32_t *n_orig)
+{
+    if (!c || !n_orig) return fail(GALOIS_E_ARG, "cnf and n_orig are required");
+    *n_orig = c->n_orig;
+    return GALOIS_OK;
+}
+
+// Eq.11: |S| = max(1, ceil(rho n)) over the original variables.
+static int32_t units_per_candidate(const galois_cnf *c, double rho)
+{
+    return std::max<int32_t>(1, (int32_t)std::ceil(rho * (double)c->n_orig - 1e-9));
+}
+
+extern "C" int galois_candidate_pool_size(const galois_cnf *c, double rho, int32_t *S)
+{
+    if (!c || !S) return fail(GALOIS_E_ARG, "cnf and S are required");
+    if (!(rho > 0.0 && rho <= 1.0)) return fail(GALOIS_E_ARG, "need 0 < rho <= 1");
+    *S = units_per_candidate(c, rho);
+    return GALOIS_OK;
+}
+
 extern "C" int galois_cnf_get_csc(const galois_cnf *c, int32_t *code_off, int32_t *occ_slot)
 {
     if (!c) return fail(GALOIS_E_ARG, "cnf is NULL");
@@ -516,6 +542,12 @@ struct galois_engine {
     int32_t rank = 0, world = 1;
     unsigned char nccl_id[128] = {0};
     bool use_comm = false;         // NCCL path (world > 1, or a 1-rank communicator for tests)
+    // NCCL exchange off the critical path: the MIN all-reduce and k_gfinalize of a check run
+    // on `xstream` (forked after the checking sweep by ev_chk) while the update runs; the
+    // main stream joins ev_x before its next sweep or result read (x_pending)
+    cudaStream_t xstream = nullptr;
+    cudaEvent_t ev_chk = nullptr, ev_x = nullptr;
+    bool x_pending = false;
     bool debug = false, profiling = false;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
@@ -576,6 +608,7 @@ struct galois_engine {
     cudaGraphExec_t graph = nullptr;
     int32_t graph_steps = 0;
     bool graph_failed = false;
+    int32_t graphs_mode = 0;     // galois_engine_set_graphs: -1 never, 0 auto, 1 always
     // profiling
     struct Rec {
         int cls;
@@ -623,16 +656,16 @@ struct galois_engine {
         return e;
     }
     template <typename F>
-    void timed(int cls, F &&f)
+    void timed(int cls, F &&f, cudaStream_t on = nullptr)
     {
         if (!profiling) {
             f();
             return;
         }
         Rec r{cls, take_event(), take_event()};
-        cudaEventRecord(r.a, stream);
+        cudaEventRecord(r.a, on ? on : stream);
         f();
-        cudaEventRecord(r.b, stream);
+        cudaEventRecord(r.b, on ? on : stream);
         recs.push_back(r);
     }
 };
@@ -688,6 +721,24 @@ extern "C" int galois_engine_create(const galois_cnf *cnf, int64_t batch, int32_
 
 // results formed over several sub-engines / windows (f4 windows, lanes)
 static bool aggregated(const galois_engine *e) { return e->windows > 1 || !e->lane.empty(); }
+
+// Test hooks on a split engine: f(lane, offset of the lane's first member in the slice) for
+// every lane holding members (host arrays are [local member][...], so lane rows follow each
+// other).
+template <typename F>
+static int for_each_lane(galois_engine *e, F &&f)
+{
+    for (galois_engine *l : e->lane) {
+        if (l->b_loc == 0) continue;
+        if (int rc = f(l, (size_t)(l->b0 - e->b0))) return rc;
+    }
+    return GALOIS_OK;
+}
+
+#define NO_WINDOWS(e)                                                                                        \
+    do {                                                                                                     \
+        if ((e)->windows > 1) return fail(GALOIS_E_STATE, "not available on a sub-batched engine (run only)"); \
+    } while (0)
 
 #define SETTER_ENTRY(e)                                                                        \
     do {                                                                                       \
@@ -809,6 +860,14 @@ extern "C" int galois_engine_set_lanes(galois_engine *e, int32_t lanes)
     return GALOIS_OK;
 }
 
+extern "C" int galois_engine_set_graphs(galois_engine *e, int32_t mode)
+{
+    SETTER_ENTRY(e);
+    if (mode < -1 || mode > 1) return fail(GALOIS_E_ARG, "graphs mode must be -1, 0 or 1");
+    e->graphs_mode = mode;
+    return GALOIS_OK;
+}
+
 extern "C" int galois_comm_unique_id(void *out128)
 {
     if (!out128) return fail(GALOIS_E_ARG, "out is NULL");
@@ -842,31 +901,54 @@ static BestArgs best_args(const galois_engine *e)
     ba.unsat_last = e->unsat_last;
     ba.b_loc = e->b_loc;
     ba.b0 = e->b0;
-    ba.finalize = e->use_comm ? 0 : 1;
+    ba.finalize = 1;                  // this rank's record (with NCCL the global one follows on xstream)
     // small instances: the sweep's last CTA also copies the winner's bits (n loads in one
     // CTA); large ones launch the grid-wide k_extract instead
     ba.best_bits = e->best_bits;
     ba.W = e->W;
-    ba.extract_n = (!e->use_comm && e->cnf->n <= 32768) ? e->cnf->n : 0;
+    ba.extract_n = e->cnf->n <= 32768 ? e->cnf->n : 0;
     return ba;
 }
 
+// The main stream waits for the exchange of the last check (before anything that rewrites
+// key_local, reads the control block, or ends a graph capture). One step of lag at most:
+// a rank that did not hold the SAT member may run the update right after the deciding check.
+static int exchange_join(galois_engine *e)
+{
+    if (!e->x_pending) return GALOIS_OK;
+    ENG_CUDA(e, cudaStreamWaitEvent(e->stream, e->ev_x, 0));
+    e->x_pending = false;
+    return GALOIS_OK;
+}
+
+// a9 with NCCL: fork the check's key to the exchange stream, MIN all-reduce it over the
+// ranks and fold it into the global record there; the main stream continues with the update.
+static int exchange_fork(galois_engine *e)
+{
+    ENG_CUDA(e, cudaEventRecord(e->ev_chk, e->stream));
+    ENG_CUDA(e, cudaStreamWaitEvent(e->xstream, e->ev_chk, 0));
+    std::string why;
+    if (!e->comm.allreduce_min_u64(&e->ctrl->key_local, &e->ctrl->key_global, e->xstream, &why))
+        return poison(e, GALOIS_E_NCCL, why);
+    e->timed(3, [&] { launch::gfinalize(e->ctrl, e->xstream); }, e->xstream);
+    ENG_CUDA(e, cudaEventRecord(e->ev_x, e->xstream));
+    e->x_pending = true;
+    return GALOIS_OK;
+}
+
 // After the counts of a check are complete. best_done: the sweep's last CTA already
-// reduced them (and finalized on one rank). extract: launch k_extract for the winner's
-// bits (false when the sweep's last CTA already copied them).
+// reduced them into this rank's record. extract: launch k_extract for the record's bits
+// (false when the sweep's last CTA already copied them). With NCCL the exchange follows
+// on its own stream.
 static int enqueue_best(galois_engine *e, bool best_done, bool extract)
 {
     if (!best_done)
-        e->timed(3, [&] { launch::best(e->unsat, e->unsat_last, e->b_loc, e->b0, e->ctrl, !e->use_comm, e->stream); });
-    if (e->use_comm) {
-        std::string why;
-        if (!e->comm.allreduce_min_u64(&e->ctrl->key_local, &e->ctrl->key_global, e->stream, &why))
-            return poison(e, GALOIS_E_NCCL, why);
-        e->timed(3, [&] { launch::finalize(e->ctrl, e->b0, e->b_loc, e->stream); });
-    }
+        e->timed(3, [&] { launch::best(e->unsat, e->unsat_last, e->b_loc, e->b0, e->ctrl, true, e->stream); });
     if (extract)
         e->timed(3, [&] { launch::extract(e->R, e->cnf->n, e->W, e->b0, e->ctrl, e->best_bits, e->stream); });
     ENG_CUDA(e, cudaGetLastError());
+    if (e->use_comm)
+        if (int rc = exchange_fork(e)) return rc;
     return GALOIS_OK;
 }
 
@@ -875,6 +957,7 @@ static int enqueue_best(galois_engine *e, bool best_done, bool extract)
 static int flush_check(galois_engine *e)
 {
     if (!e->pending_check) return GALOIS_OK;
+    if (int rc = exchange_join(e)) return rc;
     const DevCnf c = e->cnf->view();
     ENG_CUDA(e, cudaMemsetAsync(e->unsat, 0, sizeof(int32_t) * (size_t)e->b_pad, e->stream));
     bool done = false;
@@ -897,6 +980,7 @@ static int enqueue_step(galois_engine *e)
     const DevCnf c = e->cnf->view();
     StepParams p = e->params();
     const int32_t s = e->steps_enqueued + 1;
+    if (int rc = exchange_join(e)) return rc;
     if (e->mode == GALOIS_MODE_ST) {
         const bool chk = e->pending_check;
         // Lambda of step s goes to lam[s & 1]; the update of step s zeroes lam[(s+1) & 1]
@@ -945,10 +1029,6 @@ static int prepare_lanes(galois_engine *e, int64_t ls, int64_t lspan)
         ENG_CUDA(e, stream_acquire(&e->stream));
         e->own_stream = true;
     }
-    if (e->use_comm) {                   // one communicator per lane, split from the engine's
-        std::string why;
-        if (!e->comm.init(e->rank, e->world, e->nccl_id, &why)) return poison(e, GALOIS_E_NCCL, why);
-    }
     e->lane_size = ls;
     for (int64_t off = 0; off < lspan; off += ls) {
         galois_engine *l = new galois_engine();
@@ -968,18 +1048,12 @@ static int prepare_lanes(galois_engine *e, int64_t ls, int64_t lspan)
         l->seed = e->seed;
         l->pins = e->pins;
         l->profiling = e->profiling;
+        l->graphs_mode = e->graphs_mode;
         l->fixed_slice = true;
         l->b0 = e->b0 + off;
         l->b_loc = (int32_t)std::max<int64_t>(0, std::min<int64_t>(ls, e->b_loc - off));
-        l->b_per = e->b_per;             // rank stride of the global member index (winner's owner)
-        l->use_comm = e->use_comm;
-        l->rank = e->rank;
-        l->world = e->world;
+        l->b_per = e->b_per;
         e->lane.push_back(l);
-        if (e->use_comm) {
-            std::string why;
-            if (!l->comm.dup_from(e->comm, &why)) return poison(e, GALOIS_E_NCCL, why);
-        }
         if (int rc = prepare(l)) {
             e->poisoned = true;
             return rc;
@@ -1008,6 +1082,7 @@ static int prepare(galois_engine *e)
         per = (per + 31) / 32 * 32;
         e->b_per = per;
         e->b0 = per * e->rank;
+        if (per > INT32_MAX - 1024) return poison(e, GALOIS_E_ARG, "local batch slice must be < 2^31 - 1024 members");
         const int64_t left = e->B - e->b0;
         e->b_loc = (int32_t)std::max<int64_t>(0, std::min<int64_t>(per, left));
     }
@@ -1019,9 +1094,8 @@ static int prepare(galois_engine *e)
         e->windows = (int32_t)((span + e->sub - 1) / e->sub);
         e->b_loc = (int32_t)std::min<int64_t>(e->sub, e->slice_loc);
     }
-    if (e->lanes_req > 1 && e->windows == 1 && e->mode == GALOIS_MODE_ST && !e->debug) {
-        // with NCCL every rank forms the same lanes (from b_per; the last rank's may be short or empty)
-        const int64_t lspan = e->use_comm ? e->b_per : e->b_loc;
+    if (e->lanes_req > 1 && e->windows == 1 && e->mode == GALOIS_MODE_ST && !e->debug && !e->use_comm) {
+        const int64_t lspan = e->b_loc;
         const int64_t per_lane = (lspan + e->lanes_req - 1) / e->lanes_req;
         const int64_t ls = (per_lane + 1023) / 1024 * 1024;
         if (lspan > ls) return prepare_lanes(e, ls, lspan);
@@ -1104,18 +1178,21 @@ static int prepare(galois_engine *e)
     Ctrl h{};
     h.t = 0;
     h.stopped = 0;
-    h.best_u = INT32_MAX;
-    h.best_t = -1;
-    h.best_b = -1;
+    h.best_u = h.g_u = INT32_MAX;
+    h.best_t = h.g_t = -1;
+    h.best_b = h.g_b = -1;
     ENG_CUDA(e, pinned_ctrl_acquire(&e->h_ctrl));
     e->h_ctrl[0] = h;
     // (no sync: later D2H copies into h_ctrl are ordered after this one on the stream, and
     // the host writes h_ctrl[0] again only after a stream synchronisation)
     ENG_CUDA(e, cudaMemcpyAsync(e->ctrl, &e->h_ctrl[0], sizeof(Ctrl), cudaMemcpyHostToDevice, e->stream));
     for (auto &ev : e->poll_ev) ENG_CUDA(e, cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-    if (e->use_comm && !e->comm.comm) {  // (a lane's communicator is split from its parent's)
+    if (e->use_comm) {
         std::string why;
         if (!e->comm.init(e->rank, e->world, e->nccl_id, &why)) return poison(e, GALOIS_E_NCCL, why);
+        ENG_CUDA(e, stream_acquire(&e->xstream));
+        ENG_CUDA(e, cudaEventCreateWithFlags(&e->ev_chk, cudaEventDisableTiming));
+        ENG_CUDA(e, cudaEventCreateWithFlags(&e->ev_x, cudaEventDisableTiming));
     }
     e->prepared = true;
     // a3: initial logits, first sample, and the check at t = 0
@@ -1142,12 +1219,14 @@ static int launch_graph_chunk(galois_engine *e, int32_t G)
         cudaGraphExecDestroy(e->graph);
         e->graph = nullptr;
     }
+    if (int rc = exchange_join(e)) return rc;        // (no event from outside the capture)
     const int32_t s0 = e->steps_enqueued;
     const bool pend0 = e->pending_check;
     cudaGraph_t g = nullptr;
     bool ok = cudaStreamBeginCapture(e->stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
     int rc = GALOIS_OK;
     for (int32_t i = 0; ok && i < G && rc == GALOIS_OK; ++i) rc = enqueue_step(e);
+    if (ok && rc == GALOIS_OK) rc = exchange_join(e);   // the exchange stream rejoins inside the graph
     if (ok) ok = cudaStreamEndCapture(e->stream, &g) == cudaSuccess && rc == GALOIS_OK;
     if (ok) ok = cudaGraphInstantiate(&e->graph, g, 0) == cudaSuccess;
     if (g) cudaGraphDestroy(g);
@@ -1158,6 +1237,7 @@ static int launch_graph_chunk(galois_engine *e, int32_t G)
         e->poisoned = false;
         e->steps_enqueued = s0;
         e->pending_check = pend0;
+        e->x_pending = false;
         for (int32_t i = 0; i < G; ++i)
             if (int r2 = enqueue_step(e)) return r2;
         return GALOIS_OK;
@@ -1167,8 +1247,21 @@ static int launch_graph_chunk(galois_engine *e, int32_t G)
     return GALOIS_OK;
 }
 
+// The reported best record (u*, t*, b*): this rank's own on one rank, the global one (over
+// all ranks, k_gfinalize) with NCCL.
+struct Record {
+    int32_t u, t;
+    int64_t b;
+};
+static Record record_of(const galois_engine *e, const Ctrl &h)
+{
+    if (e->use_comm) return Record{h.g_u, h.g_t, h.g_b};
+    return Record{h.best_u, h.best_t, h.best_b};
+}
+
 static int read_ctrl(galois_engine *e, Ctrl *out)
 {
+    if (int rc = exchange_join(e)) return rc;
     ENG_CUDA(e, cudaMemcpyAsync(&e->h_ctrl[0], e->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, e->stream));
     ENG_CUDA(e, cudaStreamSynchronize(e->stream));
     *out = e->h_ctrl[0];
@@ -1233,10 +1326,19 @@ static int run_lanes(galois_engine *e);
 static bool small_run_ok(const galois_engine *e)
 {
     return e->small_gs && e->mode == GALOIS_MODE_ST && !e->use_comm && e->windows == 1 && e->lane.empty() &&
-           !e->debug && !e->profiling && e->steps_enqueued < e->T;
+           !e->debug && !e->profiling && e->graphs_mode != 1 && e->steps_enqueued < e->T;
 }
 
 static int run_steps(galois_engine *e);
+
+// CUDA graphs of G-step chunks: forced on / off by galois_engine_set_graphs, else used when
+// the capture + instantiation (~ms) is amortised over many chunks (short time-to-SAT runs
+// launch directly)
+static bool use_graphs(const galois_engine *e, int32_t left, int32_t G)
+{
+    if (e->graphs_mode != 0) return e->graphs_mode > 0;
+    return left >= 32 * G;
+}
 
 static int run_small(galois_engine *e)
 {
@@ -1269,7 +1371,7 @@ static int run_steps(galois_engine *e)
     // graphs only pay off when the capture + instantiation (~ms) is amortised over many
     // chunks; short runs (time-to-SAT) launch directly
     const bool graphs = !e->profiling && e->stream != nullptr && e->mode == GALOIS_MODE_ST && !e->graph_failed &&
-                        e->T - e->steps_enqueued >= 32 * G;
+                        use_graphs(e, e->T - e->steps_enqueued, G);
     int iter = 0;
     while (e->steps_enqueued < e->T) {
         const int32_t s0 = e->steps_enqueued;
@@ -1280,6 +1382,7 @@ static int run_steps(galois_engine *e)
             while (e->steps_enqueued < end)
                 if (int rc = enqueue_step(e)) return rc;
         }
+        if (int rc = exchange_join(e)) return rc;   // every rank polls the same global decision
         Ctrl *slot = &e->h_ctrl[iter & 1];
         ENG_CUDA(e, cudaMemcpyAsync(slot, e->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, e->stream));
         ENG_CUDA(e, cudaEventRecord(e->poll_ev[iter & 1], e->stream));
@@ -1314,9 +1417,9 @@ static int reseat(galois_engine *e, int32_t w)
     }
     ENG_CUDA(e, cudaStreamSynchronize(e->stream));
     Ctrl h{};
-    h.best_u = INT32_MAX;
-    h.best_t = -1;
-    h.best_b = -1;
+    h.best_u = h.g_u = INT32_MAX;
+    h.best_t = h.g_t = -1;
+    h.best_b = h.g_b = -1;
     e->h_ctrl[0] = h;
     ENG_CUDA(e, cudaMemcpyAsync(e->ctrl, &e->h_ctrl[0], sizeof(Ctrl), cudaMemcpyHostToDevice, e->stream));
     ENG_CUDA(e, cudaMemsetAsync(e->unsat, 0, sizeof(int32_t) * (size_t)e->b_pad, e->stream));
@@ -1350,21 +1453,20 @@ static int run_windows(galois_engine *e)
         Ctrl h;
         if (int r2 = read_ctrl(e, &h)) return r2;
         const galois_engine::Agg &a = e->agg;
-        const bool better = h.best_b >= 0 &&
-                            (h.best_u != a.u ? h.best_u < a.u : h.best_t != a.t ? h.best_t < a.t : h.best_b < a.b);
+        const Record rec = record_of(e, h);
+        const bool better = rec.b >= 0 && (rec.u != a.u ? rec.u < a.u : rec.t != a.t ? rec.t < a.t : rec.b < a.b);
         if (better) {
-            if (e->use_comm) {
+            if (e->use_comm) {           // every rank takes the same decision (global record)
                 std::string why;
-                if (!e->comm.broadcast_bytes(e->best_bits, (size_t)e->cnf->n, (int)(h.best_b / e->b_per), e->stream,
-                                             &why))
+                if (!e->comm.broadcast_bytes(e->best_bits, (size_t)e->cnf->n, (int)(rec.b / e->b_per), e->stream, &why))
                     return poison(e, GALOIS_E_NCCL, why);
             }
             ENG_CUDA(e, cudaMemcpyAsync(e->agg_bits.data(), e->best_bits, (size_t)e->cnf->n, cudaMemcpyDeviceToHost,
                                         e->stream));
 
-            e->agg.u = h.best_u;
-            e->agg.t = h.best_t;
-            e->agg.b = h.best_b;
+            e->agg.u = rec.u;
+            e->agg.t = rec.t;
+            e->agg.b = rec.b;
         }
         if (e->b_loc > 0) {
             ENG_CUDA(e, cudaMemcpyAsync(e->agg_counts.data() + (size_t)w * e->sub, e->unsat_last,
@@ -1386,7 +1488,7 @@ static int run_windows(galois_engine *e)
                 }
         }
         ENG_CUDA(e, cudaStreamSynchronize(e->stream));
-        e->agg.steps = std::max(e->agg.steps, h.t);
+        e->agg.steps = std::max(e->agg.steps, (e->use_comm && h.stopped) ? rec.t : h.t);
         if (h.stopped) e->agg.sat = true;
     }
     e->agg.ran = true;
@@ -1459,11 +1561,6 @@ static int lanes_refresh(galois_engine *e)
         const bool better = h.best_b >= 0 &&
                             (h.best_u != a.u ? h.best_u < a.u : h.best_t != a.t ? h.best_t < a.t : h.best_b < a.b);
         if (better) {
-            if (e->use_comm) {            // the winner's bits from its owner (collective on the lane's comm)
-                std::string why;
-                if (!l->comm.broadcast_bytes(l->best_bits, (size_t)n, (int)(h.best_b / e->b_per), l->stream, &why))
-                    return poison(e, GALOIS_E_NCCL, why);
-            }
             ENG_CUDA(e, cudaMemcpyAsync(e->agg_bits.data(), l->best_bits, (size_t)n, cudaMemcpyDeviceToHost, l->stream));
             a.u = h.best_u;
             a.t = h.best_t;
@@ -1511,7 +1608,7 @@ static int run_lanes(galois_engine *e)
             galois_engine *l = e->lane[i];
             if (l->steps_enqueued >= l->T) continue;
             const int32_t s0 = l->steps_enqueued;
-            const bool graphs = !l->profiling && !l->graph_failed && l->T - s0 >= 32 * G;
+            const bool graphs = !l->profiling && !l->graph_failed && use_graphs(l, l->T - s0, G);
             if (graphs && s0 % G == 0 && s0 + G < l->T) {
                 if (int rc = launch_graph_chunk(l, G)) return lane_fail(e, rc);
             } else {
@@ -1560,7 +1657,8 @@ extern "C" int galois_engine_info(galois_engine *e, int64_t *local_batch, int64_
     if (int rc = settle(e, &h)) return rc;
     if (local_batch) *local_batch = e->b_loc;
     if (first_global_b) *first_global_b = e->b0;
-    if (steps_done) *steps_done = h.t;
+    // with NCCL a rank may have run one update past the deciding check (exchange_join)
+    if (steps_done) *steps_done = (e->use_comm && h.stopped) ? record_of(e, h).t : h.t;
     if (stopped) *stopped = h.stopped;
     return GALOIS_OK;
 }
@@ -1589,9 +1687,12 @@ extern "C" int galois_best_assignment(galois_engine *e, uint8_t *values, int32_t
         h = e->h_ctrl[0];
         if (h.nonfinite) return poison(e, GALOIS_E_NONFINITE, "an iterate became NaN/Inf");
     } else {
+        // the owner's own record is the global winner (a rank owns the global record only
+        // through a strictly smaller local count, so its best_bits were extracted at that
+        // check): broadcast them from there
         if (int rc = settle(e, &h)) return rc;
-        if (h.best_b >= 0) {
-            const int root = (int)(h.best_b / e->b_per);
+        if (h.g_b >= 0) {
+            const int root = (int)(h.g_b / e->b_per);
             std::string why;
             if (!e->comm.broadcast_bytes(e->best_bits, (size_t)e->cnf->n, root, e->stream, &why))
                 return poison(e, GALOIS_E_NCCL, why);
@@ -1600,9 +1701,10 @@ extern "C" int galois_best_assignment(galois_engine *e, uint8_t *values, int32_t
             ENG_CUDA(e, cudaMemcpyAsync(values, e->best_bits, (size_t)e->cnf->n, cudaMemcpyDeviceToHost, e->stream));
         ENG_CUDA(e, cudaStreamSynchronize(e->stream));
     }
-    if (unsat) *unsat = h.best_u;
-    if (global_b) *global_b = h.best_b;
-    if (step) *step = h.best_t;
+    const Record rec = record_of(e, h);
+    if (unsat) *unsat = rec.u;
+    if (global_b) *global_b = rec.b;
+    if (step) *step = rec.t;
     return GALOIS_OK;
 }
 
@@ -1736,7 +1838,7 @@ extern "C" int galois_candidate_pool(galois_engine *e, int64_t global_b, int32_t
     if (N < 1 || !(rho > 0.0 && rho <= 1.0)) return fail(GALOIS_E_ARG, "need N >= 1 and 0 < rho <= 1");
     if (int rc = prepare(e)) return rc;
     const int32_t n = e->cnf->n;
-    const int32_t S = std::max<int32_t>(1, (int32_t)std::ceil(rho * (double)n - 1e-9));
+    const int32_t S = units_per_candidate(e->cnf, rho);
     if (S > launch::max_sorted()) return fail(GALOIS_E_ARG, "|S| exceeds 4096");
     if ((int64_t)N * n > (int64_t(1) << 31)) return fail(GALOIS_E_ARG, "N * n too large");
     if (S_out) *S_out = S;
@@ -1753,7 +1855,7 @@ extern "C" int galois_candidate_pool(galois_engine *e, int64_t global_b, int32_t
         return rc;
     }
     launch::pool(d_z, n, N, (float)(1.0 / e->tau), pool_seed, d_x, d_c, e->stream);
-    if (units) launch::topk(d_x, d_c, n, N, S, d_u, e->stream);
+    if (units) launch::topk(d_x, d_c, n, e->cnf->n_orig, N, S, d_u, e->stream);
     ENG_CUDA(e, cudaGetLastError());
     if (values) ENG_CUDA(e, cudaMemcpyAsync(values, d_x, (size_t)N * n, cudaMemcpyDeviceToHost, e->stream));
     if (confidence) ENG_CUDA(e, cudaMemcpyAsync(confidence, d_c, (size_t)N * n * 4, cudaMemcpyDeviceToHost, e->stream));
@@ -1768,8 +1870,8 @@ extern "C" int galois_cube_variables(galois_engine *e, int64_t global_b, int32_t
     ENGINE_ENTRY(e);
     if (!vars) return fail(GALOIS_E_ARG, "vars is NULL");
     if (int rc = prepare(e)) return rc;
-    const int32_t n = e->cnf->n;
-    if (d < 1 || d > n || d > launch::max_sorted()) return fail(GALOIS_E_ARG, "need 1 <= d <= min(n, 4096)");
+    const int32_t n = e->cnf->n, n_orig = e->cnf->n_orig;   // cubes over the original variables
+    if (d < 1 || d > n_orig || d > launch::max_sorted()) return fail(GALOIS_E_ARG, "need 1 <= d <= min(n, 4096)");
     ENG_CUDA(e, cudaStreamSynchronize(e->stream));
     float *d_z = nullptr;
     int32_t *d_v = nullptr;
@@ -1780,7 +1882,7 @@ extern "C" int galois_cube_variables(galois_engine *e, int64_t global_b, int32_t
         cudaFreeAsync(d_v, e->stream);
         return rc;
     }
-    launch::lowconf(d_z, n, d, d_v, e->stream);
+    launch::lowconf(d_z, n_orig, d, d_v, e->stream);
     ENG_CUDA(e, cudaGetLastError());
     ENG_CUDA(e, cudaMemcpyAsync(vars, d_v, (size_t)d * 4, cudaMemcpyDeviceToHost, e->stream));
     ENG_CUDA(e, cudaFreeAsync(d_z, e->stream));
@@ -1793,7 +1895,20 @@ extern "C" int galois_engine_get_iterate(galois_engine *e, float *z, float *m, f
 {
     ENGINE_ENTRY(e);
     if (int rc = prepare(e)) return rc;
-    WHOLE_SLICE_ONLY(e);
+    NO_WINDOWS(e);
+    if (!e->lane.empty()) {
+        const size_t n = (size_t)e->cnf->n;
+        int32_t tmax = 0;
+        const int rc = for_each_lane(e, [&](galois_engine *l, size_t off) {
+            int32_t tl = 0;
+            const int r = galois_engine_get_iterate(l, z ? z + off * n : nullptr, m ? m + off * n : nullptr,
+                                                    v ? v + off * n : nullptr, &tl);
+            tmax = std::max(tmax, tl);
+            return r;
+        });
+        if (t) *t = tmax;
+        return rc;
+    }
     if (z) if (int rc = copy_transposed_out(e, e->z, z)) return rc;
     if (m) if (int rc = copy_transposed_out(e, e->m, m)) return rc;
     if (v) if (int rc = copy_transposed_out(e, e->v, v)) return rc;
@@ -1811,7 +1926,18 @@ extern "C" int galois_engine_set_iterate(galois_engine *e, const float *z, const
     if (!z || !m || !v) return fail(GALOIS_E_ARG, "z, m and v are required");
     if (t < 0 || t > e->T) return fail(GALOIS_E_ARG, "t must be in [0, steps]");
     if (int rc = prepare(e)) return rc;
-    WHOLE_SLICE_ONLY(e);
+    NO_WINDOWS(e);
+    if (!e->lane.empty()) {
+        const size_t n = (size_t)e->cnf->n;
+        const int rc = for_each_lane(e, [&](galois_engine *l, size_t off) {
+            return galois_engine_set_iterate(l, z + off * n, m + off * n, v + off * n, t);
+        });
+        if (rc) return rc;
+        for (galois_engine *l : e->lane) l->steps_enqueued = t;
+        e->steps_enqueued = t;
+        e->agg.ran = false;
+        return GALOIS_OK;
+    }
     const int32_t n = e->cnf->n;
     const float *src[3] = {z, m, v};
     float *dst[3] = {e->z, e->m, e->v};
@@ -1840,6 +1966,53 @@ extern "C" int galois_engine_set_iterate(galois_engine *e, const float *z, const
     return GALOIS_OK;
 }
 
+// One member's state read in place on the device (column lb of the [n][b_pad] arrays), so
+// full-size engines (C4: 4 GB per state array) can be compared member by member.
+extern "C" int galois_engine_get_member(galois_engine *e, int64_t global_b, float *z, float *m, float *v,
+                                        uint8_t *x_next, uint8_t *r, int32_t *G, float *g1, int32_t *t,
+                                        int32_t *unsat, int32_t *check_t)
+{
+    ENGINE_ENTRY(e);
+    if (int rc = prepare(e)) return rc;
+    if (e->windows > 1) return fail(GALOIS_E_STATE, "not available on a sub-batched engine (run only)");
+    galois_engine *x = e;
+    for (galois_engine *l : e->lane)
+        if (global_b >= l->b0 && global_b < l->b0 + l->b_loc) x = l;
+    if (x == e && !e->lane.empty()) return fail(GALOIS_E_ARG, "member is not local to this rank");
+    int32_t lb = 0;
+    if (int rc = local_member(x, global_b, &lb)) return rc;
+    if ((G || g1) && !x->debug) return fail(GALOIS_E_STATE, "G / g1 need set_debug(1) before the first step");
+    if ((G || g1) && x->mode != GALOIS_MODE_ST) return fail(GALOIS_E_STATE, "G / g1 of one member: ST mode only");
+    const int32_t n = x->cnf->n;
+    ENG_CUDA(e, cudaStreamSynchronize(x->stream));
+    char *d = nullptr;
+    ENG_CUDA(e, cudaMallocAsync((void **)&d, (size_t)n * 22 + 256, x->stream));
+    float *dz = (float *)d, *dm = dz + n, *dv = dm + n, *dg1 = dv + n;
+    int32_t *dG = (int32_t *)(dg1 + n);
+    uint8_t *dx = (uint8_t *)(dG + n), *dr = dx + n;
+    const float *src[5] = {x->z, x->m, x->v, x->dbg_g1, (const float *)x->dbg_G};
+    float *dst[5] = {dz, dm, dv, dg1, (float *)dG};
+    void *host[5] = {z, m, v, g1, G};
+    for (int a = 0; a < 5; ++a)
+        if (host[a]) launch::gather_z(src[a], n, x->b_pad, lb, dst[a], x->stream);   // (a bit copy)
+    if (x_next || r) launch::member_bits(x->X, n, x->W, lb, x_next ? dx : nullptr, r ? dr : nullptr, x->stream);
+    for (int a = 0; a < 5; ++a)
+        if (host[a]) ENG_CUDA(e, cudaMemcpyAsync(host[a], dst[a], (size_t)n * 4, cudaMemcpyDeviceToHost, x->stream));
+    if (x_next) ENG_CUDA(e, cudaMemcpyAsync(x_next, dx, (size_t)n, cudaMemcpyDeviceToHost, x->stream));
+    if (r) ENG_CUDA(e, cudaMemcpyAsync(r, dr, (size_t)n, cudaMemcpyDeviceToHost, x->stream));
+    if (unsat) ENG_CUDA(e, cudaMemcpyAsync(unsat, x->unsat_last + lb, 4, cudaMemcpyDeviceToHost, x->stream));
+    ENG_CUDA(e, cudaFreeAsync(d, x->stream));
+    if (t || check_t) {
+        if (int rc = exchange_join(x)) return rc;
+        ENG_CUDA(e, cudaMemcpyAsync(&x->h_ctrl[0], x->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, x->stream));
+        ENG_CUDA(e, cudaStreamSynchronize(x->stream));
+        if (t) *t = x->h_ctrl[0].t;
+        if (check_t) *check_t = x->h_ctrl[0].last_check_t;
+    }
+    ENG_CUDA(e, cudaStreamSynchronize(x->stream));
+    return GALOIS_OK;
+}
+
 extern "C" int galois_engine_get_grad(galois_engine *e, int32_t *G, float *g1)
 {
     ENGINE_ENTRY(e);
@@ -1864,7 +2037,9 @@ extern "C" int galois_engine_get_loss(galois_engine *e, float *lambda)
     ENGINE_ENTRY(e);
     if (!lambda) return fail(GALOIS_E_ARG, "lambda is NULL");
     if (int rc = prepare(e)) return rc;
-    WHOLE_SLICE_ONLY(e);
+    NO_WINDOWS(e);
+    if (!e->lane.empty())
+        return for_each_lane(e, [&](galois_engine *l, size_t off) { return galois_engine_get_loss(l, lambda + off); });
     if (e->mode == GALOIS_MODE_ST) {
         // Lambda of the last completed step t lives in lam[t & 1] (see enqueue_step)
         Ctrl h;
@@ -1885,7 +2060,13 @@ extern "C" int galois_engine_get_bits(galois_engine *e, uint8_t *x_next, uint8_t
 {
     ENGINE_ENTRY(e);
     if (int rc = prepare(e)) return rc;
-    WHOLE_SLICE_ONLY(e);
+    NO_WINDOWS(e);
+    if (!e->lane.empty()) {
+        const size_t n = (size_t)e->cnf->n;
+        return for_each_lane(e, [&](galois_engine *l, size_t off) {
+            return galois_engine_get_bits(l, x_next ? x_next + off * n : nullptr, r ? r + off * n : nullptr);
+        });
+    }
     const int32_t n = e->cnf->n;
     std::vector<uint32_t> tmp((size_t)n * 2 * xr_pad(e->W));
     ENG_CUDA(e, cudaMemcpyAsync(tmp.data(), e->X, tmp.size() * 4, cudaMemcpyDeviceToHost, e->stream));
@@ -1940,6 +2121,9 @@ extern "C" void galois_engine_free(galois_engine *e)
     for (auto ev : e->join_ev) cudaEventDestroy(ev);
     if (e->fork_ev) cudaEventDestroy(e->fork_ev);
     e->comm.destroy(e->poisoned);
+    if (e->xstream) stream_release(e->xstream);
+    if (e->ev_chk) cudaEventDestroy(e->ev_chk);
+    if (e->ev_x) cudaEventDestroy(e->ev_x);
     engine_free_buffers(e);
     for (auto &r : e->recs) {
         cudaEventDestroy(r.a);

@@ -49,6 +49,12 @@ struct Ctrl {
     unsigned long long key_global;  // same, min over ranks (NCCL MIN)
     int32_t last_check_t; // step of the last check
     uint32_t done_ctas;   // CTAs of the running update kernel that finished (last one ticks t)
+    // NCCL (world > 1): the best record over ALL ranks, kept by k_gfinalize on the engine's
+    // exchange stream from the MIN all-reduced key of every check; best_* above is then this
+    // rank's own record (whose rounding bits best_bits hold)
+    int32_t g_u;
+    int32_t g_t;
+    int64_t g_b;
 };
 
 struct DevCnf {

@@ -46,6 +46,9 @@ inline PhiloxKeys philox_round_keys(uint64_t seed)
 #ifndef GALOIS_PHILOX_ROUNDS_EXPERIMENT
 #define GALOIS_PHILOX_ROUNDS_EXPERIMENT 10   // timing experiment only: results differ from the oracle
 #endif
+#if GALOIS_PHILOX_ROUNDS_EXPERIMENT != 10 && !defined(GALOIS_PARITY_BREAKING_EXPERIMENT)
+#error "GALOIS_PHILOX_ROUNDS_EXPERIMENT breaks oracle parity: also define GALOIS_PARITY_BREAKING_EXPERIMENT"
+#endif
 __device__ __forceinline__ uint4 philox4x32_10(uint4 c, const PhiloxKeys &pk)
 {
 #pragma unroll

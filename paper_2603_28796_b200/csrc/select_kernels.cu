@@ -150,16 +150,19 @@ __global__ void __launch_bounds__(256) k_pool(const float *__restrict__ zsel, in
 // One CTA per candidate: the S most confident variables as unit literals, descending
 // confidence, ties to the lower index.
 __global__ void __launch_bounds__(kSelThreads) k_topk(const uint8_t *__restrict__ x, const float *__restrict__ conf,
-                                                      int32_t n, int32_t S, int32_t *__restrict__ units)
+                                                      int32_t n, int32_t n_sel, int32_t S,
+                                                      int32_t *__restrict__ units)
 {
+    // rows of n variables; the units come from the first n_sel (the original variables of
+    // a normalised CNF: P:214 excludes the auxiliaries)
     __shared__ uint64_t s_keys[kMaxSorted];
     const int32_t k = blockIdx.x;
     const float *c = conf + (size_t)k * n;
     auto key_of = [&](int32_t v) -> uint64_t {
         return ((uint64_t)__float_as_uint(c[v]) << 32) | (uint64_t)(0xFFFFFFFFu - (uint32_t)v);
     };
-    const uint64_t thr = select_threshold(n, S, key_of);
-    collect_sorted_desc(n, S, thr, key_of, s_keys);
+    const uint64_t thr = select_threshold(n_sel, S, key_of);
+    collect_sorted_desc(n_sel, S, thr, key_of, s_keys);
     for (int32_t j = threadIdx.x; j < S; j += blockDim.x) {
         const int32_t v = (int32_t)(0xFFFFFFFFu - (uint32_t)(s_keys[j] & 0xFFFFFFFFull));
         units[(size_t)k * S + j] = x[(size_t)k * n + v] ? v + 1 : -(v + 1);
@@ -204,9 +207,10 @@ void pool(const float *zsel, int32_t n, int32_t N, float inv_tau, uint64_t pool_
     k_pool<<<(unsigned)(g < 1 ? 1 : g), 256, 0, st>>>(zsel, n, N, inv_tau, philox_round_keys(pool_seed), x, conf);
 }
 
-void topk(const uint8_t *x, const float *conf, int32_t n, int32_t N, int32_t S, int32_t *units, cudaStream_t st)
+void topk(const uint8_t *x, const float *conf, int32_t n, int32_t n_sel, int32_t N, int32_t S, int32_t *units,
+          cudaStream_t st)
 {
-    k_topk<<<N, kSelThreads, 0, st>>>(x, conf, n, S, units);
+    k_topk<<<N, kSelThreads, 0, st>>>(x, conf, n, n_sel, S, units);
 }
 
 void lowconf(const float *zsel, int32_t n, int32_t d, int32_t *vars, cudaStream_t st)

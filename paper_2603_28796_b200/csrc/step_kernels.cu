@@ -8,7 +8,7 @@
 //                     multiple of 4 (b_pad < 1024 padded to 32): U = AND of false-literal
 //                     words, exclusive products E = ~any | (S_i & ~atleast2) in CSC order
 //                     (negative occurrences complemented), per-member counts of U
-//   k_best / k_finalize / k_extract  a8-a9 best tracking and the winner's bits
+//   k_best / k_gfinalize / k_extract  a8-a9 best tracking (local, over ranks) and the winner's bits
 // (the sweep for b_pad >= 1024 is k_sweep in clause_kernels.cu, the update in
 // update_kernels.cu)
 //
@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(256) k_clauses_st(DevCnf c, int32_t W, int32_t
 }
 
 // ------------------------------------------------------------------- a8/a9: best
-// Single block: min over local members of (u << 32 | global b). world == 1 finalizes too.
+// Single block: min over local members of (u << 32 | global b), and this rank's best record.
 __global__ void __launch_bounds__(1024) k_best(const int32_t *__restrict__ unsat, int32_t *__restrict__ unsat_last,
                                                int32_t b_loc, int64_t b0, Ctrl *__restrict__ ctrl, int32_t finalize)
 {
@@ -202,10 +202,21 @@ __global__ void __launch_bounds__(1024) k_best(const int32_t *__restrict__ unsat
     block_best(unsat, unsat_last, b_loc, b0, ctrl, finalize != 0);
 }
 
-__global__ void k_finalize(Ctrl *__restrict__ ctrl, int64_t b0, int32_t b_loc)
+// NCCL exchange (a9), on the engine's exchange stream after the MIN all-reduce of check
+// t's key: the global record improves only on a strictly smaller count (ties keep the
+// earlier check, and within a check the key orders by global member), and a global count
+// of 0 stops every rank. Never returns early: a rank stopped by its own SAT must still
+// fold that check into the global record.
+__global__ void k_gfinalize(Ctrl *__restrict__ ctrl)
 {
-    if (ctrl->stopped) return;
-    finalize_best(ctrl, ctrl->key_global, b0, b_loc);
+    const unsigned long long key = ctrl->key_global;
+    const int64_t u = (int64_t)(key >> 32);         // 2^32 - 1 when no rank has members
+    if (u < (int64_t)ctrl->g_u) {
+        ctrl->g_u = (int32_t)u;
+        ctrl->g_t = ctrl->last_check_t;
+        ctrl->g_b = (int64_t)(key & 0xFFFFFFFFull);
+    }
+    if (ctrl->g_u == 0) ctrl->stopped = 1;
 }
 
 // Copy the rounding column of the new best member (only when it improved on this rank).
@@ -218,8 +229,26 @@ __global__ void k_extract(const uint32_t *__restrict__ R, int32_t n, int32_t W, 
         best_bits[v] = (uint8_t)((R[xr_at(v, (int32_t)(lb >> 5), W)] >> bitpos((int)(lb & 31))) & 1u);
 }
 
+// One member's sample and rounding bits (test hook galois_engine_get_member).
+__global__ void k_member_bits(const uint32_t *__restrict__ X, int32_t n, int32_t W, int32_t lb,
+                              uint8_t *__restrict__ x_out, uint8_t *__restrict__ r_out)
+{
+    const size_t w = (size_t)(lb >> 5);
+    const int bit = bitpos(lb & 31);
+    for (int32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+        const size_t at = xr_at(v, (int32_t)w, W);
+        if (x_out) x_out[v] = (uint8_t)((X[at] >> bit) & 1u);
+        if (r_out) r_out[v] = (uint8_t)((X[at + 4] >> bit) & 1u);   // R = X + 4 words
+    }
+}
+
 // ------------------------------------------------------------------ launch wrappers
 namespace launch {
+
+void member_bits(const uint32_t *X, int32_t n, int32_t W, int32_t lb, uint8_t *x_out, uint8_t *r_out, cudaStream_t st)
+{
+    k_member_bits<<<(n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096, 256, 0, st>>>(X, n, W, lb, x_out, r_out);
+}
 
 static unsigned grid_cap(uint64_t work, unsigned threads, unsigned cap)
 {
@@ -280,9 +309,9 @@ void best(const int32_t *unsat, int32_t *unsat_last, int32_t b_loc, int64_t b0, 
     k_best<<<1, 1024, 0, st>>>(unsat, unsat_last, b_loc, b0, ctrl, finalize ? 1 : 0);
 }
 
-void finalize(Ctrl *ctrl, int64_t b0, int32_t b_loc, cudaStream_t st)
+void gfinalize(Ctrl *ctrl, cudaStream_t st)
 {
-    k_finalize<<<1, 1, 0, st>>>(ctrl, b0, b_loc);
+    k_gfinalize<<<1, 1, 0, st>>>(ctrl);
 }
 
 void extract(const uint32_t *R, int32_t n, int32_t W, int64_t b0, const Ctrl *ctrl, uint8_t *best_bits,

@@ -631,6 +631,9 @@ __global__ void __launch_bounds__(256 + 32, kTmaCtasPerSm) k_update_tma(DevCnf c
         float g1o[4];
         // cube pins (C5: 16 of 100k variables): the pinned code path only where the
         // item's variable is pinned (uniform over the item), the plain one elsewhere
+#if defined(GALOIS_UPD_MEMONLY) && !defined(GALOIS_PARITY_BREAKING_EXPERIMENT)
+#error "GALOIS_UPD_MEMONLY breaks oracle parity: also define GALOIS_PARITY_BREAKING_EXPERIMENT"
+#endif
 #ifdef GALOIS_UPD_MEMONLY   // experiment: the data movement of this kernel without its arithmetic
         xn = (uint32_t)G[0] & 15u; rn = __float_as_uint(z.x) & 15u; (void)bq; (void)g1o;
         z.x += 1.0f; m.x += 1.0f; vv.x += 1.0f;

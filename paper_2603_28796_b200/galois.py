@@ -38,6 +38,7 @@ EXPORTED = (
     "galois_engine_get_grad", "galois_engine_get_loss", "galois_engine_get_bits",
     "galois_engine_kernel_times", "galois_select_member", "galois_candidate_pool", "galois_cube_variables",
     "galois_cnf_normalize", "galois_cnf_get_csr", "galois_engine_set_subbatch", "galois_engine_set_lanes", "galois_engine_bytes_per_member",
+    "galois_engine_set_graphs", "galois_engine_get_member", "galois_cnf_original_vars", "galois_candidate_pool_size",
 )
 
 
@@ -96,6 +97,10 @@ def lib() -> ctypes.CDLL:
             "galois_engine_set_subbatch": [P, I32],
             "galois_engine_set_lanes": [P, I32],
             "galois_engine_bytes_per_member": [P, I32, P],
+            "galois_engine_set_graphs": [P, I32],
+            "galois_engine_get_member": [P, I64, P, P, P, P, P, P, P, P, P, P],
+            "galois_cnf_original_vars": [P, P],
+            "galois_candidate_pool_size": [P, F, P],
         }
         for name, args in sig.items():
             fn = getattr(L, name)
@@ -191,6 +196,16 @@ class Cnf:
         out.n, out.m, out.num_aux = info["n"], info["m"], aux.value
         return out
 
+    def original_vars(self) -> int:
+        out = ctypes.c_int32()
+        _check(lib().galois_cnf_original_vars(self.handle, ctypes.byref(out)))
+        return out.value
+
+    def pool_size(self, rho: float) -> int:
+        out = ctypes.c_int32()
+        _check(lib().galois_candidate_pool_size(self.handle, float(rho), ctypes.byref(out)))
+        return out.value
+
     def bytes_per_member(self, mode: int = 0) -> int:
         out = ctypes.c_int64()
         _check(lib().galois_engine_bytes_per_member(self.handle, int(mode), ctypes.byref(out)))
@@ -234,7 +249,7 @@ class Engine:
                  eps: float = 1e-8, optimizer: int = 0, check_interval: int = 1,
                  cubes: Sequence[int] = (), debug: bool = False, stream=None,
                  rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None, sub_batch: int = 0,
-                 lanes: int = 1):
+                 lanes: int = 1, graphs: int = 0):
         self.cnf = cnf
         self.n = cnf.n
         self.handle = galois_engine_create(cnf.handle, batch, steps, lr, seed)
@@ -256,6 +271,8 @@ class Engine:
             _check(L.galois_engine_set_subbatch(self.handle, int(sub_batch)))
         if lanes != 1:
             _check(L.galois_engine_set_lanes(self.handle, int(lanes)))
+        if graphs:
+            _check(L.galois_engine_set_graphs(self.handle, int(graphs)))
         if world > 1 or nccl_id is not None:
             buf = ctypes.create_string_buffer(bytes(nccl_id), 128)
             _check(L.galois_engine_set_comm(self.handle, int(rank), int(world), buf))
@@ -306,6 +323,23 @@ class Engine:
         v = np.ascontiguousarray(v, np.float32)
         _check(lib().galois_engine_set_iterate(self.handle, _p(z), _p(m), _p(v), int(t)))
 
+    def get_member(self, global_b: int, grad: bool = False):
+        """One member's z, m, v (float32 [n]), sample bits x_next and rounding r (uint8 [n]),
+        t, its count at the last check that ran (unsat, check_t; no pending check is run),
+        and with grad=True (debug engines) G (int32) and g1 (float32)."""
+        n = self.n
+        z = np.zeros(n, np.float32); m = np.zeros_like(z); v = np.zeros_like(z)
+        x = np.zeros(n, np.uint8); r = np.zeros(n, np.uint8)
+        G = np.zeros(n, np.int32) if grad else None
+        g1 = np.zeros(n, np.float32) if grad else None
+        t, u, ct = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+        _check(lib().galois_engine_get_member(self.handle, int(global_b), _p(z), _p(m), _p(v), _p(x), _p(r),
+                                              _p(G), _p(g1), ctypes.byref(t), ctypes.byref(u), ctypes.byref(ct)))
+        out = dict(z=z, m=m, v=v, x_next=x, r=r, t=t.value, unsat=u.value, check_t=ct.value)
+        if grad:
+            out.update(G=G, g1=g1)
+        return out
+
     def get_grad(self):
         nb = self.info()["local_batch"]
         G = np.zeros((nb, self.n), np.int32); g1 = np.zeros((nb, self.n), np.float32)
@@ -337,7 +371,7 @@ class Engine:
         """Eq.10-11: N samples of member global_b, their confidences and top-|S| unit literals
         (arrays=False: the unit lists only; values / confidence stay on the device)."""
         n = self.n
-        S = max(1, int(np.ceil(rho * n - 1e-9)))
+        S = self.cnf.pool_size(rho)                   # |S| (Eq.11) from the library
         x = np.zeros((N, n), np.uint8) if arrays else None
         c = np.zeros((N, n), np.float32) if arrays else None
         u = np.zeros((N, S), np.int32)

@@ -218,3 +218,213 @@ def one_step(G, inst, batch, t, seed=0, *, mode=0, tau=1.0, lr=0.5, optimizer=0,
     eng.free()
     cnf.free()
     return res
+
+
+# ------------------------------------------------------------------------------------
+# Production kernels at any size: sampled members, identical iterates at every step.
+# ------------------------------------------------------------------------------------
+def update_tolerances(m_prev, v_prev, go, dg, zo, mo, vo, t_next, lr, optimizer):
+    """First-order bounds of the fp32 update from identical fp64 iterates, given the
+    gradient bound dg (|g1 - go| <= dg): m, v (Adam) and z."""
+    m_prev = np.asarray(m_prev, np.float64); v_prev = np.asarray(v_prev, np.float64)
+    if optimizer == 0:
+        b1, b2, eps = 0.9, 0.999, 1e-8
+        tol_m = 1e-6 * (b1 * np.abs(m_prev) + (1 - b1) * np.abs(go)) + (1 - b1) * dg + 1e-30
+        tol_v = 1e-6 * (b2 * v_prev + (1 - b2) * go * go) + (1 - b2) * 2 * np.abs(go) * dg + 1e-30
+        c1 = lr / (1 - b1 ** t_next); c2 = 1 / np.sqrt(1 - b2 ** t_next)
+        denom = np.sqrt(vo) * c2 + eps
+        dz = np.abs(2 * c1 * mo / denom)
+        tol_z = 2 * c1 * tol_m / denom + dz * 0.5 * tol_v / np.maximum(vo, 1e-300) + 1e-6 * dz \
+            + 1e-6 * np.maximum(1, np.abs(zo))
+        return tol_m, tol_v, tol_z
+    tol_z = 2 * lr * dg + 1e-6 * np.abs(2 * lr * go) + 1e-6 * np.maximum(1, np.abs(zo))
+    return None, None, tol_z
+
+
+def _oracle_members(f, cfg, states, pool):
+    """One oracle step for each sampled member (dict b -> engine member state)."""
+    def one(item):
+        b, s = item
+        st = O.State.from_reduced(s["z"][None], s["m"][None], s["v"][None], s["t"], b0=b)
+        out = O.step(f, cfg, st)
+        return b, out, st
+    return {b: (out, st) for b, out, st in pool.map(one, list(states.items()))}
+
+
+def stepwise_sampled(G, inst, eng, members, steps, seed=0, *, tau=1.0, lr=0.5, optimizer=0, cubes=(),
+                     max_ties=2):
+    """Drive `eng` (any launch configuration: lanes, chunk loop, non-debug kernels) with
+    enqueue(1) — the fused forward + check sweep the bench runs — and before every step give
+    the sampled members' fp32 iterates (read in place with get_member) to the oracle (exact
+    map, reading R24). Per step and member: the sample bits X the forward used, Lambda, the
+    rounding R, z/m/v within the one-step bounds, and the exact unsat count of the previous
+    rounding (checked inside the fused sweep). Returns a report dict."""
+    from concurrent.futures import ThreadPoolExecutor
+    f = O.Cnf(inst.n, inst.offsets, inst.lits)
+    cfg = oracle_cfg(seed, 0, tau, lr, optimizer, cubes)
+    b0 = eng.info()["first_global_b"]
+    rep = dict(steps=0, ties=0, compared=0, counts=0)
+    states = {b: eng.get_member(b) for b in members}
+    prev_u = {}
+    for b, s in states.items():
+        assert s["t"] == 0
+        st = O.State.from_reduced(s["z"][None], s["m"][None], s["v"][None], 0, b0=b)
+        r0, u0 = O.round_and_check(f, cfg, st)
+        # identical z: the rounding [z >= 0] is the same decision in both precisions
+        np.testing.assert_array_equal(s["r"], r0[0], err_msg=f"R_0 member {b}")
+        prev_u[b] = int(u0[0])
+    with ThreadPoolExecutor(max_workers=min(16, len(members))) as pool:
+        for t in range(steps):
+            ora = _oracle_members(f, cfg, states, pool)
+            eng.enqueue(1)
+            lam = eng.get_loss()
+            new = {b: eng.get_member(b) for b in members}
+            for b in members:
+                s, n_ = states[b], new[b]
+                out, st = ora[b]
+                assert n_["t"] == t + 1, (b, n_["t"], t)
+                # the count of R_t, checked by this step's fused sweep
+                assert n_["check_t"] == t
+                assert n_["unsat"] == prev_u[b], f"unsat(R_{t}) member {b}: {n_['unsat']} vs {prev_u[b]}"
+                rep["counts"] += 1
+                z = s["z"].astype(np.float64)
+                tie_x = compare_bits(f"X_{t + 1}[{b}]", s["x_next"][None], out["xhat"], np.abs(out["a"]),
+                                     ((1e-6 + 1e-6 * np.abs(z)) / tau)[None])
+                if tie_x.any():              # the member's signal used a different bit: skip it this step
+                    rep["ties"] += 1
+                    prev_u[b] = O.unsat_count(f, n_["r"])
+                    continue
+                assert lam[b - b0] == out["lam"][0], f"Lambda_{t + 1} member {b}"
+                go = out["grad1"][0]
+                dg = 1e-5 * np.abs(go) + 1e-30
+                zo, mo, vo = (a[0] for a in st.reduced())
+                tol_m, tol_v, tol_z = update_tolerances(s["m"], s["v"], go, dg, zo, mo, vo, t + 1, lr, optimizer)
+                tie_r = compare_bits(f"R_{t + 1}[{b}]", n_["r"][None], out["r"], np.abs(zo)[None], tol_z[None])
+                if tie_r.any():
+                    rep["ties"] += 1
+                    prev_u[b] = O.unsat_count(f, n_["r"])
+                    continue
+                if tol_m is not None:
+                    assert (np.abs(n_["m"] - mo) <= tol_m).all(), f"m member {b} step {t + 1}"
+                    assert (np.abs(n_["v"] - vo) <= tol_v).all(), f"v member {b} step {t + 1}"
+                bad = np.abs(n_["z"] - zo) > tol_z
+                assert not bad.any(), f"z member {b} step {t + 1}: {np.argwhere(bad)[:3].ravel()}"
+                prev_u[b] = int(out["unsat"][0])
+                rep["compared"] += 1
+            states = new
+            rep["steps"] = t + 1
+    assert rep["ties"] <= max_ties, rep
+    return rep
+
+
+def debug_signal_sampled(G, inst, eng, members, seed=0, *, cubes=()):
+    """A debug engine (set_debug(1): the signal G and g1 stored): one enqueued step from
+    init; G of the sampled members bit-exact, g1 within relative 1e-5 (north_star)."""
+    f = O.Cnf(inst.n, inst.offsets, inst.lits)
+    cfg = oracle_cfg(seed, cubes=cubes)
+    states = {b: eng.get_member(b) for b in members}
+    eng.enqueue(1)
+    ties = 0
+    for b in members:
+        s = states[b]
+        st = O.State.from_reduced(s["z"][None], s["m"][None], s["v"][None], 0, b0=b)
+        out = O.step(f, cfg, st)
+        tie = compare_bits(f"X_1[{b}]", s["x_next"][None], out["xhat"], np.abs(out["a"]),
+                           (1e-6 + 1e-6 * np.abs(s["z"].astype(np.float64)))[None])
+        if tie.any():
+            ties += 1
+            continue
+        g = eng.get_member(b, grad=True)
+        np.testing.assert_array_equal(g["G"], out["G"][0].astype(np.int32), err_msg=f"G member {b}")
+        go = out["grad1"][0]
+        bad = np.abs(g["g1"] - go) > 1e-5 * np.abs(go) + 1e-30
+        assert not bad.any(), f"g1 member {b}"
+    return ties
+
+
+# ------------------------------------------------------------------------------------
+# Execution variants (CUDA graphs, lanes, the single-launch run, sub-batch windows)
+# against the oracle directly: several steps from one identical iterate.
+# ------------------------------------------------------------------------------------
+def oracle_multistep(f, cfg, st, t_end, K=1, check_t0=False, zone=2e-5):
+    """Step the oracle state st (all members, fp64) to t_end like galois_engine_run
+    (checks every K steps and at t_end, stop at the first SAT check). Returns the best
+    record (u, t, b) over the checks, the bits of its member, the counts of the last check,
+    the stop step, and per member whether any rounding/sampling decision came within
+    `zone` * max(1, |z|) of its threshold (a near tie: fp32 may decide it the other way)."""
+    nb, n = st.nb, f.n
+    near = np.zeros(nb, bool)
+    best = (np.iinfo(np.int64).max, -1, -1)
+    best_bits = None
+    last = None
+    T = t_end
+
+    def check(t, r, u):
+        nonlocal best, best_bits, last
+        last = u.copy()
+        i = int(np.argmin(u))
+        if u[i] < best[0]:
+            best = (int(u[i]), t, st.b0 + i)
+            best_bits = r[i].copy()
+
+    if check_t0:
+        z = st.reduced()[0]
+        near |= (np.abs(z) <= zone * np.maximum(1, np.abs(z))).any(axis=1)
+        r, u = round_and_check_np(f, cfg, st)
+        check(st.t, r, u)
+    while st.t < T and best[0] != 0:
+        z_pre = st.reduced()[0]
+        out = O.step(f, cfg, st)
+        z = st.reduced()[0]
+        near |= (np.abs(out["a"]) <= zone * np.maximum(1, np.abs(z_pre)) / cfg.tau).any(axis=1)
+        near |= (np.abs(z) <= zone * np.maximum(1, np.abs(z))).any(axis=1)
+        if st.t % K == 0 or st.t == T:
+            check(st.t, out["r"], out["unsat"])
+    return dict(best=best, best_bits=best_bits, last=last, stop=st.t, near=near, state=st)
+
+
+def round_and_check_np(f, cfg, st):
+    return O.round_and_check(f, cfg, st)
+
+
+def compare_run_variant(G, inst, eng, cfg, oracle_st, T, K=1, check_t0=False, zone=2e-5, z_rel=1e-4,
+                        compare_state=True, max_near=None, counts_after_sat=True):
+    """eng: configured and holding the same iterate as oracle_st (set_iterate, or the init
+    of the same seed); runs galois_engine_run and compares with oracle_multistep: rc and stop
+    step, the best record (u*, t*, b*) and its bits, every member's last count, and
+    (compare_state) the final z within z_rel max(1, |z|) (north_star's trajectory bound).
+    counts_after_sat=False: after a SAT stop the variant documents other members' counts at
+    their own last check (lanes, windows), so counts are compared only without a SAT.
+    Members with a near tie (oracle_multistep) are excepted from the member-wise checks, and
+    the record may differ only if its member on either side is one of them."""
+    f = O.Cnf(inst.n, inst.offsets, inst.lits)
+    ref = oracle_multistep(f, cfg, oracle_st, T, K, check_t0, zone)
+    rc = eng.run()
+    near = ref["near"]
+    if max_near is not None:
+        assert near.sum() <= max_near, f"{near.sum()} near-tie members"
+    best = eng.best_assignment()
+    info = eng.info()
+    gbest = (best["unsat"], best["step"], best["global_b"])
+    b_lo = oracle_st.b0
+    assert O.unsat_count(f, best["values"]) == best["unsat"], "best bits do not reproduce the best count"
+    if gbest == ref["best"]:
+        assert (rc == G.SAT) == (ref["best"][0] == 0), (rc, ref["best"])
+        assert info["steps_done"] == ref["stop"], (info["steps_done"], ref["stop"])
+        if not near[gbest[2] - b_lo]:
+            np.testing.assert_array_equal(best["values"], ref["best_bits"])
+        same_stop = True
+    else:
+        assert near[gbest[2] - b_lo] or near[ref["best"][2] - b_lo], (gbest, ref["best"])
+        same_stop = info["steps_done"] == ref["stop"]
+    ok = ~near
+    if same_stop and (counts_after_sat or rc != G.SAT):
+        counts, _ = eng.unsat_counts()
+        np.testing.assert_array_equal(counts[ok], ref["last"][ok])
+        if compare_state:
+            z, m, v, _ = eng.get_iterate()
+            zo, mo, vo = ref["state"].reduced()
+            err = np.abs(z - zo)[ok]
+            if err.size:
+                assert (err <= z_rel * np.maximum(1, np.abs(zo[ok]))).all(), f"z drift {err.max()}"
+    return dict(near=int(near.sum()), best=gbest, oracle_best=ref["best"], rc=rc, stop=ref["stop"])

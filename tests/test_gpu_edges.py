@@ -138,3 +138,28 @@ def test_graph_replay_equals_plain_launches(G):
     assert a[0] == b[0] == G.BUDGET and a[1:4] == b[1:4] and a[6] == b[6] == 300
     np.testing.assert_array_equal(a[4], b[4])
     np.testing.assert_array_equal(a[5], b[5])
+
+
+@pytest.mark.parametrize("batch,field", [(64, "z"), (2048, "z"), (2048, "m")])
+def test_nonfinite_iterate_poisons(G, batch, field):
+    """SPEC: a NaN/Inf iterate is a hard error. An injected NaN logit (or an
+    infinite first moment, which drives z to -inf) makes the update raise the device's non-finite flag; the step
+    returns E_NONFINITE, and the handle is poisoned (every later call E_STATE)."""
+    import numpy as np
+    inst = I.random_ksat(100, 420, 3, 1)
+    cnf = G.Cnf.from_instance(inst)
+    eng = G.Engine(cnf, batch, 10, 0.5, 0)
+    z, m, v, _ = eng.get_iterate()
+    if field == "z":
+        z[batch // 2, 17] = np.nan
+    else:
+        m[batch // 2, 17] = np.inf
+    eng.set_iterate(z, m, v, 0)
+    with pytest.raises(G.GaloisError) as e:
+        eng.step()
+    assert e.value.code == G.E_NONFINITE
+    with pytest.raises(G.GaloisError) as e:
+        eng.info()
+    assert e.value.code == G.E_STATE
+    eng.free()
+    cnf.free()
