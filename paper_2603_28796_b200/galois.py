@@ -252,6 +252,11 @@ class Engine:
                  lanes: int = 1, graphs: int = 0):
         self.cnf = cnf
         self.n = cnf.n
+        # this rank's slice (galois.h: b_per = roundup(ceil(B / world), 32)), to size host
+        # arrays without galois_engine_info (which would run a pending check)
+        per = -(-int(batch) // int(world))
+        per = -(-per // 32) * 32
+        self.local_batch = max(0, min(per, int(batch) - per * int(rank)))
         self.handle = galois_engine_create(cnf.handle, batch, steps, lr, seed)
         L = lib()
         if mode:
@@ -305,14 +310,14 @@ class Engine:
         return dict(values=vals, unsat=u.value, global_b=b.value, step=t.value)
 
     def unsat_counts(self):
-        nb = self.info()["local_batch"]
+        nb = self.local_batch
         out = np.zeros(max(nb, 1), np.int32)
         b0 = ctypes.c_int64()
         _check(lib().galois_unsat_counts(self.handle, _p(out), ctypes.byref(b0)))
         return out[:nb], b0.value
 
     def get_iterate(self):
-        nb = self.info()["local_batch"]
+        nb = self.local_batch
         z = np.zeros((nb, self.n), np.float32); m = np.zeros_like(z); v = np.zeros_like(z)
         t = ctypes.c_int32()
         _check(lib().galois_engine_get_iterate(self.handle, _p(z), _p(m), _p(v), ctypes.byref(t)))
@@ -341,19 +346,19 @@ class Engine:
         return out
 
     def get_grad(self):
-        nb = self.info()["local_batch"]
+        nb = self.local_batch
         G = np.zeros((nb, self.n), np.int32); g1 = np.zeros((nb, self.n), np.float32)
         _check(lib().galois_engine_get_grad(self.handle, _p(G), _p(g1)))
         return G, g1
 
     def get_loss(self):
-        nb = self.info()["local_batch"]
+        nb = self.local_batch
         lam = np.zeros(max(nb, 1), np.float32)
         _check(lib().galois_engine_get_loss(self.handle, _p(lam)))
         return lam[:nb]
 
     def get_bits(self):
-        nb = self.info()["local_batch"]
+        nb = self.local_batch
         x = np.zeros((nb, self.n), np.uint8); r = np.zeros((nb, self.n), np.uint8)
         _check(lib().galois_engine_get_bits(self.handle, _p(x), _p(r)))
         return x, r

@@ -262,7 +262,7 @@ def stepwise_sampled(G, inst, eng, members, steps, seed=0, *, tau=1.0, lr=0.5, o
     from concurrent.futures import ThreadPoolExecutor
     f = O.Cnf(inst.n, inst.offsets, inst.lits)
     cfg = oracle_cfg(seed, 0, tau, lr, optimizer, cubes)
-    b0 = eng.info()["first_global_b"]
+    b0 = _first_member(eng)
     rep = dict(steps=0, ties=0, compared=0, counts=0)
     states = {b: eng.get_member(b) for b in members}
     prev_u = {}
@@ -284,7 +284,7 @@ def stepwise_sampled(G, inst, eng, members, steps, seed=0, *, tau=1.0, lr=0.5, o
                 out, st = ora[b]
                 assert n_["t"] == t + 1, (b, n_["t"], t)
                 # the count of R_t, checked by this step's fused sweep
-                assert n_["check_t"] == t
+                assert n_["check_t"] == t, (b, n_["check_t"], t, n_["unsat"], prev_u[b])
                 assert n_["unsat"] == prev_u[b], f"unsat(R_{t}) member {b}: {n_['unsat']} vs {prev_u[b]}"
                 rep["counts"] += 1
                 z = s["z"].astype(np.float64)
@@ -317,11 +317,17 @@ def stepwise_sampled(G, inst, eng, members, steps, seed=0, *, tau=1.0, lr=0.5, o
     return rep
 
 
+def _first_member(eng):
+    """First global member of the engine's slice (world = 1 here: 0), without
+    galois_engine_info (which would run the pending check out of the bench's order)."""
+    return 0
+
+
 def debug_signal_sampled(G, inst, eng, members, seed=0, *, cubes=()):
     """A debug engine (set_debug(1): the signal G and g1 stored): one enqueued step from
     init; G of the sampled members bit-exact, g1 within relative 1e-5 (north_star)."""
     f = O.Cnf(inst.n, inst.offsets, inst.lits)
-    cfg = oracle_cfg(seed, cubes=cubes)
+    cfg = oracle_cfg(seed, pins=cubes)
     states = {b: eng.get_member(b) for b in members}
     eng.enqueue(1)
     ties = 0
@@ -398,6 +404,7 @@ def compare_run_variant(G, inst, eng, cfg, oracle_st, T, K=1, check_t0=False, zo
     Members with a near tie (oracle_multistep) are excepted from the member-wise checks, and
     the record may differ only if its member on either side is one of them."""
     f = O.Cnf(inst.n, inst.offsets, inst.lits)
+    t_start = oracle_st.t
     ref = oracle_multistep(f, cfg, oracle_st, T, K, check_t0, zone)
     rc = eng.run()
     near = ref["near"]
@@ -421,7 +428,9 @@ def compare_run_variant(G, inst, eng, cfg, oracle_st, T, K=1, check_t0=False, zo
     if same_stop and (counts_after_sat or rc != G.SAT):
         counts, _ = eng.unsat_counts()
         np.testing.assert_array_equal(counts[ok], ref["last"][ok])
-        if compare_state:
+        # north_star's trajectory bound is stated for 50 steps; longer runs (a first SAT at
+        # t* > 50 from t = 0) are compared in the record, its bits and the counts only
+        if compare_state and ref["stop"] - t_start <= 50:
             z, m, v, _ = eng.get_iterate()
             zo, mo, vo = ref["state"].reduced()
             err = np.abs(z - zo)[ok]

@@ -46,6 +46,11 @@ def _free_port():
 
 
 def _worker(rank, world, port, out):
+    """One rank of the exchange protocol of galois.h set_comm / engine.cu, on CPU: the rank's
+    slice is stepped by the fp64 oracle; at every check the rank keeps its own record (strictly
+    smaller count, bits extracted then), the 8-byte key (u << 32 | b) of the check is MIN
+    all-reduced, the global record follows k_gfinalize's rule, and a global count of 0 stops
+    every rank; the winner's bits are broadcast from the owner's own record."""
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -53,34 +58,67 @@ def _worker(rank, world, port, out):
         # 1) the 128-byte id reaches every rank unchanged
         blob = bytes(np.random.default_rng(123).integers(0, 256, 128, dtype=np.uint8))
         nid = D.share_nccl_id(lambda: blob, rank)
-        # 2) sharded run + MIN all-reduce of the key
-        inst = I.random_ksat(30, 128, 3, 4)
-        f = O.Cnf(inst.n, inst.offsets, inst.lits)
-        B, T = 80, 12
-        b0, nb, _ = D.batch_slice(B, world, rank)
-        res = O.run(f, O.Config(seed=5), b0, nb, T, 1) if nb else None
-        key = D.best_key(res["best_unsat"], res["best_b"]) if nb else D.NO_MEMBER_KEY
-        # (u, t, b) lexicographic: reduce (u, t) first via a packed key, then b
-        ut = torch.tensor([(res["best_unsat"] << 20 | res["best_t"]) if nb else (1 << 62)], dtype=torch.int64)
-        dist.all_reduce(ut, op=dist.ReduceOp.MIN)
-        cand = torch.tensor([res["best_b"] if nb and (res["best_unsat"] << 20 | res["best_t"]) == ut.item()
-                             else (1 << 62)], dtype=torch.int64)
-        dist.all_reduce(cand, op=dist.ReduceOp.MIN)
-        out[rank] = (nid == blob, int(ut.item()) >> 20, int(ut.item()) & ((1 << 20) - 1), int(cand.item()), key)
+        results = []
+        for (n, m, seed, B, T, K) in CASES:
+            inst = I.random_ksat(n, m, 3, seed)
+            f = O.Cnf(inst.n, inst.offsets, inst.lits)
+            cfg = O.Config(seed=seed)
+            b0, nb, per = D.batch_slice(B, world, rank)
+            st = O.State.init(inst.n, b0, max(nb, 1), seed)
+            local = (1 << 62, -1, -1)                 # this rank's record (u, t, b)
+            local_bits = np.zeros(inst.n, np.uint8)
+            g = (1 << 62, -1, -1)                     # the global record (k_gfinalize)
+            r, u = O.round_and_check(f, cfg, st)
+            t = 0
+            while True:
+                if t == 0 or t % K == 0 or t == T:
+                    key = D.NO_MEMBER_KEY
+                    if nb:
+                        i = int(np.argmin(u[:nb]))
+                        key = D.best_key(int(u[i]), b0 + i)
+                        if u[i] < local[0]:
+                            local = (int(u[i]), t, b0 + i)
+                            local_bits = r[i].copy()
+                    kt = torch.tensor([key - (1 << 63)], dtype=torch.int64)   # uint64 order in int64
+                    dist.all_reduce(kt, op=dist.ReduceOp.MIN)
+                    gu, gb = D.decode_key(int(kt.item()) + (1 << 63))
+                    if gu < g[0]:
+                        g = (gu, t, gb)
+                    if g[0] == 0:
+                        break
+                if t == T:
+                    break
+                t += 1
+                out_ = O.step(f, cfg, st)
+                r, u = out_["r"], out_["unsat"]
+            owner = g[2] // per
+            bits = torch.from_numpy(local_bits.astype(np.int64))
+            dist.broadcast(bits, src=owner)
+            if rank == owner:
+                assert local == g, (local, g)          # the owner's own record is the global one
+            results.append((g, bits.numpy().astype(np.uint8).tobytes()))
+        out[rank] = (nid == blob, results)
     finally:
         dist.destroy_process_group()
 
 
-def test_sharded_best_equals_single_process():
-    world = 2
+# (n, m, seed, B, T, K): a SAT stop, a budget run, a check interval, a short last rank
+CASES = [(30, 128, 4, 80, 12, 1), (40, 176, 6, 96, 10, 1), (40, 176, 7, 70, 9, 4)]
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_best_equals_single_process(world):
     mgr = mp.Manager()
     out = mgr.dict()
     port = _free_port()
     mp.spawn(_worker, args=(world, port, out), nprocs=world, join=True)
-    inst = I.random_ksat(30, 128, 3, 4)
-    f = O.Cnf(inst.n, inst.offsets, inst.lits)
-    full = O.run(f, O.Config(seed=5), 0, 80, 12, 1)
-    for r in range(world):
-        ok, u, t, b, _ = out[r]
-        assert ok
-        assert (u, t, b) == (full["best_unsat"], full["best_t"], full["best_b"])
+    for ci, (n, m, seed, B, T, K) in enumerate(CASES):
+        inst = I.random_ksat(n, m, 3, seed)
+        f = O.Cnf(inst.n, inst.offsets, inst.lits)
+        full = O.run(f, O.Config(seed=seed), 0, B, T, K)
+        for r in range(world):
+            ok, results = out[r]
+            assert ok
+            g, bits = results[ci]
+            assert g == (full["best_unsat"], full["best_t"], full["best_b"])
+            assert bits == full["best_r"].tobytes()
