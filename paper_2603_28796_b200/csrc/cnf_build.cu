@@ -245,7 +245,8 @@ __global__ void k_slot_info(const uint32_t *__restrict__ codes, const int32_t *_
 __global__ void k_sweep_widths(int64_t m, const int32_t *__restrict__ clause_off, const int32_t *__restrict__ perm,
                                int32_t *__restrict__ w)
 {
-    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c <= m; c += (int64_t)gridDim.x * blockDim.x) {
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c <= m + kSweepOffPad;
+         c += (int64_t)gridDim.x * blockDim.x) {
         int32_t x = 0;
         if (c < m) {
             const int32_t cl = perm[c];
@@ -287,8 +288,8 @@ cudaError_t launch_sweep_order(int64_t m, const int32_t *d_clause_off, const int
                                const int2 *d_slot_info, int32_t *d_sweep_off, int2 *d_sweep_slot, int32_t *d_scratch,
                                cudaStream_t st)
 {
-    k_sweep_widths<<<grid_for(m + 1), kThreads, 0, st>>>(m, d_clause_off, d_clause_perm, d_sweep_off);
-    exclusive_scan(d_sweep_off, d_sweep_off, m + 1, d_scratch, st);
+    k_sweep_widths<<<grid_for(m + 1 + kSweepOffPad), kThreads, 0, st>>>(m, d_clause_off, d_clause_perm, d_sweep_off);
+    exclusive_scan(d_sweep_off, d_sweep_off, m + 1 + kSweepOffPad, d_scratch, st);
     if (m > 0)
         k_sweep_slots<<<grid_for(m), kThreads, 0, st>>>(m, d_clause_off, d_clause_perm, d_slot_info, d_sweep_off,
                                                        d_sweep_slot);

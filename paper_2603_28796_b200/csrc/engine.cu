@@ -350,8 +350,10 @@ static int cnf_build_device(int dev, int32_t num_vars, int64_t num_clauses, int6
         return bail(GALOIS_E_VAR_RANGE, buf);
     }
     c->max_width = h_err[4];
-    LOAD_TRY(dmalloc(&c->sweep_off, (size_t)m + 1, st));
-    LOAD_TRY(dmalloc(&c->sweep_slot, (size_t)std::max<int64_t>(L, 1), st));
+    // padded for the staged sweep's tile copies (k_sweep_tma): offsets past m hold L, and a
+    // 16-B aligned slot copy may read one int2 past L
+    LOAD_TRY(dmalloc(&c->sweep_off, (size_t)m + 1 + kSweepOffPad, st));
+    LOAD_TRY(dmalloc(&c->sweep_slot, (size_t)L + 2, st));
     LOAD_TRY(launch_sweep_order(m, c->clause_off, c->clause_perm, c->slot_info, c->sweep_off, c->sweep_slot,
                                 (int32_t *)d_scratch, st));
 

@@ -24,6 +24,7 @@
 namespace galois {
 
 constexpr int kHubDegree = 256;      // variables with more occurrences use the hub path
+constexpr int kSweepOffPad = 128;    // sweep_off entries past m (all = L): whole-tile copies
 
 // word w of row v of the interleaved X/R array (apply to X for X words, to R = X + 4 for R)
 __host__ __device__ __forceinline__ int32_t xr_pad(int32_t W) { return (W + 3) & ~3; }
@@ -63,8 +64,8 @@ struct DevCnf {
     int32_t L;
     const int32_t *clause_off;   // [m+1]
     const int32_t *clause_perm;  // [m] clauses in stable width order (warp-uniform widths)
-    const int32_t *sweep_off;    // [m+1] CSR offsets in clause_perm order
-    const int2 *sweep_slot;      // [L] slot_info in clause_perm order (sweep c = clause_perm[c])
+    const int32_t *sweep_off;    // [m+1+kSweepOffPad] CSR offsets in clause_perm order (tail = L)
+    const int2 *sweep_slot;      // [L+2] slot_info in clause_perm order (sweep c = clause_perm[c])
     const int2 *slot_info;       // [L] {code, csc position}
     const int32_t *code_off;     // [2n+1]
     const int32_t *occ_slot;     // [L]

@@ -67,7 +67,9 @@ __device__ __forceinline__ uint4 philox4x32_10(uint4 c, const PhiloxKeys &pk)
 // binary32 (24 significant bits; Sterbenz), so the pair costs one LOP3 and two FADDs.
 __device__ __forceinline__ float2 unif_pair(uint32_t w)
 {
-    const float f = __uint_as_float(0x3F800000u | (w & 0x7FFFFFu));
+    uint32_t b;                             // (w & 0x7FFFFF) | 0x3F800000 in ONE LOP3
+    asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(b) : "r"(w), "r"(0x7FFFFFu), "r"(0x3F800000u));
+    const float f = __uint_as_float(b);
     const float u = f - 0.999999940395355224609375f;
     return make_float2(u, 1.0f - u);
 }
@@ -81,10 +83,10 @@ __device__ __forceinline__ float logistic_from_word(uint32_t w)
     return (__log2f(uu.x) - __log2f(uu.y)) * 0.69314718055994531f;
 }
 
-// Same uniform in fp64 (init path only).
-__device__ __forceinline__ double uniform_f64(uint32_t w)
+// Init uniform (2k+1) 2^-24, k = the low 23 bits of the word: exact in binary32.
+__device__ __forceinline__ float uniform_f32(uint32_t w)
 {
-    return (double)(((w & 0x7FFFFFu) << 1) | 1u) * (1.0 / 16777216.0);  // (2k+1) 2^-24
+    return (float)(((w & 0x7FFFFFu) << 1) | 1u) * (1.0f / 16777216.0f);
 }
 
 }  // namespace galois

@@ -1,7 +1,7 @@
 // step_kernels.cu — rows a3, a5/a8 (small batches) and a8-a9 of SURVEY §8 (straight-
 // through mode, the paper's).
 //
-//   k_init        a3  theta ~ N(0,1) -> z0 = theta_1 - theta_0 (fp64 Box-Muller), first
+//   k_init        a3  theta ~ N(0,1) -> z0 = theta_1 - theta_0 (Box-Muller, fp32), first
 //                     sample X_1 and rounding R_0
 //   k_resample        R_t and X_{t+1} from an injected iterate (set_iterate test hook)
 //   k_clauses_st  a5/a8 the scalar clause sweep for batches whose word count W is not a
@@ -43,12 +43,13 @@ __global__ void __launch_bounds__(256) k_init(StepParams p, float4 *__restrict__
             const uint4 w = philox4x32_10(make_uint4((uint32_t)v, (uint32_t)((bq >> 1) + h), 0u, 0u), key);
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
-                const double u0 = uniform_f64(j ? w.z : w.x);
-                const double u1 = uniform_f64(j ? w.w : w.y);
-                const double rho = sqrt(-2.0 * log(u0));
-                double s, c;
-                sincospi(2.0 * u1, &s, &c);
-                zz[2 * h + j] = (float)(rho * s - rho * c);  // theta_1 - theta_0
+                // Box-Muller theta_0 = rho cos(2 pi u1), theta_1 = rho sin(2 pi u1), rho =
+                // sqrt(-2 ln u0); z0 = theta_1 - theta_0 = sqrt(-4 ln u0) sin(pi (2 u1 - 1/4))
+                // (sin a - cos a = sqrt2 sin(a - pi/4)): one sinpi, no cancellation, so fp32
+                // keeps a few ulps of relative error (u0, 2 u1 - 1/4 are exact in binary32)
+                const float u0 = uniform_f32(j ? w.z : w.x);
+                const float u1 = uniform_f32(j ? w.w : w.y);
+                zz[2 * h + j] = sqrtf(-4.0f * logf(u0)) * sinpif(fmaf(2.0f, u1, -0.25f));
             }
         }
         const uint4 wn = philox4x32_10(make_uint4((uint32_t)v, (uint32_t)(bq >> 2), 1u, 1u), key);

@@ -510,7 +510,7 @@ __global__ void __launch_bounds__(256 + 32, kTmaCtasPerSm) k_update_tma(DevCnf c
     if (tid == 0) {
         for (int i = 0; i < kStages; ++i) {
             mbar_init(&full[i], 1);
-            mbar_init(&empty[i], kConsumerWarps);
+            mbar_init(&empty[i], 32 * kConsumerWarps);   // every consumer thread releases
         }
         fence_mbar_init();
     }
@@ -518,7 +518,9 @@ __global__ void __launch_bounds__(256 + 32, kTmaCtasPerSm) k_update_tma(DevCnf c
 
     if (warp == kConsumerWarps) {          // ------------------------------ producer warp
         if (lane == 0) {
-            uint32_t slot = 0;
+            int st = 0;                    // ring stage, its phase parity, and whether the ring wrapped
+            uint32_t ph = 0;
+            bool wrapped = false;
             for (uint32_t item = blockIdx.x; item < rm.items; item += gridDim.x) {
                 const uint32_t v = div_cpr(rm, item), ch = item - v * rm.cpr;
                 const int32_t k0 = c.code_off[2 * v], k1 = c.code_off[2 * v + 1], k2 = c.code_off[2 * v + 2];
@@ -528,10 +530,9 @@ __global__ void __launch_bounds__(256 + 32, kTmaCtasPerSm) k_update_tma(DevCnf c
                 const int32_t pieces = hub ? 1 : max(1, (k2 - k0 + kStageRows - 1) / kStageRows);
                 const size_t off = (size_t)v * QW + (size_t)ch * 256u;
                 const uint32_t *Ech = E + (size_t)ch * c.L * 32u;
-                for (int32_t pc = 0; pc < pieces; ++pc, ++slot) {
-                    const int st = (int)(slot % kStages);
-                    if (slot >= (uint32_t)kStages) {
-                        mbar_wait_s(empty_s + 8u * st, ((slot / kStages) - 1u) & 1u);
+                for (int32_t pc = 0; pc < pieces; ++pc) {
+                    if (wrapped) {
+                        mbar_wait_s(empty_s + 8u * st, ph ^ 1u);
                         fence_proxy_async_smem();
                     }
                     const int32_t r0 = hub ? k0 : k0 + pc * kStageRows;
@@ -548,6 +549,11 @@ __global__ void __launch_bounds__(256 + 32, kTmaCtasPerSm) k_update_tma(DevCnf c
                         bulk_g2s_s(sbs + kStageE + 8192, v4 + off, 4096u, fb);
                     }
                     if (ebytes) bulk_g2s_s(sbs, Ech + (size_t)r0 * 32u, ebytes, fb);
+                    if (++st == kStages) {
+                        st = 0;
+                        ph ^= 1u;
+                        wrapped = true;
+                    }
                 }
             }
         }
@@ -561,7 +567,8 @@ __global__ void __launch_bounds__(256 + 32, kTmaCtasPerSm) k_update_tma(DevCnf c
         if (p.clear_b) p.clear_b[i] = 0;
     }
     const int sh = tid & 7;
-    uint32_t slot = 0;
+    int st = 0;                            // ring stage and its phase parity (no division)
+    uint32_t ph = 0;
     for (uint32_t item = blockIdx.x; item < rm.items; item += gridDim.x) {
         float4 z, m, vv;
         int32_t v = 0, flags = 0, negs = 0;
@@ -574,9 +581,7 @@ __global__ void __launch_bounds__(256 + 32, kTmaCtasPerSm) k_update_tma(DevCnf c
 #pragma unroll
         for (int k = 0; k < kSlicedPlanes; ++k) PS[k] = 0;
         do {
-            const int st = (int)(slot % kStages);
-            mbar_wait_s(full_s + 8u * st, (slot / kStages) & 1u);
-            ++slot;
+            mbar_wait_s(full_s + 8u * st, ph);
             const StageHdr h = hdr[st];
             flags = hflags[st];
             v = h.v;
@@ -611,8 +616,11 @@ __global__ void __launch_bounds__(256 + 32, kTmaCtasPerSm) k_update_tma(DevCnf c
                     if (nneg > 0) { G[0] -= nneg; G[1] -= nneg; G[2] -= nneg; G[3] -= nneg; }
                 }
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive_s(empty_s + 8u * st);   // this warp is done reading the stage
+            mbar_arrive_s(empty_s + 8u * st);   // this thread is done reading the stage
+            if (++st == kStages) {
+                st = 0;
+                ph ^= 1u;
+            }
         } while (!(flags & 2));
         const uint32_t q = (item - (uint32_t)v * rm.cpr) * 256u + (uint32_t)tid;
         if (kSliced && (flags & 4)) {
@@ -685,7 +693,7 @@ __global__ void __launch_bounds__(256 + 32, kTmaCtasPerSm) k_hub_partial_tma(Dev
     if (tid == 0) {
         for (int i = 0; i < kStages; ++i) {
             mbar_init(&full[i], 1);
-            mbar_init(&empty[i], kConsumerWarps);
+            mbar_init(&empty[i], 32 * kConsumerWarps);   // every consumer thread releases
         }
         fence_mbar_init();
     }
@@ -731,8 +739,7 @@ __global__ void __launch_bounds__(256 + 32, kTmaCtasPerSm) k_hub_partial_tma(Dev
             for (int k = 0; k < kHP; ++k) Q[k] = 0;
             add_rows<kHP, (1 << kHP) - 1>(Q, reinterpret_cast<const uint32_t *>(smem + st * kHubStageBytes) + lane, h.z,
                                          warp);
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[st]);            // this warp is done with the stage
+            mbar_arrive(&empty[st]);                           // this thread is done with the stage
             const int pb = (int)(slot & 1u);
 #pragma unroll
             for (int k = 0; k < kHP; ++k) sP[pb][warp][k][lane] = Q[k];
@@ -764,8 +771,7 @@ __global__ void __launch_bounds__(256 + 32, kTmaCtasPerSm) k_hub_partial_tma(Dev
                                  tid & 7, sh, G);
             const int32_t nneg = h.z - h.y;
             G[0] -= nneg; G[1] -= nneg; G[2] -= nneg; G[3] -= nneg;
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[st]);
+            mbar_arrive(&empty[st]);
             const uint32_t ch = item - (uint32_t)h.w * rm.cpr;
             partial[(size_t)h.w * rm.QW + ch * 256u + tid] = make_short4((short)G[0], (short)G[1], (short)G[2], (short)G[3]);
         }

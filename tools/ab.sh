@@ -10,7 +10,7 @@ for W in "$@"; do
         lib=${spec%%@*}
         envs=""
         [[ "$spec" == *@* ]] && envs=${spec#*@}
-        out=$(env ${envs//,/ } GALOIS_LIB=$lib timeout 600 python bench.py --workload $W --no-cpu-baseline --no-e2e 2>/dev/null | tail -1)
+        out=$(env ${envs//,/ } GALOIS_LIB=$lib timeout 600 python bench.py --workload $W --no-cpu-baseline --no-e2e --no-tts 2>/dev/null | tail -1)
         echo "$W $spec: $(echo "$out" | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(round(d['ms_per_step'],4), {k: round(v, 4) for k, v in d['kernels_ms_per_step'].items()})" 2>/dev/null | tail -1)"
     done
 done
