@@ -265,13 +265,14 @@ def stepwise_sampled(G, inst, eng, members, steps, seed=0, *, tau=1.0, lr=0.5, o
     b0 = _first_member(eng)
     rep = dict(steps=0, ties=0, compared=0, counts=0)
     states = {b: eng.get_member(b) for b in members}
+    t0 = states[members[0]]["t"]             # 0 after init, or wherever the engine stands
     prev_u = {}
     for b, s in states.items():
-        assert s["t"] == 0
-        st = O.State.from_reduced(s["z"][None], s["m"][None], s["v"][None], 0, b0=b)
+        assert s["t"] == t0
+        st = O.State.from_reduced(s["z"][None], s["m"][None], s["v"][None], t0, b0=b)
         r0, u0 = O.round_and_check(f, cfg, st)
         # identical z: the rounding [z >= 0] is the same decision in both precisions
-        np.testing.assert_array_equal(s["r"], r0[0], err_msg=f"R_0 member {b}")
+        np.testing.assert_array_equal(s["r"], r0[0], err_msg=f"R_{t0} member {b}")
         prev_u[b] = int(u0[0])
     with ThreadPoolExecutor(max_workers=min(16, len(members))) as pool:
         for t in range(steps):
@@ -282,33 +283,34 @@ def stepwise_sampled(G, inst, eng, members, steps, seed=0, *, tau=1.0, lr=0.5, o
             for b in members:
                 s, n_ = states[b], new[b]
                 out, st = ora[b]
-                assert n_["t"] == t + 1, (b, n_["t"], t)
-                # the count of R_t, checked by this step's fused sweep
-                assert n_["check_t"] == t, (b, n_["check_t"], t, n_["unsat"], prev_u[b])
-                assert n_["unsat"] == prev_u[b], f"unsat(R_{t}) member {b}: {n_['unsat']} vs {prev_u[b]}"
+                tt = t0 + t                  # this step advances tt -> tt + 1
+                assert n_["t"] == tt + 1, (b, n_["t"], tt)
+                # the count of R_tt, checked by this step's fused sweep
+                assert n_["check_t"] == tt, (b, n_["check_t"], tt, n_["unsat"], prev_u[b])
+                assert n_["unsat"] == prev_u[b], f"unsat(R_{tt}) member {b}: {n_['unsat']} vs {prev_u[b]}"
                 rep["counts"] += 1
                 z = s["z"].astype(np.float64)
-                tie_x = compare_bits(f"X_{t + 1}[{b}]", s["x_next"][None], out["xhat"], np.abs(out["a"]),
+                tie_x = compare_bits(f"X_{tt + 1}[{b}]", s["x_next"][None], out["xhat"], np.abs(out["a"]),
                                      ((1e-6 + 1e-6 * np.abs(z)) / tau)[None])
                 if tie_x.any():              # the member's signal used a different bit: skip it this step
                     rep["ties"] += 1
                     prev_u[b] = O.unsat_count(f, n_["r"])
                     continue
-                assert lam[b - b0] == out["lam"][0], f"Lambda_{t + 1} member {b}"
+                assert lam[b - b0] == out["lam"][0], f"Lambda_{tt + 1} member {b}"
                 go = out["grad1"][0]
                 dg = 1e-5 * np.abs(go) + 1e-30
                 zo, mo, vo = (a[0] for a in st.reduced())
-                tol_m, tol_v, tol_z = update_tolerances(s["m"], s["v"], go, dg, zo, mo, vo, t + 1, lr, optimizer)
-                tie_r = compare_bits(f"R_{t + 1}[{b}]", n_["r"][None], out["r"], np.abs(zo)[None], tol_z[None])
+                tol_m, tol_v, tol_z = update_tolerances(s["m"], s["v"], go, dg, zo, mo, vo, tt + 1, lr, optimizer)
+                tie_r = compare_bits(f"R_{tt + 1}[{b}]", n_["r"][None], out["r"], np.abs(zo)[None], tol_z[None])
                 if tie_r.any():
                     rep["ties"] += 1
                     prev_u[b] = O.unsat_count(f, n_["r"])
                     continue
                 if tol_m is not None:
-                    assert (np.abs(n_["m"] - mo) <= tol_m).all(), f"m member {b} step {t + 1}"
-                    assert (np.abs(n_["v"] - vo) <= tol_v).all(), f"v member {b} step {t + 1}"
+                    assert (np.abs(n_["m"] - mo) <= tol_m).all(), f"m member {b} step {tt + 1}"
+                    assert (np.abs(n_["v"] - vo) <= tol_v).all(), f"v member {b} step {tt + 1}"
                 bad = np.abs(n_["z"] - zo) > tol_z
-                assert not bad.any(), f"z member {b} step {t + 1}: {np.argwhere(bad)[:3].ravel()}"
+                assert not bad.any(), f"z member {b} step {tt + 1}: {np.argwhere(bad)[:3].ravel()}"
                 prev_u[b] = int(out["unsat"][0])
                 rep["compared"] += 1
             states = new

@@ -369,6 +369,24 @@ def test_normalized_trajectory(G):
     assert len(rep.resyncs) <= 8, rep.resyncs
 
 
+def test_normalized_steps_31_to_50_identical_iterates(G):
+    """Steps 31-50 of the same phi' (north_star's 50-step horizon), compared one step at a
+    time from identical iterates (reading of the 50-step tolerance past the
+    fp32 drift horizon): the engine runs its first 30 steps alone, then before each of
+    steps 31..50 the sampled members' fp32 iterates go to the oracle, and X, Lambda, R,
+    the unsat count of the previous rounding and z/m/v are held to the one-step bounds."""
+    n2, phi2 = _oracle_normalize(I.industrial(200, 500, 4, planted=True, wmax=10), 3)
+    inst = I.from_clauses("phi'", n2, phi2)
+    cnf = G.Cnf.from_instance(inst)
+    eng = G.Engine(cnf, 1024, 50, 0.5, 1)
+    eng.enqueue(30)
+    members = (0, 1, 7, 100, 333, 512, 777, 1023)
+    rep = parity.stepwise_sampled(G, inst, eng, members, 20, seed=1)
+    assert rep["compared"] >= len(members) * 20 - 4, rep
+    eng.free()
+    cnf.free()
+
+
 # ------------------------------------------------------------------ f4: sub-batching
 def _solve(G, inst, batch, steps, seed, **kw):
     cnf = G.Cnf.from_instance(inst)
