@@ -124,6 +124,29 @@ def peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def l2_roofline(per_kernel, dom, gather_bytes, xr_bytes, names):
+    """Roofline of a dominant clause sweep whose X/R rows are L2-resident (C3b): its row
+    gathers per launch over the launch time, against the measured L2 random-gather
+    bandwidth (profiles/l2_gather_peak.json, tools/randbw.cu). None otherwise."""
+    if dom != "forward" or xr_bytes > 64e6 or dom not in per_kernel:
+        return None
+    path = os.path.join(ROOT, "profiles", "l2_gather_peak.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as f:
+        p = json.load(f)
+    peak = float(p["table_2MB_gbs"] if xr_bytes <= 8e6 else p["table_34MB_gbs"])
+    ms = per_kernel[dom]["ms_per_launch"]
+    gbs = gather_bytes / (ms / 1e3) / 1e9
+    return {"bound": "l2", "kernel": names[dom], "achieved": gbs, "peak": peak, "unit": "GB/s",
+            "frac": gbs / peak, "traffic": None, "algorithmic_bytes_per_launch": gather_bytes,
+            "peak_source": "measured L2 random 256-B gather bandwidth (profiles/l2_gather_peak.json)",
+            "ms_per_launch": ms, "xr_working_set_bytes": xr_bytes,
+            "hbm_model_frac": per_kernel[dom]["frac"],
+            "note": "X/R rows L2-resident: the sweep's row gathers against L2; E writes and the index "
+                    "stream are in hbm_model_frac"}
+
+
 def ncu_traffic(workload, cls="update"):
     """Per-launch DRAM bytes of the dominant kernel from the committed ncu --set full
     summary (profiles/ncu_traffic.json), or None."""
@@ -326,6 +349,7 @@ def main():
     ap.add_argument("--tts", default=None, help="only measure time-to-first-SAT on this config's SAT set")
     ap.add_argument("--tts-seeds", type=int, default=10)
     ap.add_argument("--no-tts", action="store_true", help="skip the configs[0] time-to-first-SAT block")
+    ap.add_argument("--no-c5", action="store_true", help="N > 1: skip the C5 strong-scaling key")
     ap.add_argument("--lanes", type=int, default=None,
                     help="concurrent lanes per GPU (galois_engine_set_lanes); default: 4 for local batches "
                          ">= 4096, else 1")
@@ -449,6 +473,10 @@ def main():
         # E rows of hub occurrences read, int16x4 partials written
         "hub_partial": L_hub * W * 4 + hub_chunks * b_pad * 2,
     }
+    # the sweep's row gathers (X every step, R every K-th) and the X/R working set: when the
+    # rows stay L2-resident the sweep is judged against L2 gather bandwidth, not HBM
+    alg_gather = L * W * 4 + L * W * 4 / args.check_interval
+    xr_bytes = n * b_pad // 4
     peak, peak_src = peaks()
     per_kernel = {}
     for cls, nbytes in alg.items():
@@ -479,18 +507,25 @@ def main():
     gpu_launches = int(sum(c for _, c in kt.values())) * n_lanes    # every lane launches the same kernels
     total_kernel_ms = sum(t for t, _ in kt.values())
 
+    # e2e, time-to-first-SAT and (N > 1) C5 strong scaling run on every rank (NCCL
+    # engines), each timed as the max over ranks
+    extra = {"e2e": None, "tts": None, "c5": None}
+    dist_args = (pg, rank, world, new_nccl_id) if pg else None
+    if not args.no_e2e:
+        extra["e2e"] = run_e2e(G, inst, B, args, torch, dev, lanes if world == 1 else 1, dist=dist_args)
+    if not args.no_tts:                      # north_star's second metric, on configs[0] (C1)
+        extra["tts"] = time_to_sat(G, torch, dev, "C1", range(8), dist=dist_args)
+        extra["tts"].pop("per_instance", None)
+    if world > 1 and args.workload != "C5" and not args.no_c5:
+        extra["c5"] = strong_c5(G, torch, dev, args, dist_args)
+
     line = None
     if rank == 0:
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             cpu = oracle_sample(inst, B, seconds=args.ref_seconds)
-        e2e = None
-        if world == 1 and not args.no_e2e:
-            e2e = run_e2e(G, inst, B, args, torch, dev, lanes)
-        tts = None
-        if world == 1 and not args.no_tts:      # north_star's second metric, on configs[0] (C1)
-            tts = time_to_sat(G, torch, dev, "C1", range(8))
-            tts.pop("per_instance", None)
+        e2e = extra["e2e"]
+        tts = extra["tts"]
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
@@ -501,7 +536,7 @@ def main():
                        "lanes_per_gpu": n_lanes,
                        "l2": l2_note,
                        "parallelism": f"dp{world} (batch sharding, NCCL MIN all-reduce of the best key per step)"},
-            "roofline": {"bound": "hbm", "kernel": KNAME[dom],
+            "roofline": l2_roofline(per_kernel, dom, alg_gather, xr_bytes, KNAME) or {"bound": "hbm", "kernel": KNAME[dom],
                          "achieved": per_kernel.get(dom, {}).get("achieved_gbs"), "peak": peak, "unit": "GB/s",
                          "frac": per_kernel.get(dom, {}).get("frac"),
                          "traffic": ncu_traffic(args.workload, dom),
@@ -525,6 +560,8 @@ def main():
             "cpu_baseline": cpu,
             "time_to_first_sat": tts,
         }
+        if extra["c5"] is not None:
+            line["c5_strong_scaling"] = extra["c5"]
     eng.free()
     cnf.free()
     if pg:
@@ -583,6 +620,36 @@ def time_to_sat(G, torch, dev, which="C1", seeds=range(10), batch=None, steps=No
             "per_instance": out}
 
 
+def strong_c5(G, torch, dev, args, dist, steps=10, warmup=3):
+    """configs[4] at N GPUs (extra key of an N > 1 run): the cube-split 100k-variable
+    instance's GLOBAL batch of 65,536 members sharded over the ranks (strong scaling) with
+    the NCCL MIN exchange every step; device time of `steps` steps after `warmup`, CUDA
+    events on the engine stream, max over ranks."""
+    pg, rank, world, new_id = dist
+    inst = make_instance("C5")
+    B = WORKLOADS["C5"]["batch"]
+    stream = torch.cuda.current_stream(dev)
+    cnf = G.Cnf.from_instance(inst)
+    eng = G.Engine(cnf, B, warmup + steps, 0.5, 0, cubes=inst.pins, stream=stream.cuda_stream, rank=rank,
+                   world=world, nccl_id=new_id())
+    eng.enqueue(warmup)
+    torch.cuda.synchronize(dev)
+    pg.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    eng.enqueue(steps)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    pg.all_reduce(t, op=pg.ReduceOp.MAX)
+    ms = float(t.item())
+    eng.free()
+    cnf.free()
+    return {"workload": "C5", "scaling": "strong", "global_batch": B, "batch_per_gpu": -(-B // world),
+            "n_gpus": world, "steps": steps, "warmup": warmup, "ms_per_step": ms / steps,
+            "value": inst.L * B * steps / (ms / 1e3), "unit": UNIT}
+
+
 def default_lanes(batch_per_gpu):
     """Concurrent lanes per GPU: 4 for local batches of 4096-8192 members
     (C2: 0.266 -> 0.247 ms/step), 2 from 16384 on (C3b: 0.493 -> 0.484 ms with 2 instead of
@@ -600,12 +667,16 @@ def effective_lanes(b_loc, lanes, world):
     return -(-b_loc // ls) if b_loc > ls else 1
 
 
-def run_e2e(G, inst, B, args, torch, dev, lanes=1):
+def run_e2e(G, inst, B, args, torch, dev, lanes=1, dist=None):
     """Same metric end to end through the public C ABI with HOST buffers: CNF upload
     (host -> device), device CSR/CSC build, engine create + init, galois_engine_run of
     the timed steps (host polls the device stop flag), and the results read back
-    (unsat counts + best assignment). Host wall clock bracketed by device syncs."""
+    (unsat counts + best assignment). Host wall clock bracketed by device syncs. Under
+    torchrun (dist = (process group, rank, world, id factory)) every rank uploads its
+    replica of the CNF and runs its slice of the global batch B with the NCCL exchange;
+    the time is the max over ranks and the byte counts are summed over ranks."""
     import numpy as np
+    pg, rank, world, new_id = dist if dist else (None, 0, 1, None)
     off = np.ascontiguousarray(inst.offsets, dtype=np.int64)
     lits = np.ascontiguousarray(inst.lits, dtype=np.int32)
     results = []
@@ -613,27 +684,34 @@ def run_e2e(G, inst, B, args, torch, dev, lanes=1):
     # (C4: the CNF upload takes ~350 ms in the first passes, ~20 ms after, with sporadic
     # 50-250 ms host-side stalls); the line reports the median of the last five passes
     for rep in range(8):
+        kw = dict(rank=rank, world=world, nccl_id=new_id()) if pg else {}
         torch.cuda.synchronize(dev)
+        if pg:
+            pg.barrier()
         t0 = time.perf_counter()
         cnf = G.Cnf(inst.n, off, lits)
         eng = G.Engine(cnf, B, args.steps, 0.5, 0, cubes=inst.pins, lanes=lanes,
-                       check_interval=args.check_interval)
+                       check_interval=args.check_interval, **kw)
         eng.run()
         counts, _ = eng.unsat_counts()
         best = eng.best_assignment()
         torch.cuda.synchronize(dev)
         el = time.perf_counter() - t0
+        if pg:
+            t = torch.tensor([el], dtype=torch.float64, device=dev)
+            pg.all_reduce(t, op=pg.ReduceOp.MAX)
+            el = float(t.item())
         done = eng.info()["steps_done"]
         eng.free()
         cnf.free()
         results.append((el, done))
     el, done = sorted(results[-5:])[2]
-    h2d = off.nbytes + lits.nbytes + 8 * (args.steps + 2) + 64
+    h2d = world * (off.nbytes + lits.nbytes + 8 * (args.steps + 2) + 64)   # every rank uploads a replica
     K = args.check_interval                      # run(): one 64-byte poll per chunk of G steps
     KK = K if K % 2 == 0 else 2 * K
     polls = -(-args.steps // (KK * max(1, 8 // KK))) + 2
-    d2h = 64 * polls + 4 * B + inst.n
-    return {"value": inst.L * B * done / el, "unit": UNIT, "steps": done,
+    d2h = world * 64 * polls + 4 * B + world * inst.n     # polls and the winner's bits on every rank
+    return {"value": inst.L * B * done / el, "unit": UNIT, "steps": done, "n_gpus": world,
             "h2d_bytes_per_step": h2d / max(done, 1), "d2h_bytes_per_step": d2h / max(done, 1),
             "wall_s": el, "includes": "cnf upload + CSR/CSC build + create/init + run + read-back"}
 

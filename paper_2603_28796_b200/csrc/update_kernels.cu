@@ -26,14 +26,14 @@ namespace {
 
 constexpr int kBatch = 8;             // independent E loads in flight per thread (global path)
 #ifndef GALOIS_UPD_STAGES
-#define GALOIS_UPD_STAGES 3
+#define GALOIS_UPD_STAGES 4
 #endif
 #ifndef GALOIS_UPD_CTAS
-#define GALOIS_UPD_CTAS 4
+#define GALOIS_UPD_CTAS 3
 #endif
 constexpr int kStages = GALOIS_UPD_STAGES;   // TMA pipeline depth
 constexpr int kStageRows = 32;        // E rows staged per item (variables with degree <= 32)
-constexpr int kTmaCtasPerSm = GALOIS_UPD_CTAS;   // 4 x (3 x 16 KB) shared memory per SM
+constexpr int kTmaCtasPerSm = GALOIS_UPD_CTAS;   // 3 x (4 x 16 KB) shared memory per SM
 constexpr int kStageE = kStageRows * 128;
 constexpr int kStageBytes = kStageE + 3 * 4096;   // E rows + z, m, v of 256 quads
 constexpr int kTmaSmem = kStages * kStageBytes;
@@ -677,21 +677,21 @@ __global__ void __launch_bounds__(256 + 32, kTmaCtasPerSm) k_update_tma(DevCnf c
 // against 128-occurrence chunks at 4 CTAs per SM: C3b hub partials 0.194 -> 0.183 ms,
 // update 0.065 -> 0.060 ms (half the partials to read), C4 0.191 -> 0.181 ms.
 constexpr int kHubStageBytes = kHubChunk * 128;
-constexpr int kHubCtasPerSm = kStages * kHubStageBytes * kTmaCtasPerSm <= 200 * 1024 ? kTmaCtasPerSm
-                                                                                    : (200 * 1024) / (kStages * kHubStageBytes);
+constexpr int kHubStages = 3;
+constexpr int kHubCtasPerSm = 2;                 // 2 x (3 x 32 KB) shared memory per SM
 
-__global__ void __launch_bounds__(256 + 32, kTmaCtasPerSm) k_hub_partial_tma(DevCnf c, RowMap rm,
+__global__ void __launch_bounds__(256 + 32, kHubCtasPerSm) k_hub_partial_tma(DevCnf c, RowMap rm,
                                                                            const uint32_t *__restrict__ E,
                                                                            short4 *__restrict__ partial,
                                                                            const Ctrl *__restrict__ ctrl)
 {
     extern __shared__ __align__(128) uint8_t smem[];
-    __shared__ uint64_t full[kStages], empty[kStages];
-    __shared__ int4 hdr[kStages];          // {first row, positive rows, rows, hub chunk}
+    __shared__ uint64_t full[kHubStages], empty[kHubStages];
+    __shared__ int4 hdr[kHubStages];          // {first row, positive rows, rows, hub chunk}
     if (ctrl->stopped) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid == 0) {
-        for (int i = 0; i < kStages; ++i) {
+        for (int i = 0; i < kHubStages; ++i) {
             mbar_init(&full[i], 1);
             mbar_init(&empty[i], 32 * kConsumerWarps);   // every consumer thread releases
         }
@@ -702,9 +702,9 @@ __global__ void __launch_bounds__(256 + 32, kTmaCtasPerSm) k_hub_partial_tma(Dev
         if (lane == 0) {
             uint32_t slot = 0;
             for (uint32_t item = blockIdx.x; item < rm.items; item += gridDim.x, ++slot) {
-                const int st = (int)(slot % kStages);
-                if (slot >= (uint32_t)kStages) {
-                    mbar_wait(&empty[st], ((slot / kStages) - 1u) & 1u);
+                const int st = (int)(slot % kHubStages);
+                if (slot >= (uint32_t)kHubStages) {
+                    mbar_wait(&empty[st], ((slot / kHubStages) - 1u) & 1u);
                     fence_proxy_async_smem();
                 }
                 const uint32_t hc = div_cpr(rm, item), ch = item - hc * rm.cpr;
@@ -731,8 +731,8 @@ __global__ void __launch_bounds__(256 + 32, kTmaCtasPerSm) k_hub_partial_tma(Dev
         constexpr int kHP = kHubChunk <= 248 ? 5 : 6;
         __shared__ uint32_t sP[2][kConsumerWarps][kHP][32];
         for (uint32_t item = blockIdx.x; item < rm.items; item += gridDim.x, ++slot) {
-            const int st = (int)(slot % kStages);
-            mbar_wait(&full[st], (slot / kStages) & 1u);
+            const int st = (int)(slot % kHubStages);
+            mbar_wait(&full[st], (slot / kHubStages) & 1u);
             const int4 h = hdr[st];
             uint32_t Q[kHP];
 #pragma unroll
@@ -761,8 +761,8 @@ __global__ void __launch_bounds__(256 + 32, kTmaCtasPerSm) k_hub_partial_tma(Dev
         }
 #else
         for (uint32_t item = blockIdx.x; item < rm.items; item += gridDim.x, ++slot) {
-            const int st = (int)(slot % kStages);
-            mbar_wait(&full[st], (slot / kStages) & 1u);
+            const int st = (int)(slot % kHubStages);
+            mbar_wait(&full[st], (slot / kHubStages) & 1u);
             const int4 h = hdr[st];
             const uint32_t *srow = reinterpret_cast<const uint32_t *>(smem + st * kHubStageBytes) + (tid >> 3);
             int32_t G[4] = {0, 0, 0, 0};
@@ -1077,7 +1077,7 @@ void hub_partial(const DevCnf &c, int32_t W, int32_t b_pad, const uint32_t *E, s
     if (c.num_hub_chunks == 0) return;
     const RowMap rm = make_rowmap((uint32_t)c.num_hub_chunks, (uint32_t)b_pad);
     if (W % 32 == 0)
-        k_hub_partial_tma<<<item_grid(rm, kHubCtasPerSm), 256 + 32, kStages * kHubStageBytes, st>>>(c, rm, E, partial,
+        k_hub_partial_tma<<<item_grid(rm, kHubCtasPerSm), 256 + 32, kHubStages * kHubStageBytes, st>>>(c, rm, E, partial,
                                                                                                    ctrl);
     else
         k_hub_partial<<<item_grid(rm, 8), 256, 0, st>>>(c, W < 32 ? W : 32, rm, E, partial, ctrl);
@@ -1170,7 +1170,7 @@ cudaError_t configure_kernels()
         if (e != cudaSuccess) return e;
     }
     e = cudaFuncSetAttribute((const void *)k_hub_partial_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             kStages * kHubStageBytes);
+                             kHubStages * kHubStageBytes);
     if (e != cudaSuccess) return e;
     if (dev < 64) done.fetch_or(1ull << dev);
     return cudaSuccess;
