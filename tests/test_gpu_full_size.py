@@ -73,8 +73,9 @@ C5_MEMBERS = (0, 1023, 1024, 4100, 6143, 8191)
 def test_c5_chunk_loop_stepwise(G, c5):
     """configs[4]'s instance (100k variables, 16 cube pins) at 8192 members per GPU: the X/R
     slices of the eight 1024-member chunks (25.6 MB each) exceed the sweep's 48 MB L2 budget,
-    so k_sweep<..., kLoop = true> walks the chunks in a loop (the instantiation C5 runs at
-    every GPU count); sampled members from several chunks, pins forced."""
+    so the staged sweep k_sweep_tma<..., kLoop = true> walks the chunks in a loop (the
+    instantiation C5 runs at every GPU count); sampled members from several chunks, pins
+    forced."""
     cnf = G.Cnf.from_instance(c5)
     eng = G.Engine(cnf, 8192, 50, 0.5, 0, cubes=c5.pins)
     rep = parity.stepwise_sampled(G, c5, eng, C5_MEMBERS, 3, seed=0, cubes=c5.pins)
@@ -88,6 +89,23 @@ def test_c5_chunk_loop_debug_signal(G, c5):
     eng = G.Engine(cnf, 8192, 5, 0.5, 0, cubes=c5.pins, debug=True)
     ties = parity.debug_signal_sampled(G, c5, eng, C5_MEMBERS, seed=0, cubes=c5.pins)
     assert ties <= 1
+    eng.free()
+    cnf.free()
+
+
+def test_chunk_loop_wide_tiles_stepwise(G):
+    """k_sweep_tma's other index path: 200k variables (X/R slices of 51 MB: the chunk loop)
+    and clause widths up to 40, so the width-sorted tail has 32-clause tiles of more than
+    512 slots, which read their slots from global memory instead of the staged tile;
+    B = 2048 (two chunks), sampled members of both, 3 steps."""
+    inst = I.industrial(200_000, 120_000, 7, wmin=2, wmax=40, width_exp=1.2)
+    w = np.diff(inst.offsets)
+    assert (w >= 17).sum() >= 64                    # whole tiles past the 512-slot stage
+    cnf = G.Cnf.from_instance(inst)
+    eng = G.Engine(cnf, 2048, 20, 0.5, 0)
+    members = (0, 5, 1023, 1024, 1500, 2047)
+    rep = parity.stepwise_sampled(G, inst, eng, members, 3, seed=0)
+    assert rep["compared"] >= len(members) * 3 - 2, rep
     eng.free()
     cnf.free()
 

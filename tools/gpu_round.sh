@@ -18,7 +18,7 @@ fi
 if has bench; then
     for W in C2 C1 C3a C3b C4 C5; do
         extra="--no-cpu-baseline"
-        [ "$W" = C2 ] && extra=""
+        [ "$W" = C4 ] && extra=""
         timeout 600 python bench.py --workload $W $extra > "$OUT/bench_$W.json" 2> "$OUT/bench_$W.err"
         tail -c 400 "$OUT/bench_$W.json"; echo
     done
@@ -43,4 +43,13 @@ if has full; then
             echo "full $W $K rc=$?"
         done
     done
+fi
+if has sanitize; then
+    CS=/usr/local/cuda/bin/compute-sanitizer
+    for tool in memcheck racecheck synccheck; do
+        for part in small tma lanes loop v4 soft select tseitin window; do
+            timeout 900 $CS --tool $tool --error-exitcode 9 python tools/sanitize.py $part > "$OUT/san_${tool}_$part.log" 2>&1
+            echo "sanitize $tool $part rc=$? $(grep -E 'ERROR SUMMARY|RACECHECK SUMMARY' $OUT/san_${tool}_$part.log | tail -1)"
+        done
+    done 2>&1 | tee "$OUT/sanitize_summary.txt"
 fi
