@@ -303,26 +303,13 @@ __device__ __forceinline__ bool sample_bit_tau1(float z, float2 uu, float e)
 }
 
 // a7 for one quad: gradient, optimiser, rounding, next sample. Returns the nibbles.
-// The quad's two Philox draws (noise of step s for the gradient, of step s + 1 for the next
-// sample): they depend only on (v, quad, s), so k_update_tma draws them before waiting for
-// the item's data.
-struct QuadNoise {
-    uint4 wn, wx;
-};
-__device__ __forceinline__ QuadNoise quad_noise(const StepParams &p, int32_t v, int64_t bq, int32_t s)
-{
-    QuadNoise r;
-    r.wn = philox4x32_10(make_uint4((uint32_t)v, (uint32_t)(bq >> 2), (uint32_t)s, 1u), p.keys);
-    r.wx = philox4x32_10(make_uint4((uint32_t)v, (uint32_t)(bq >> 2), (uint32_t)(s + 1), 1u), p.keys);
-    return r;
-}
-
 template <bool kTau1, bool kAdam, bool kPins>
 __device__ __forceinline__ void quad_update(const StepParams &p, float2 ac, int32_t v, int64_t bq, int32_t s,
                                             const int32_t G[4], float4 &z, float4 &m, float4 &vv, uint32_t &xn,
-                                            uint32_t &rn, float g1o[4], bool &bad, const QuadNoise &nz)
+                                            uint32_t &rn, float g1o[4], bool &bad)
 {
-    const uint4 wn4 = nz.wn, wx4 = nz.wx;
+    const uint4 wn4 = philox4x32_10(make_uint4((uint32_t)v, (uint32_t)(bq >> 2), (uint32_t)s, 1u), p.keys);
+    const uint4 wx4 = philox4x32_10(make_uint4((uint32_t)v, (uint32_t)(bq >> 2), (uint32_t)(s + 1), 1u), p.keys);
     const uint32_t wn[4] = {wn4.x, wn4.y, wn4.z, wn4.w};
     const uint32_t wx[4] = {wx4.x, wx4.y, wx4.z, wx4.w};
     float zz[4] = {z.x, z.y, z.z, z.w}, mm[4] = {m.x, m.y, m.z, m.w}, ww[4] = {vv.x, vv.y, vv.z, vv.w};
@@ -374,14 +361,6 @@ __device__ __forceinline__ void quad_update(const StepParams &p, float2 ac, int3
     z = make_float4(zz[0], zz[1], zz[2], zz[3]);
     m = make_float4(mm[0], mm[1], mm[2], mm[3]);
     vv = make_float4(ww[0], ww[1], ww[2], ww[3]);
-}
-
-template <bool kTau1, bool kAdam, bool kPins>
-__device__ __forceinline__ void quad_update(const StepParams &p, float2 ac, int32_t v, int64_t bq, int32_t s,
-                                            const int32_t G[4], float4 &z, float4 &m, float4 &vv, uint32_t &xn,
-                                            uint32_t &rn, float g1o[4], bool &bad)
-{
-    quad_update<kTau1, kAdam, kPins>(p, ac, v, bq, s, G, z, m, vv, xn, rn, g1o, bad, quad_noise(p, v, bq, s));
 }
 
 __device__ __forceinline__ void hub_signal(const DevCnf &c, const short4 *__restrict__ partial, uint32_t QW,
@@ -593,16 +572,6 @@ __global__ void __launch_bounds__(256 + 32, kTmaCtasPerSm) k_update_tma(DevCnf c
     for (uint32_t item = blockIdx.x; item < rm.items; item += gridDim.x) {
         float4 z, m, vv;
         int32_t v = 0, flags = 0, negs = 0;
-        // the noise needs only the item's position: drawn while the item's stage may still be
-        // in flight (a consumer that would wait does the Philox rounds instead)
-        const uint32_t v_item = div_cpr(rm, item);
-        const uint32_t q = (item - v_item * rm.cpr) * 256u + (uint32_t)tid;
-        const int64_t bq = p.b0 + 4 * (int64_t)q;
-        const QuadNoise nz = quad_noise(p, (int32_t)v_item, bq, s);
-        // pin the draws ahead of the first wait (the compiler would otherwise sink them to
-        // their use after it): an empty volatile asm that consumes them
-        asm volatile("" ::"r"(nz.wn.x), "r"(nz.wn.y), "r"(nz.wn.z), "r"(nz.wn.w), "r"(nz.wx.x), "r"(nz.wx.y),
-                     "r"(nz.wx.z), "r"(nz.wx.w));
         int32_t G[4] = {0, 0, 0, 0};
         // kSliced (high average degree): counts carried across an item's pieces in SWAR bytes
         // (degree < kSlicedMinDegree: a byte cannot overflow) or bit-sliced planes (flag 16),
@@ -623,7 +592,10 @@ __global__ void __launch_bounds__(256 + 32, kTmaCtasPerSm) k_update_tma(DevCnf c
                 vv = reinterpret_cast<const float4 *>(sb + kStageE + 8192)[tid];
             }
             if (flags & 4) {
-                if (!kSliced) hub_signal(c, partial, QW, c.hub_of_var[v], q, G);
+                if (!kSliced) {
+                    const uint32_t q = (item - (uint32_t)v * rm.cpr) * 256u + (uint32_t)tid;
+                    hub_signal(c, partial, QW, c.hub_of_var[v], q, G);
+                }
             } else {
                 // rows [r0, r1): negative ones (from k1 on) are stored complemented
                 const uint32_t *srow = reinterpret_cast<const uint32_t *>(sb) + (tid >> 3);
@@ -650,6 +622,7 @@ __global__ void __launch_bounds__(256 + 32, kTmaCtasPerSm) k_update_tma(DevCnf c
                 ph ^= 1u;
             }
         } while (!(flags & 2));
+        const uint32_t q = (item - (uint32_t)v * rm.cpr) * 256u + (uint32_t)tid;
         if (kSliced && (flags & 4)) {
             hub_signal(c, partial, QW, c.hub_of_var[v], q, G);
         } else if (kSliced) {
@@ -661,6 +634,7 @@ __global__ void __launch_bounds__(256 + 32, kTmaCtasPerSm) k_update_tma(DevCnf c
 #pragma unroll
             for (int j = 0; j < 4; ++j) G[j] -= negs;
         }
+        const int64_t bq = p.b0 + 4 * (int64_t)q;
         uint32_t xn, rn;
         float g1o[4];
         // cube pins (C5: 16 of 100k variables): the pinned code path only where the
@@ -673,9 +647,9 @@ __global__ void __launch_bounds__(256 + 32, kTmaCtasPerSm) k_update_tma(DevCnf c
         z.x += 1.0f; m.x += 1.0f; vv.x += 1.0f;
 #else
         if (kPins && (flags & 8))
-            quad_update<kTau1, kAdam, true>(p, ac, v, bq, s, G, z, m, vv, xn, rn, g1o, bad, nz);
+            quad_update<kTau1, kAdam, true>(p, ac, v, bq, s, G, z, m, vv, xn, rn, g1o, bad);
         else
-            quad_update<kTau1, kAdam, false>(p, ac, v, bq, s, G, z, m, vv, xn, rn, g1o, bad, nz);
+            quad_update<kTau1, kAdam, false>(p, ac, v, bq, s, G, z, m, vv, xn, rn, g1o, bad);
 #endif
         const size_t idx = (size_t)v * QW + q;
         z4[idx] = z;
