@@ -53,6 +53,23 @@ __device__ __forceinline__ uint4 lit4(const uint4 *B, int RS, int32_t code)
     return s;
 }
 
+#ifndef GALOIS_SWEEP_XR256
+#define GALOIS_SWEEP_XR256 1   // fused forward + check: X and R of a literal in one 256-bit load
+#endif
+// X and R vectors of literal `code` (16 B each, adjacent: R = X + 4 words) in ONE 256-bit
+// load with an L2 evict-last priority (the X/R rows are the sweep's reused working set;
+// E and the index stream past them), sign applied to both
+__device__ __forceinline__ void lit_xr(const uint4 *BX, int RS, int32_t code, uint4 &x, uint4 &r)
+{
+    const uint4 *p = BX + (size_t)(code >> 1) * RS;
+    asm("ld.global.nc.L2::evict_last.v8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+        : "=r"(x.x), "=r"(x.y), "=r"(x.z), "=r"(x.w), "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+        : "l"(p));
+    const uint32_t neg = 0u - (uint32_t)(code & 1);
+    x.x ^= neg; x.y ^= neg; x.z ^= neg; x.w ^= neg;
+    r.x ^= neg; r.y ^= neg; r.z ^= neg; r.w ^= neg;
+}
+
 __device__ __forceinline__ void acc2(uint4 &any, uint4 &two, uint4 s)
 {
     two.x |= any.x & s.x; two.y |= any.y & s.y; two.z |= any.z & s.z; two.w |= any.w & s.w;
@@ -373,17 +390,31 @@ __global__ void __launch_bounds__(256, SweepShape<kWide>::kMinBlocks) k_sweep(De
 #pragma unroll
             for (int i = 0; i < kSweepCached; ++i) {
                 if (i < width) {
-                    if (kForward) {
-                        S[i] = lit4(BX, RS, si[i].x);
+                    if (kForward && kCheck && GALOIS_SWEEP_XR256) {
+                        uint4 r;
+                        lit_xr(BX, RS, si[i].x, S[i], r);
                         acc2(any, two, S[i]);
+                        or4(anyR, r);
+                    } else {
+                        if (kForward) {
+                            S[i] = lit4(BX, RS, si[i].x);
+                            acc2(any, two, S[i]);
+                        }
+                        if (kCheck) or4(anyR, lit4(BR, RS, si[i].x));
                     }
-                    if (kCheck) or4(anyR, lit4(BR, RS, si[i].x));
                 }
             }
             for (int i = kSweepCached; i < width; ++i) {
                 const int2 sj = c.sweep_slot[lo + i];
-                if (kForward) acc2(any, two, lit4(BX, RS, sj.x));
-                if (kCheck) or4(anyR, lit4(BR, RS, sj.x));
+                if (kForward && kCheck && GALOIS_SWEEP_XR256) {
+                    uint4 x, r;
+                    lit_xr(BX, RS, sj.x, x, r);
+                    acc2(any, two, x);
+                    or4(anyR, r);
+                } else {
+                    if (kForward) acc2(any, two, lit4(BX, RS, sj.x));
+                    if (kCheck) or4(anyR, lit4(BR, RS, sj.x));
+                }
             }
             if (kForward) {
 #pragma unroll
