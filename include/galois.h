@@ -186,7 +186,8 @@ int galois_engine_set_cubes(galois_engine *eng, int32_t d, const int32_t *vars);
  * (broadcast from the owner rank, b* / b_per), the unsat counts and steps_done are exactly
  * the single-GPU result; a rank that did not hold the SAT member may run one update past t*
  * (its iterate then is one step ahead; no further check runs). All ranks must make the same
- * sequence of step / enqueue / run / best_assignment calls. */
+ * sequence of step / enqueue / run / info / unsat_counts / best_assignment calls: each may
+ * run the pending check and its collective exchange. */
 int galois_engine_set_comm(galois_engine *eng, int32_t rank, int32_t world, const void *nccl_unique_id);
 
 /* Use the caller's CUDA stream (a cudaStream_t, e.g. torch.cuda.current_stream()). */

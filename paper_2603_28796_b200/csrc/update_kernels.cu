@@ -32,7 +32,14 @@ constexpr int kBatch = 8;             // independent E loads in flight per threa
 #define GALOIS_UPD_CTAS 3
 #endif
 constexpr int kStages = GALOIS_UPD_STAGES;   // TMA pipeline depth
-constexpr int kStageRows = 32;        // E rows staged per item (variables with degree <= 32)
+#ifndef GALOIS_STAGE_ROWS
+#define GALOIS_STAGE_ROWS 48
+#endif
+#ifndef GALOIS_SLICED_ROWS
+#define GALOIS_SLICED_ROWS 16
+#endif
+constexpr int kStageRows = GALOIS_STAGE_ROWS;   // E rows staged per piece (48: C3a update -1.7 %, C4 -0.7 %)
+static_assert(kStageRows <= 56, "a piece's rows must fit count_rows_sliced<3> (<= 7 per thread)");
 constexpr int kTmaCtasPerSm = GALOIS_UPD_CTAS;   // 3 x (4 x 16 KB) shared memory per SM
 constexpr int kStageE = kStageRows * 128;
 constexpr int kStageBytes = kStageE + 3 * 4096;   // E rows + z, m, v of 256 quads
@@ -609,8 +616,8 @@ __global__ void __launch_bounds__(256 + 32, kTmaCtasPerSm) k_update_tma(DevCnf c
                         for (int32_t k = 0; k < nrows; ++k) acc += quad_bits(srow[k * 32], sh);
                     }
                 } else {
-                    if (nrows >= 16)                // uniform over the CTA: a long piece
-                        count_rows_sliced<3>(srow, nrows, tid & 7, sh, G);   // <= 4 rows per thread
+                    if (nrows >= GALOIS_SLICED_ROWS)   // uniform over the CTA: a long piece
+                        count_rows_sliced<3>(srow, nrows, tid & 7, sh, G);   // <= 6 rows per thread
                     else
                         count_bits_smem(srow, nrows, sh, G);
                     if (nneg > 0) { G[0] -= nneg; G[1] -= nneg; G[2] -= nneg; G[3] -= nneg; }
