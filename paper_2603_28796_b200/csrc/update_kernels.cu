@@ -677,6 +677,258 @@ __global__ void __launch_bounds__(256 + 32, kTmaCtasPerSm) k_update_tma(DevCnf c
     last_cta_tick(ctrl);                   // one barrier site for producer and consumers
 }
 
+// ------------------------- a6 + a7: fused update over variable PAIRS (W % 32 == 0)
+// k_update_tma with item = (variables 2p and 2p + 1, 1024-member chunk): a pair whose two
+// E blocks together fit one stage (no hub, <= kPairRows rows — most variables of sparse
+// instances) travels as ONE stage — z, m, v of both (8 KB per array, one bulk copy each
+// when the rows are adjacent, i.e. b_pad = 1024) and both CSC blocks (adjacent: one copy)
+// — and each consumer thread updates its quad of BOTH variables: the per-stage costs
+// (mbarrier waits and polls, header, flags, release) are paid once per two variables, and
+// the two quads' arithmetic interleaves. Other pairs go variable by variable through
+// pieces of kPairRows rows as in k_update_tma (flag 64: the stage is about the second
+// variable). Non-debug, non-sliced instantiations only (the launcher keeps k_update_tma
+// for those); same per-quad arithmetic (quad_update), so iterates are bit-identical.
+constexpr int kPairRows = 56;                        // <= 7 rows per thread: count_rows_sliced<3>
+constexpr int kPairStages = 3;
+constexpr int kPairCtasPerSm = 2;
+constexpr int kPairE = kPairRows * 128;
+constexpr int kPairStageBytes = kPairE + 3 * 8192;   // E rows + z, m, v of two variables
+constexpr int kPairSmem = kPairStages * kPairStageBytes;
+static_assert(kPairStageBytes % 128 == 0, "stage alignment");
+
+struct PairHdr {
+    int32_t v0;       // first variable of the pair
+    int32_t r0, r1;   // CSC rows staged
+    int32_t split;    // pair stage: first row of v0 + 1
+    int32_t neg0;     // first negative row of v0 (or of the stage's variable)
+    int32_t neg1;     // pair stage: first negative row of v0 + 1
+};
+// stage flags
+constexpr int kPfFirst = 1, kPfLast = 2, kPfHub = 4, kPfPin0 = 8, kPfPin1 = 16, kPfPair = 32, kPfSlot1 = 64,
+              kPfHas1 = 128;
+
+__device__ __forceinline__ void count_piece(const uint32_t *srow, int32_t n, int qp, int32_t G[4])
+{
+    if (n >= GALOIS_SLICED_ROWS)       // uniform over the CTA: a long piece
+        count_rows_sliced<3>(srow, n, threadIdx.x & 7, qp, G);
+    else
+        count_bits_smem(srow, n, qp, G);
+}
+
+template <bool kTau1, bool kAdam, bool kPins>
+__global__ void __launch_bounds__(256 + 32, kPairCtasPerSm)
+    k_update_pair(DevCnf c, StepParams p, RowMap rm, float4 *__restrict__ z4, float4 *__restrict__ m4,
+                  float4 *__restrict__ v4, uint32_t *__restrict__ X, uint32_t *__restrict__ R,
+                  const uint32_t *__restrict__ E, const short4 *__restrict__ partial, Ctrl *__restrict__ ctrl)
+{
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ uint64_t full[kPairStages], empty[kPairStages];
+    __shared__ PairHdr hdr[kPairStages];
+    __shared__ int32_t hflags[kPairStages];
+    if (ctrl->stopped) return;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t QW = rm.QW;
+    const uint32_t full_s = smem_u32(full), empty_s = smem_u32(empty), stage_s = smem_u32(smem);
+    if (tid == 0) {
+        for (int i = 0; i < kPairStages; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], 32 * kConsumerWarps);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    if (warp == kConsumerWarps) {          // ------------------------------ producer warp
+        if (lane == 0) {
+            int st = 0;
+            uint32_t ph = 0;
+            bool wrapped = false;
+            auto acquire = [&]() -> uint32_t {  // the next free stage's shared-window address
+                if (wrapped) {
+                    mbar_wait_s(empty_s + 8u * st, ph ^ 1u);
+                    fence_proxy_async_smem();
+                }
+                return stage_s + (uint32_t)(st * kPairStageBytes);
+            };
+            auto advance = [&]() {
+                if (++st == kPairStages) {
+                    st = 0;
+                    ph ^= 1u;
+                    wrapped = true;
+                }
+            };
+            for (uint32_t item = blockIdx.x; item < rm.items; item += gridDim.x) {
+                const uint32_t pr = div_cpr(rm, item), ch = item - pr * rm.cpr;
+                const int32_t v0 = 2 * (int32_t)pr;
+                const bool has1 = v0 + 1 < c.n;
+                const int32_t k0 = c.code_off[2 * v0], k1 = c.code_off[2 * v0 + 1], k2 = c.code_off[2 * v0 + 2];
+                const int32_t k3 = has1 ? c.code_off[2 * v0 + 3] : k2, k4 = has1 ? c.code_off[2 * v0 + 4] : k2;
+                const bool hub0 = c.num_hubs > 0 && c.hub_of_var[v0] >= 0;
+                const bool hub1 = has1 && c.num_hubs > 0 && c.hub_of_var[v0 + 1] >= 0;
+                const int32_t pins = (kPins && p.pin_rank[v0] >= 0 ? kPfPin0 : 0) |
+                                     (kPins && has1 && p.pin_rank[v0 + 1] >= 0 ? kPfPin1 : 0) | (has1 ? kPfHas1 : 0);
+                const size_t off0 = (size_t)v0 * QW + (size_t)ch * 256u, off1 = off0 + QW;
+                const uint32_t *Ech = E + (size_t)ch * c.L * 32u;
+                if (has1 && !hub0 && !hub1 && k4 - k0 <= kPairRows) {
+                    const uint32_t sbs = acquire(), fb = full_s + 8u * st;
+                    hdr[st] = PairHdr{v0, k0, k4, k2, k1, k3};
+                    hflags[st] = kPfFirst | kPfLast | kPfPair | pins;
+                    const uint32_t ebytes = (uint32_t)(k4 - k0) * 128u;
+                    mbar_arrive_expect_tx_s(fb, 3u * 8192u + ebytes);
+                    if (QW == 256u) {           // the two rows are adjacent
+                        bulk_g2s_s(sbs + kPairE, z4 + off0, 8192u, fb);
+                        bulk_g2s_s(sbs + kPairE + 8192, m4 + off0, 8192u, fb);
+                        bulk_g2s_s(sbs + kPairE + 16384, v4 + off0, 8192u, fb);
+                    } else {
+                        bulk_g2s_s(sbs + kPairE, z4 + off0, 4096u, fb);
+                        bulk_g2s_s(sbs + kPairE + 4096, z4 + off1, 4096u, fb);
+                        bulk_g2s_s(sbs + kPairE + 8192, m4 + off0, 4096u, fb);
+                        bulk_g2s_s(sbs + kPairE + 12288, m4 + off1, 4096u, fb);
+                        bulk_g2s_s(sbs + kPairE + 16384, v4 + off0, 4096u, fb);
+                        bulk_g2s_s(sbs + kPairE + 20480, v4 + off1, 4096u, fb);
+                    }
+                    if (ebytes) bulk_g2s_s(sbs, Ech + (size_t)k0 * 32u, ebytes, fb);
+                    advance();
+                    continue;
+                }
+                for (int slot = 0; slot < (has1 ? 2 : 1); ++slot) {
+                    const int32_t kb = slot ? k2 : k0, kn = slot ? k3 : k1, ke = slot ? k4 : k2;
+                    const bool hub = slot ? hub1 : hub0;
+                    const int32_t pieces = hub ? 1 : max(1, (ke - kb + kPairRows - 1) / kPairRows);
+                    const size_t off = slot ? off1 : off0;
+                    for (int32_t pc = 0; pc < pieces; ++pc) {
+                        const uint32_t sbs = acquire(), fb = full_s + 8u * st;
+                        const int32_t r0 = hub ? kb : kb + pc * kPairRows;
+                        const int32_t r1 = hub ? kb : min(ke, r0 + kPairRows);
+                        const bool last = pc == pieces - 1 && slot == (has1 ? 1 : 0);
+                        hdr[st] = PairHdr{v0, r0, r1, r1, kn, kn};
+                        hflags[st] = (pc == 0 ? kPfFirst : 0) | (last ? kPfLast : 0) | (hub ? kPfHub : 0) |
+                                     (slot ? kPfSlot1 : 0) | pins;
+                        const uint32_t ebytes = (uint32_t)(r1 - r0) * 128u;
+                        mbar_arrive_expect_tx_s(fb, (pc == 0 ? 3u * 4096u : 0u) + ebytes);
+                        if (pc == 0) {
+                            const uint32_t zb = sbs + kPairE + (uint32_t)slot * 4096u;
+                            bulk_g2s_s(zb, z4 + off, 4096u, fb);
+                            bulk_g2s_s(zb + 8192, m4 + off, 4096u, fb);
+                            bulk_g2s_s(zb + 16384, v4 + off, 4096u, fb);
+                        }
+                        if (ebytes) bulk_g2s_s(sbs, Ech + (size_t)r0 * 32u, ebytes, fb);
+                        advance();
+                    }
+                }
+            }
+        }
+    } else {
+    // ------------------------------------------------------------------ consumer warps
+    const int32_t s = ctrl->t + 1;
+    const float2 ac = p.adam_consts[s];
+    bool bad = false;
+    for (int32_t i = blockIdx.x * 256 + tid; i < p.b_pad; i += gridDim.x * 256) {   // next sweep's counters
+        if (p.clear_a) p.clear_a[i] = 0;
+        if (p.clear_b) p.clear_b[i] = 0;
+    }
+    const int sh = tid & 7;
+    int st = 0;
+    uint32_t ph = 0;
+    for (uint32_t item = blockIdx.x; item < rm.items; item += gridDim.x) {
+        const uint32_t pr = div_cpr(rm, item);
+        const uint32_t q = (item - pr * rm.cpr) * 256u + (uint32_t)tid;
+        const int32_t v0 = 2 * (int32_t)pr;
+        float4 z0, m0, w0, z1, m1, w1;
+        int32_t G0[4] = {0, 0, 0, 0}, G1[4] = {0, 0, 0, 0};
+        int32_t flags = 0;
+        do {
+            mbar_wait_s(full_s + 8u * st, ph);
+            const PairHdr h = hdr[st];
+            flags = hflags[st];
+            const uint8_t *sb = smem + st * kPairStageBytes;
+            const float4 *za = reinterpret_cast<const float4 *>(sb + kPairE);
+            const uint32_t *srow = reinterpret_cast<const uint32_t *>(sb) + (tid >> 3);
+            if (flags & kPfPair) {
+                z0 = za[tid];       z1 = za[256 + tid];
+                m0 = za[512 + tid]; m1 = za[768 + tid];
+                w0 = za[1024 + tid]; w1 = za[1280 + tid];
+                const int32_t n0 = h.split - h.r0, n1 = h.r1 - h.split;
+                count_piece(srow, n0, sh, G0);
+                count_piece(srow + n0 * 32, n1, sh, G1);
+                const int32_t g0 = h.split - h.neg0, g1 = h.r1 - h.neg1;   // negative rows (complemented)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    G0[j] -= g0;
+                    G1[j] -= g1;
+                }
+            } else {
+                const bool slot1 = (flags & kPfSlot1) != 0;
+                if (flags & kPfFirst) {
+                    if (slot1) {
+                        z1 = za[256 + tid]; m1 = za[768 + tid]; w1 = za[1280 + tid];
+                    } else {
+                        z0 = za[tid]; m0 = za[512 + tid]; w0 = za[1024 + tid];
+                    }
+                }
+                int32_t Gt[4] = {0, 0, 0, 0};
+                if (flags & kPfHub) {
+                    hub_signal(c, partial, QW, c.hub_of_var[v0 + (slot1 ? 1 : 0)], q, Gt);
+                } else {
+                    const int32_t nrows = h.r1 - h.r0, nneg = h.r1 - max(h.neg0, h.r0);
+                    count_piece(srow, nrows, sh, Gt);
+                    if (nneg > 0) {
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) Gt[j] -= nneg;
+                    }
+                }
+                if (slot1) {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) G1[j] += Gt[j];
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) G0[j] += Gt[j];
+                }
+            }
+            mbar_arrive_s(empty_s + 8u * st);
+            if (++st == kPairStages) {
+                st = 0;
+                ph ^= 1u;
+            }
+        } while (!(flags & kPfLast));
+        const int64_t bq = p.b0 + 4 * (int64_t)q;
+        uint32_t xn, rn;
+        float g1o[4];
+        if (kPins && (flags & kPfPin0))
+            quad_update<kTau1, kAdam, true>(p, ac, v0, bq, s, G0, z0, m0, w0, xn, rn, g1o, bad);
+        else
+            quad_update<kTau1, kAdam, false>(p, ac, v0, bq, s, G0, z0, m0, w0, xn, rn, g1o, bad);
+        size_t idx = (size_t)v0 * QW + q;
+        z4[idx] = z0;
+        m4[idx] = m0;
+        v4[idx] = w0;
+        uint32_t xw = pack_quads(xn, lane), rw = pack_quads(rn, lane);
+        if ((lane & 7) == 0) {
+            X[xr_at(v0, (int32_t)(q >> 3), p.W)] = xw;
+            R[xr_at(v0, (int32_t)(q >> 3), p.W)] = rw;
+        }
+        if (flags & kPfHas1) {             // uniform over the CTA
+            if (kPins && (flags & kPfPin1))
+                quad_update<kTau1, kAdam, true>(p, ac, v0 + 1, bq, s, G1, z1, m1, w1, xn, rn, g1o, bad);
+            else
+                quad_update<kTau1, kAdam, false>(p, ac, v0 + 1, bq, s, G1, z1, m1, w1, xn, rn, g1o, bad);
+            idx += QW;
+            z4[idx] = z1;
+            m4[idx] = m1;
+            v4[idx] = w1;
+            xw = pack_quads(xn, lane);
+            rw = pack_quads(rn, lane);
+            if ((lane & 7) == 0) {
+                X[xr_at(v0 + 1, (int32_t)(q >> 3), p.W)] = xw;
+                R[xr_at(v0 + 1, (int32_t)(q >> 3), p.W)] = rw;
+            }
+        }
+    }
+    if (bad) atomicOr(&ctrl->nonfinite, 1);
+    }                                      // consumer warps
+    last_cta_tick(ctrl);
+}
+
 // --------------------------------------------- a6: hub partial sums, TMA-staged (W % 32 == 0)
 // Item = (hub chunk of <= kHubChunk = 256 occurrences, 1024-member chunk): the chunk's E
 // rows (<= 32 KB, contiguous) arrive by one bulk copy; per quad the signed count
@@ -1115,6 +1367,20 @@ template <bool a, bool b, bool c, bool d>
 struct SelTma {
     static constexpr UpdKernel k = k_update_tma<a, b, c, d, false>;
 };
+using PairKernel = void (*)(DevCnf, StepParams, RowMap, float4 *, float4 *, float4 *, uint32_t *, uint32_t *,
+                            const uint32_t *, const short4 *, Ctrl *);
+static PairKernel pick_pair(int variant)   // variant bits: 4 tau1, 2 adam, 1 pins
+{
+    static const PairKernel table[8] = {k_update_pair<false, false, false>, k_update_pair<false, false, true>,
+                                        k_update_pair<false, true, false>,  k_update_pair<false, true, true>,
+                                        k_update_pair<true, false, false>,  k_update_pair<true, false, true>,
+                                        k_update_pair<true, true, false>,   k_update_pair<true, true, true>};
+    return table[variant & 7];
+}
+#ifndef GALOIS_UPD_PAIR
+#define GALOIS_UPD_PAIR 1
+#endif
+
 template <bool a, bool b, bool c, bool d>
 struct SelTmaSliced {
     static constexpr UpdKernel k = k_update_tma<a, b, c, d, true>;
@@ -1176,6 +1442,10 @@ cudaError_t configure_kernels()
                                  kTmaSmem);
         if (e != cudaSuccess) return e;
     }
+    for (int v = 0; v < 8; ++v) {
+        e = cudaFuncSetAttribute((const void *)pick_pair(v), cudaFuncAttributeMaxDynamicSharedMemorySize, kPairSmem);
+        if (e != cudaSuccess) return e;
+    }
     e = cudaFuncSetAttribute((const void *)k_hub_partial_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              kHubStages * kHubStageBytes);
     if (e != cudaSuccess) return e;
@@ -1190,7 +1460,11 @@ void update_st(const DevCnf &c, const StepParams &p, float *z, float *m, float *
     const RowMap rm = make_rowmap((uint32_t)p.n, (uint32_t)p.b_pad);
     const int variant = (dbg_G ? 8 : 0) | (p.inv_tau == 1.0f ? 4 : 0) | (p.optimizer == 0 ? 2 : 0) |
                         (p.pin_rank ? 1 : 0);
-    if (use_tma_update(p.W)) {
+    if (GALOIS_UPD_PAIR && use_tma_update(p.W) && !dbg_G && !use_sliced(c)) {
+        const RowMap rp = make_rowmap(((uint32_t)p.n + 1u) / 2u, (uint32_t)p.b_pad);
+        pick_pair(variant)<<<item_grid(rp, kPairCtasPerSm), 256 + 32, kPairSmem, st>>>(
+            c, p, rp, (float4 *)z, (float4 *)m, (float4 *)v, X, R, E, partial, ctrl);
+    } else if (use_tma_update(p.W)) {
         // smem attribute set by configure_kernels()
         const UpdKernel k = use_sliced(c) ? pick<SelTmaSliced>(variant) : pick<SelTma>(variant);
         k<<<item_grid(rm, kTmaCtasPerSm), 256 + 32, kTmaSmem, st>>>(c, p, rm, (float4 *)z, (float4 *)m, (float4 *)v, X, R, E,

@@ -110,6 +110,24 @@ def test_chunk_loop_wide_tiles_stepwise(G):
     cnf.free()
 
 
+@pytest.mark.parametrize("batch", [1024, 2048])
+def test_pair_update_odd_n_stepwise(G, batch):
+    """The production update over variable pairs (k_update_pair): an odd variable count
+    (the last pair has one variable), hubs, degrees past one 56-row piece (such pairs go
+    variable by variable) and pairs that travel as one stage; B = 1024 stages the two rows
+    of a pair with one copy per array, B = 2048 with two. Sampled members, 4 steps."""
+    inst = I.industrial(2501, 30_000, 21, occ_exp=0.9)
+    deg = I.degrees(inst)
+    assert inst.n % 2 == 1 and (deg > 256).any() and ((deg > 56) & (deg <= 256)).any()
+    cnf = G.Cnf.from_instance(inst)
+    eng = G.Engine(cnf, batch, 20, 0.5, 0)
+    members = (0, 3, 511, 700, batch - 1)
+    rep = parity.stepwise_sampled(G, inst, eng, members, 4, seed=0)
+    assert rep["compared"] >= len(members) * 4 - 2, rep
+    eng.free()
+    cnf.free()
+
+
 def test_c2_lanes_stepwise(G):
     """configs[1] (B = 4096) split into the bench's 4 lanes (4 streams): sampled members of
     every lane, 4 steps."""
