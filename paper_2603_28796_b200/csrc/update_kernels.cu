@@ -688,9 +688,18 @@ __global__ void __launch_bounds__(256 + 32, kTmaCtasPerSm) k_update_tma(DevCnf c
 // pieces of kPairRows rows as in k_update_tma (flag 64: the stage is about the second
 // variable). Non-debug, non-sliced instantiations only (the launcher keeps k_update_tma
 // for those); same per-quad arithmetic (quad_update), so iterates are bit-identical.
-constexpr int kPairRows = 56;                        // <= 7 rows per thread: count_rows_sliced<3>
-constexpr int kPairStages = 3;
-constexpr int kPairCtasPerSm = 2;
+#ifndef GALOIS_PAIR_ROWS
+#define GALOIS_PAIR_ROWS 56
+#endif
+constexpr int kPairRows = GALOIS_PAIR_ROWS;          // <= 7 rows per thread: count_rows_sliced<3>
+#ifndef GALOIS_PAIR_STAGES
+#define GALOIS_PAIR_STAGES 3
+#endif
+#ifndef GALOIS_PAIR_CTAS
+#define GALOIS_PAIR_CTAS 2
+#endif
+constexpr int kPairStages = GALOIS_PAIR_STAGES;
+constexpr int kPairCtasPerSm = GALOIS_PAIR_CTAS;
 constexpr int kPairE = kPairRows * 128;
 constexpr int kPairStageBytes = kPairE + 3 * 8192;   // E rows + z, m, v of two variables
 constexpr int kPairSmem = kPairStages * kPairStageBytes;
