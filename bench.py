@@ -498,7 +498,9 @@ def main():
                "measured_dram_gbs": (sum(fb_dram) / (fb_ms / 1e3) / 1e9) if fb_ms and all(fb_dram) else None,
                "measured_frac": (sum(fb_dram) / (fb_ms / 1e3) / 1e9 / peak) if fb_ms and all(fb_dram) else None,
                "measured_source": "profiles/ncu_traffic.json (dram__bytes_read.sum + dram__bytes_write.sum per launch)"}
-    KNAME = {"update": "k_update_tma (fused signal reduction + Adam + round + sample)",
+    KNAME = {"update": ("k_update_tma<kSliced> (fused signal reduction + Adam + round + sample)"
+                        if L >= 48 * n else
+                        "k_update_pair (fused signal reduction + Adam + round + sample, two variables per stage)"),
              "forward": "k_sweep (clause forward of X_s fused with the exact check of R_{s-1})",
              "hub_partial": "k_hub_partial_tma (signal partial sums of hub variables)"}
     ws = 12 * n * b_pad + L * b_pad // 8 + n * b_pad // 4     # z, m, v + E + X, R
