@@ -3,7 +3,7 @@
     compute-sanitizer --tool memcheck|racecheck|synccheck|initcheck python tools/sanitize.py [part ...]
 
 parts: small (k_small_run, cooperative grid barrier: C1 through run()), tma (the
-TMA-pipelined update, sweep, hub partials, k_extract: 2048 members), lanes (2 lanes on
+TMA-pipelined updates k_update_pair / k_update_tma, sweep, hub partials, k_extract), lanes (2 lanes on
 their own streams, CUDA graph chunks), loop (k_sweep<kLoop>), v4 (b_pad < 1024 sweep and
 k_update_st), soft (SOFT mode), select (theta_sel / pool / top-|S| / cube variables),
 tseitin (device normalisation), window (f4 sub-batching). Default: all.
@@ -55,6 +55,15 @@ def part_tma():
     e = G.Engine(cnf, 2048, 3, 0.5, 1, debug=True)
     e.step()
     e.get_grad()
+    e.free()
+    cnf.free()
+    # k_update_pair with adjacent rows (B = 1024), an odd n (a lone last variable), hubs and
+    # pairs that go variable by variable
+    inst = I.industrial(2501, 30_000, 21, occ_exp=0.9)
+    cnf = G.Cnf.from_instance(inst)
+    e = G.Engine(cnf, 1024, 3, 0.5, 2)
+    e.enqueue(3)
+    e.best_assignment()
     e.free()
     cnf.free()
 
