@@ -36,7 +36,7 @@ if has launches; then
 fi
 if has full; then
     for W in C2 C4; do
-        for K in k_update_tma k_sweep k_hub_partial_tma; do
+        for K in k_update_pair k_update_tma k_sweep k_hub_partial_tma; do
             timeout 900 $NCU --set full --clock-control none --import-source on -k regex:$K -s 20 -c 1 \
                 -o "$OUT/full_${W}_$K" python bench.py --workload $W --steps 24 --warmup 3 --lanes 1 --no-cpu-baseline \
                 --no-e2e > "$OUT/full_${W}_$K.log" 2>&1

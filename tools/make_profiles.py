@@ -56,7 +56,7 @@ def table(seq, split=None):
     return "\n".join(out), agg
 
 
-main = ("k_sweep<1, 1, 0, 0>", "k_update_tma<0, 1, 1, 0, 0>")
+main = ("k_sweep<1, 1, 0, 0>", "k_update_pair<1, 1, 0>")
 c2 = seqof(os.path.join(SRC, "launches_C2.csv"))
 c4 = seqof(os.path.join(SRC, "launches_C4.csv"))
 t2, agg2 = table(c2, (28, main))
@@ -101,7 +101,7 @@ parts = [f"# Round {int(RND[1:])} — ncu --set full of the step kernels (one la
 for W in ("C2", "C4"):
     parts += [f"## {W}", ""]
     first = True
-    for K in ("k_update_tma", "k_sweep", "k_hub_partial_tma"):
+    for K in ("k_update_pair", "k_update_tma", "k_sweep", "k_hub_partial_tma"):
         rep = os.path.join(SRC, f"full_{W}_{K}.ncu-rep")
         if not os.path.exists(rep):
             continue

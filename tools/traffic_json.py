@@ -14,7 +14,7 @@ import os
 import subprocess
 import sys
 
-CLASS = {"k_update_tma": "update", "k_sweep": "forward", "k_hub_partial_tma": "hub_partial"}
+CLASS = {"k_update_tma": "update", "k_update_pair": "update", "k_sweep": "forward", "k_hub_partial_tma": "hub_partial"}
 UNITS = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 
 
@@ -49,6 +49,8 @@ def main():
         rec = launch_bytes(rep)
         if rec is None or kern not in CLASS:
             continue
+        if CLASS[kern] in out.get(wl, {}) and kern == "k_update_tma":
+            continue                        # the pair kernel's capture is the production one
         out.setdefault(wl, {})[CLASS[kern]] = rec
     path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "ncu_traffic.json")
     with open(path, "w") as f:
