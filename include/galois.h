@@ -180,9 +180,9 @@ int galois_engine_set_cubes(galois_engine *eng, int32_t d, const int32_t *vars);
  * The communicator is initialised (collectively) at the first step.
  * Exchange (row a9; mechanism ours, the paper's 2 -> 8 GPU split is Table 3):
  * every rank keeps its own best record and the winner's bits exactly as on one rank; after
- * each check an 8-byte MIN all-reduce of (u << 32 | global member) and the global record
- * update run on an engine-owned exchange stream, overlapping the update of the same step;
- * the main stream joins it before the next sweep. The global record (u*, t*, b*), its bits
+ * each check an 8-byte MIN all-reduce of (u << 32 | global member) runs on an engine-owned
+ * exchange stream, overlapping the update of the same step; the main stream joins it and
+ * folds it into the global record before the next sweep. The global record (u*, t*, b*), its bits
  * (broadcast from the owner rank, b* / b_per), the unsat counts and steps_done are exactly
  * the single-GPU result; a rank that did not hold the SAT member may run one update past t*
  * (its iterate then is one step ahead; no further check runs). All ranks must make the same

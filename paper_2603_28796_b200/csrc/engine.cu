@@ -544,9 +544,9 @@ struct galois_engine {
     int32_t rank = 0, world = 1;
     unsigned char nccl_id[128] = {0};
     bool use_comm = false;         // NCCL path (world > 1, or a 1-rank communicator for tests)
-    // NCCL exchange off the critical path: the MIN all-reduce and k_gfinalize of a check run
-    // on `xstream` (forked after the checking sweep by ev_chk) while the update runs; the
-    // main stream joins ev_x before its next sweep or result read (x_pending)
+    // NCCL exchange off the critical path: the MIN all-reduce of a check runs on `xstream`
+    // (forked after the checking sweep by ev_chk) while the update runs; the main stream
+    // joins ev_x and runs k_gfinalize before its next sweep or result read (x_pending)
     cudaStream_t xstream = nullptr;
     cudaEvent_t ev_chk = nullptr, ev_x = nullptr;
     bool x_pending = false;
@@ -903,7 +903,7 @@ static BestArgs best_args(const galois_engine *e)
     ba.unsat_last = e->unsat_last;
     ba.b_loc = e->b_loc;
     ba.b0 = e->b0;
-    ba.finalize = 1;                  // this rank's record (with NCCL the global one follows on xstream)
+    ba.finalize = 1;                  // this rank's record (with NCCL the global one follows at the join)
     // small instances: the sweep's last CTA also copies the winner's bits (n loads in one
     // CTA); large ones launch the grid-wide k_extract instead
     ba.best_bits = e->best_bits;
@@ -919,12 +919,17 @@ static int exchange_join(galois_engine *e)
 {
     if (!e->x_pending) return GALOIS_OK;
     ENG_CUDA(e, cudaStreamWaitEvent(e->stream, e->ev_x, 0));
+    // the global record and stop flag are folded in on the MAIN stream: the update kernels
+    // that overlapped the all-reduce read ctrl->stopped, so no other stream may write it
+    // while they run (a flag flipping mid-launch would stop only part of a grid)
+    e->timed(3, [&] { launch::gfinalize(e->ctrl, e->stream); });
     e->x_pending = false;
     return GALOIS_OK;
 }
 
-// a9 with NCCL: fork the check's key to the exchange stream, MIN all-reduce it over the
-// ranks and fold it into the global record there; the main stream continues with the update.
+// a9 with NCCL: fork the check's key to the exchange stream and MIN all-reduce it over the
+// ranks there; the main stream continues with the update and folds the result into the
+// global record (k_gfinalize) when it joins, before its next sweep or result read.
 static int exchange_fork(galois_engine *e)
 {
     ENG_CUDA(e, cudaEventRecord(e->ev_chk, e->stream));
@@ -932,7 +937,6 @@ static int exchange_fork(galois_engine *e)
     std::string why;
     if (!e->comm.allreduce_min_u64(&e->ctrl->key_local, &e->ctrl->key_global, e->xstream, &why))
         return poison(e, GALOIS_E_NCCL, why);
-    e->timed(3, [&] { launch::gfinalize(e->ctrl, e->xstream); }, e->xstream);
     ENG_CUDA(e, cudaEventRecord(e->ev_x, e->xstream));
     e->x_pending = true;
     return GALOIS_OK;
