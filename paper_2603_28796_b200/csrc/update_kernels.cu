@@ -304,16 +304,13 @@ __device__ __forceinline__ const uint32_t *e_column(const uint32_t *E, int32_t L
 // tau = 1 rewrites of Eq.3 with no logarithm: with (u, ub = 1 - u) and e = exp(-|z|),
 // sigma(z + logit u) sigma(-(z + logit u)) = u ub e / d^2 with d = u + ub e (z >= 0) or
 // ub + u e (z < 0); and [z + logit u >= 0] <=> u >= ub e (z >= 0) or u e >= ub (z < 0).
-__device__ __forceinline__ bool sample_bit_tau1(float z, float2 uu, float e)
-{
-    return z >= 0.0f ? (uu.x >= uu.y * e) : (uu.x * e >= uu.y);
-}
 
-// a7 for one quad: gradient, optimiser, rounding, next sample. Returns the nibbles.
+// a7 for one quad: gradient, optimiser, rounding, next sample. Returns the four members'
+// sample and rounding bits as predicates (the TMA kernels ballot them directly).
 template <bool kTau1, bool kAdam, bool kPins>
-__device__ __forceinline__ void quad_update(const StepParams &p, float2 ac, int32_t v, int64_t bq, int32_t s,
-                                            const int32_t G[4], float4 &z, float4 &m, float4 &vv, uint32_t &xn,
-                                            uint32_t &rn, float g1o[4], bool &bad)
+__device__ __forceinline__ void quad_update_bits(const StepParams &p, float2 ac, int32_t v, int64_t bq, int32_t s,
+                                                 const int32_t G[4], float4 &z, float4 &m, float4 &vv,
+                                                 bool (&xbit)[4], bool (&rbit)[4], float g1o[4], bool &bad)
 {
     const uint4 wn4 = philox4x32_10(make_uint4((uint32_t)v, (uint32_t)(bq >> 2), (uint32_t)s, 1u), p.keys);
     const uint4 wx4 = philox4x32_10(make_uint4((uint32_t)v, (uint32_t)(bq >> 2), (uint32_t)(s + 1), 1u), p.keys);
@@ -321,7 +318,6 @@ __device__ __forceinline__ void quad_update(const StepParams &p, float2 ac, int3
     const uint32_t wx[4] = {wx4.x, wx4.y, wx4.z, wx4.w};
     float zz[4] = {z.x, z.y, z.z, z.w}, mm[4] = {m.x, m.y, m.z, m.w}, ww[4] = {vv.x, vv.y, vv.z, vv.w};
     const int pin_r = kPins ? (int)p.pin_rank[v] : -1;       // cube pin of this variable
-    xn = rn = 0;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
         float g1;
@@ -354,20 +350,49 @@ __device__ __forceinline__ void quad_update(const StepParams &p, float2 ac, int3
         } else {
             rb = zz[j] >= 0.0f;
             if (kTau1) {
+                // [z + logit u >= 0] with e = exp(-|z|): u - ub e >= 0 (z >= 0) or u e - ub >= 0
+                // (z < 0); as one FMA g = x - e y with (x, y) = (u, ub) or (ub, u), and the
+                // z < 0 case read as -g >= 0 (the fma of negated operands is exactly -(u e - ub))
                 const float2 uu = unif_pair(wx[j]);
                 const float e = exp_neg_abs(zz[j]);
-                xb = (rb && uu.x >= uu.y * e) || (!rb && uu.x * e >= uu.y);
+                const float g = fmaf(-e, rb ? uu.y : uu.x, rb ? uu.x : uu.y);
+                const float h = rb ? g : -g;          // one FSEL: the decision stays a predicate
+                xb = h >= 0.0f;
             } else {
                 xb = zz[j] + logistic_from_word(wx[j]) >= 0.0f;
             }
         }
-        rn |= rb ? (1u << j) : 0u;
-        xn |= xb ? (1u << j) : 0u;
+        rbit[j] = rb;
+        xbit[j] = xb;
     }
     bad |= !isfinite((zz[0] + zz[1]) + (zz[2] + zz[3]));   // NaN/Inf in any lane survives the sum
     z = make_float4(zz[0], zz[1], zz[2], zz[3]);
     m = make_float4(mm[0], mm[1], mm[2], mm[3]);
     vv = make_float4(ww[0], ww[1], ww[2], ww[3]);
+}
+
+// The same with the bits as nibbles (bit j = member j), for callers whose lanes do not all
+// take part (k_update_st's ragged rows, k_small_run).
+template <bool kTau1, bool kAdam, bool kPins>
+__device__ __forceinline__ void quad_update(const StepParams &p, float2 ac, int32_t v, int64_t bq, int32_t s,
+                                            const int32_t G[4], float4 &z, float4 &m, float4 &vv, uint32_t &xn,
+                                            uint32_t &rn, float g1o[4], bool &bad)
+{
+    bool xb[4], rb[4];
+    quad_update_bits<kTau1, kAdam, kPins>(p, ac, v, bq, s, G, z, m, vv, xb, rb, g1o, bad);
+    xn = (xb[0] ? 1u : 0u) | (xb[1] ? 2u : 0u) | (xb[2] ? 4u : 0u) | (xb[3] ? 8u : 0u);
+    rn = (rb[0] ? 1u : 0u) | (rb[1] ? 2u : 0u) | (rb[2] ? 4u : 0u) | (rb[3] ? 8u : 0u);
+}
+
+// The 32-bit word of this lane's 8-lane group from every lane's four member bits (all 32
+// lanes take part): pack_quads without building the nibble first.
+__device__ __forceinline__ uint32_t pack_bits(const bool (&b)[4], int lane)
+{
+    const uint32_t b0 = __ballot_sync(0xffffffffu, b[0]), b1 = __ballot_sync(0xffffffffu, b[1]);
+    const uint32_t b2 = __ballot_sync(0xffffffffu, b[2]), b3 = __ballot_sync(0xffffffffu, b[3]);
+    const uint32_t k = (uint32_t)(lane >> 3) & 3u;
+    const uint32_t sel = k | ((k + 4u) << 4);
+    return __byte_perm(__byte_perm(b0, b1, sel), __byte_perm(b2, b3, sel), 0x5410);
 }
 
 __device__ __forceinline__ void hub_signal(const DevCnf &c, const short4 *__restrict__ partial, uint32_t QW,
@@ -901,32 +926,32 @@ __global__ void __launch_bounds__(256 + 32, kPairCtasPerSm)
             }
         } while (!(flags & kPfLast));
         const int64_t bq = p.b0 + 4 * (int64_t)q;
-        uint32_t xn, rn;
+        bool xb[4], rb[4];
         float g1o[4];
         if (kPins && (flags & kPfPin0))
-            quad_update<kTau1, kAdam, true>(p, ac, v0, bq, s, G0, z0, m0, w0, xn, rn, g1o, bad);
+            quad_update_bits<kTau1, kAdam, true>(p, ac, v0, bq, s, G0, z0, m0, w0, xb, rb, g1o, bad);
         else
-            quad_update<kTau1, kAdam, false>(p, ac, v0, bq, s, G0, z0, m0, w0, xn, rn, g1o, bad);
+            quad_update_bits<kTau1, kAdam, false>(p, ac, v0, bq, s, G0, z0, m0, w0, xb, rb, g1o, bad);
         size_t idx = (size_t)v0 * QW + q;
         z4[idx] = z0;
         m4[idx] = m0;
         v4[idx] = w0;
-        uint32_t xw = pack_quads(xn, lane), rw = pack_quads(rn, lane);
+        uint32_t xw = pack_bits(xb, lane), rw = pack_bits(rb, lane);
         if ((lane & 7) == 0) {
             X[xr_at(v0, (int32_t)(q >> 3), p.W)] = xw;
             R[xr_at(v0, (int32_t)(q >> 3), p.W)] = rw;
         }
         if (flags & kPfHas1) {             // uniform over the CTA
             if (kPins && (flags & kPfPin1))
-                quad_update<kTau1, kAdam, true>(p, ac, v0 + 1, bq, s, G1, z1, m1, w1, xn, rn, g1o, bad);
+                quad_update_bits<kTau1, kAdam, true>(p, ac, v0 + 1, bq, s, G1, z1, m1, w1, xb, rb, g1o, bad);
             else
-                quad_update<kTau1, kAdam, false>(p, ac, v0 + 1, bq, s, G1, z1, m1, w1, xn, rn, g1o, bad);
+                quad_update_bits<kTau1, kAdam, false>(p, ac, v0 + 1, bq, s, G1, z1, m1, w1, xb, rb, g1o, bad);
             idx += QW;
             z4[idx] = z1;
             m4[idx] = m1;
             v4[idx] = w1;
-            xw = pack_quads(xn, lane);
-            rw = pack_quads(rn, lane);
+            xw = pack_bits(xb, lane);
+            rw = pack_bits(rb, lane);
             if ((lane & 7) == 0) {
                 X[xr_at(v0 + 1, (int32_t)(q >> 3), p.W)] = xw;
                 R[xr_at(v0 + 1, (int32_t)(q >> 3), p.W)] = rw;
