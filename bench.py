@@ -128,8 +128,8 @@ def l2_roofline(per_kernel, dom, gather_bytes, xr_bytes, names):
     """Roofline of a dominant clause sweep whose X/R rows are L2-resident (C3b): its row
     gathers per launch over the launch time, against the measured L2 random-gather
     bandwidth (profiles/l2_gather_peak.json, tools/randbw.cu). None otherwise."""
-    if dom != "forward" or xr_bytes > 64e6 or dom not in per_kernel:
-        return None
+    if dom != "forward" or xr_bytes > 64e6 or dom not in per_kernel or per_kernel[dom]["ms_per_launch"] < 0.05:
+        return None                          # (C1: a launch-bound 7 us sweep has no bandwidth bound)
     path = os.path.join(ROOT, "profiles", "l2_gather_peak.json")
     if not os.path.exists(path):
         return None
