@@ -58,9 +58,15 @@ __global__ void __launch_bounds__(256) k_init(StepParams p, float4 *__restrict__
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             const int pb = pinned_bit(p, v, bq + j);
-            const float ell = logistic_from_word(wv[j]);
-            const uint32_t xb = pb >= 0 ? (uint32_t)pb : (zz[j] + ell >= 0.0f ? 1u : 0u);
-            const uint32_t rb = pb >= 0 ? (uint32_t)pb : (zz[j] >= 0.0f ? 1u : 0u);
+            // X_1 = [z0 + logit u >= 0] (the sign of a = (z0 + ell) / tau does not depend on
+            // tau > 0), without a logarithm: with e = exp(-|z0|), u - ub e >= 0 (z0 >= 0)
+            // or u e - ub >= 0 (z0 < 0), as one FMA (the update's rewrite, update_kernels.cu)
+            const float2 uu = unif_pair(wv[j]);
+            const float e = exp_neg_abs(zz[j]);
+            const bool r0 = zz[j] >= 0.0f;
+            const float g = fmaf(-e, r0 ? uu.y : uu.x, r0 ? uu.x : uu.y);
+            const uint32_t xb = pb >= 0 ? (uint32_t)pb : ((r0 ? g : -g) >= 0.0f ? 1u : 0u);
+            const uint32_t rb = pb >= 0 ? (uint32_t)pb : (r0 ? 1u : 0u);
             xn |= xb << j;
             rn |= rb << j;
         }
