@@ -310,10 +310,9 @@ __device__ __forceinline__ const uint32_t *e_column(const uint32_t *E, int32_t L
 template <bool kTau1, bool kAdam, bool kPins>
 __device__ __forceinline__ void quad_update_bits(const StepParams &p, float2 ac, int32_t v, int64_t bq, int32_t s,
                                                  const int32_t G[4], float4 &z, float4 &m, float4 &vv,
-                                                 bool (&xbit)[4], bool (&rbit)[4], float g1o[4], bool &bad)
+                                                 bool (&xbit)[4], bool (&rbit)[4], float g1o[4], bool &bad,
+                                                 const uint4 wn4, const uint4 wx4)
 {
-    const uint4 wn4 = philox4x32_10(make_uint4((uint32_t)v, (uint32_t)(bq >> 2), (uint32_t)s, 1u), p.keys);
-    const uint4 wx4 = philox4x32_10(make_uint4((uint32_t)v, (uint32_t)(bq >> 2), (uint32_t)(s + 1), 1u), p.keys);
     const uint32_t wn[4] = {wn4.x, wn4.y, wn4.z, wn4.w};
     const uint32_t wx[4] = {wx4.x, wx4.y, wx4.z, wx4.w};
     float zz[4] = {z.x, z.y, z.z, z.w}, mm[4] = {m.x, m.y, m.z, m.w}, ww[4] = {vv.x, vv.y, vv.z, vv.w};
@@ -369,6 +368,21 @@ __device__ __forceinline__ void quad_update_bits(const StepParams &p, float2 ac,
     z = make_float4(zz[0], zz[1], zz[2], zz[3]);
     m = make_float4(mm[0], mm[1], mm[2], mm[3]);
     vv = make_float4(ww[0], ww[1], ww[2], ww[3]);
+}
+
+// The quad's two Philox draws: the noise of step s (gradient) and of step s + 1 (next sample).
+__device__ __forceinline__ uint4 quad_noise(const StepParams &p, int32_t v, int64_t bq, int32_t step)
+{
+    return philox4x32_10(make_uint4((uint32_t)v, (uint32_t)(bq >> 2), (uint32_t)step, 1u), p.keys);
+}
+
+template <bool kTau1, bool kAdam, bool kPins>
+__device__ __forceinline__ void quad_update_bits(const StepParams &p, float2 ac, int32_t v, int64_t bq, int32_t s,
+                                                 const int32_t G[4], float4 &z, float4 &m, float4 &vv,
+                                                 bool (&xbit)[4], bool (&rbit)[4], float g1o[4], bool &bad)
+{
+    quad_update_bits<kTau1, kAdam, kPins>(p, ac, v, bq, s, G, z, m, vv, xbit, rbit, g1o, bad,
+                                          quad_noise(p, v, bq, s), quad_noise(p, v, bq, s + 1));
 }
 
 // The same with the bits as nibbles (bit j = member j), for callers whose lanes do not all
@@ -713,6 +727,9 @@ __global__ void __launch_bounds__(256 + 32, kTmaCtasPerSm) k_update_tma(DevCnf c
 // pieces of kPairRows rows as in k_update_tma (flag 64: the stage is about the second
 // variable). Non-debug, non-sliced instantiations only (the launcher keeps k_update_tma
 // for those); same per-quad arithmetic (quad_update), so iterates are bit-identical.
+#ifndef GALOIS_PAIR_NOISE4
+#define GALOIS_PAIR_NOISE4 1
+#endif
 #ifndef GALOIS_PAIR_ROWS
 #define GALOIS_PAIR_ROWS 56
 #endif
@@ -928,10 +945,20 @@ __global__ void __launch_bounds__(256 + 32, kPairCtasPerSm)
         const int64_t bq = p.b0 + 4 * (int64_t)q;
         bool xb[4], rb[4];
         float g1o[4];
+#if GALOIS_PAIR_NOISE4
+        // the pair's four Philox calls drawn together: four independent round chains
+        const uint4 n0 = quad_noise(p, v0, bq, s), x0 = quad_noise(p, v0, bq, s + 1);
+        const uint4 n1 = quad_noise(p, v0 + 1, bq, s), x1 = quad_noise(p, v0 + 1, bq, s + 1);
+        if (kPins && (flags & kPfPin0))
+            quad_update_bits<kTau1, kAdam, true>(p, ac, v0, bq, s, G0, z0, m0, w0, xb, rb, g1o, bad, n0, x0);
+        else
+            quad_update_bits<kTau1, kAdam, false>(p, ac, v0, bq, s, G0, z0, m0, w0, xb, rb, g1o, bad, n0, x0);
+#else
         if (kPins && (flags & kPfPin0))
             quad_update_bits<kTau1, kAdam, true>(p, ac, v0, bq, s, G0, z0, m0, w0, xb, rb, g1o, bad);
         else
             quad_update_bits<kTau1, kAdam, false>(p, ac, v0, bq, s, G0, z0, m0, w0, xb, rb, g1o, bad);
+#endif
         size_t idx = (size_t)v0 * QW + q;
         z4[idx] = z0;
         m4[idx] = m0;
@@ -942,10 +969,17 @@ __global__ void __launch_bounds__(256 + 32, kPairCtasPerSm)
             R[xr_at(v0, (int32_t)(q >> 3), p.W)] = rw;
         }
         if (flags & kPfHas1) {             // uniform over the CTA
+#if GALOIS_PAIR_NOISE4
+            if (kPins && (flags & kPfPin1))
+                quad_update_bits<kTau1, kAdam, true>(p, ac, v0 + 1, bq, s, G1, z1, m1, w1, xb, rb, g1o, bad, n1, x1);
+            else
+                quad_update_bits<kTau1, kAdam, false>(p, ac, v0 + 1, bq, s, G1, z1, m1, w1, xb, rb, g1o, bad, n1, x1);
+#else
             if (kPins && (flags & kPfPin1))
                 quad_update_bits<kTau1, kAdam, true>(p, ac, v0 + 1, bq, s, G1, z1, m1, w1, xb, rb, g1o, bad);
             else
                 quad_update_bits<kTau1, kAdam, false>(p, ac, v0 + 1, bq, s, G1, z1, m1, w1, xb, rb, g1o, bad);
+#endif
             idx += QW;
             z4[idx] = z1;
             m4[idx] = m1;
