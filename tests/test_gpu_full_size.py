@@ -110,19 +110,25 @@ def test_chunk_loop_wide_tiles_stepwise(G):
     cnf.free()
 
 
-@pytest.mark.parametrize("batch", [1024, 2048])
-def test_pair_update_odd_n_stepwise(G, batch):
+@pytest.mark.parametrize("batch,pinned", [(1024, False), (2048, False), (1024, True)])
+def test_pair_update_odd_n_stepwise(G, batch, pinned):
     """The production update over variable pairs (k_update_pair): an odd variable count
     (the last pair has one variable), hubs, degrees past one 56-row piece (such pairs go
     variable by variable) and pairs that travel as one stage; B = 1024 stages the two rows
-    of a pair with one copy per array, B = 2048 with two. Sampled members, 4 steps."""
+    of a pair with one copy per array, B = 2048 with two. With `pinned`, cube pins on the
+    two highest-degree (hub) variables and on two low-degree ones whose pair partner is
+    free. Sampled members, 4 steps."""
     inst = I.industrial(2501, 30_000, 21, occ_exp=0.9)
     deg = I.degrees(inst)
     assert inst.n % 2 == 1 and (deg > 256).any() and ((deg > 56) & (deg <= 256)).any()
+    pins = ()
+    if pinned:
+        low = [v for v in range(0, inst.n - 1, 2) if 0 < deg[v] <= 8][:2]     # 0-based, even: pair heads
+        pins = tuple(sorted(set(I.top_degree_vars(inst, 2)) | {v + 1 for v in low}))
     cnf = G.Cnf.from_instance(inst)
-    eng = G.Engine(cnf, batch, 20, 0.5, 0)
+    eng = G.Engine(cnf, batch, 20, 0.5, 0, cubes=pins)
     members = (0, 3, 511, 700, batch - 1)
-    rep = parity.stepwise_sampled(G, inst, eng, members, 4, seed=0)
+    rep = parity.stepwise_sampled(G, inst, eng, members, 4, seed=0, cubes=pins)
     assert rep["compared"] >= len(members) * 4 - 2, rep
     eng.free()
     cnf.free()
