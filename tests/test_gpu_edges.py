@@ -88,6 +88,19 @@ def test_tiny_and_ragged_batches(G, batch):
     assert len(rep.resyncs) <= 2
 
 
+def test_local_slice_beyond_int32_is_rejected(G):
+    """A local batch slice of 2^31 members or more (the slice is indexed in int32) is
+    rejected with E_ARG at preparation, before any allocation."""
+    inst = I.random_ksat(30, 120, 3, 1)
+    cnf = G.Cnf.from_instance(inst)
+    eng = G.Engine(cnf, 2 ** 31 + 4096, 3, 0.5, 0)
+    with pytest.raises(G.GaloisError) as e:
+        eng.step()
+    assert e.value.code == G.E_ARG
+    eng.free()
+    cnf.free()
+
+
 def test_call_order_and_arguments(G):
     inst = I.random_ksat(30, 120, 3, 1)
     cnf = G.Cnf.from_instance(inst)
