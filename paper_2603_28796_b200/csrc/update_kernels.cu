@@ -350,13 +350,12 @@ __device__ __forceinline__ void quad_update_bits(const StepParams &p, float2 ac,
             rb = zz[j] >= 0.0f;
             if (kTau1) {
                 // [z + logit u >= 0] with e = exp(-|z|): u - ub e >= 0 (z >= 0) or u e - ub >= 0
-                // (z < 0); as one FMA g = x - e y with (x, y) = (u, ub) or (ub, u), and the
-                // z < 0 case read as -g >= 0 (the fma of negated operands is exactly -(u e - ub))
-                const float2 uu = unif_pair(wx[j]);
+                // (z < 0);
+                // with ub = 1 - u both cases are one FMA on u alone:
+                //   z >= 0: u - ub e = u (1 + e) - e;   z < 0: u e - ub = u (1 + e) - 1
+                const float u = unif_pair(wx[j]).x;
                 const float e = exp_neg_abs(zz[j]);
-                const float g = fmaf(-e, rb ? uu.y : uu.x, rb ? uu.x : uu.y);
-                const float h = rb ? g : -g;          // one FSEL: the decision stays a predicate
-                xb = h >= 0.0f;
+                xb = fmaf(u, 1.0f + e, rb ? -e : -1.0f) >= 0.0f;
             } else {
                 xb = zz[j] + logistic_from_word(wx[j]) >= 0.0f;
             }
