@@ -237,6 +237,11 @@ int galois_engine_set_graphs(galois_engine *eng, int32_t mode);
  * buffers, counters), for sizing sub_batch to a memory budget. */
 int galois_engine_bytes_per_member(const galois_cnf *cnf, int32_t mode, int64_t *bytes);
 
+/* Device memory available to a new engine on `device`: the driver's free bytes plus what
+ * the library's stream-ordered pool holds unused (freed engines and CNFs stay reserved in
+ * it for reuse). Divide by bytes_per_member for the largest resident sub_batch (f4). */
+int galois_device_free_bytes(int32_t device, int64_t *bytes);
+
 /* Test hook: also store the per-step clause signal G and gradient g1 (see get_grad). */
 int galois_engine_set_debug(galois_engine *eng, int32_t enable);
 
@@ -267,7 +272,13 @@ int galois_candidate_pool_size(const galois_cnf *cnf, double rho, int32_t *S);
  * rho = 0.0005) as DIMACS unit literals (+v if x = 1, else -v), ordered by descending
  * confidence, ties to the lower index.
  *   values [N][n] uint8 (may be NULL), confidence [N][n] float (may be NULL),
- *   units [N][S] int32 (may be NULL; S <= 4096), *S_out = S. E_ARG on bad sizes. */
+ *   units [N][S] int32 (may be NULL; S <= 2^20), *S_out = S. E_ARG on bad sizes
+ *   (N * n > 2^31 when values or confidence is requested).
+ * With values = confidence = NULL the pool is drawn over the n_orig original variables
+ * only (the same per-variable counters, so the same draws) in groups of candidates whose
+ * device scratch stays near 1.3 GB — the form for instances of the paper's largest size
+ * (P:559), where |S| = ceil(0.0005 n_orig) exceeds one CTA's shared-memory sort (4096
+ * keys) and is sorted in global memory instead. */
 int galois_candidate_pool(galois_engine *eng, int64_t global_b, int32_t N, double rho, uint64_t pool_seed,
                           uint8_t *values, float *confidence, int32_t *units, int32_t *S_out);
 

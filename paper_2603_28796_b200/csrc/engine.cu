@@ -55,10 +55,10 @@ cudaError_t configure_kernels();
 void select_member(const int32_t *counts, int32_t b_loc, int64_t b0, int32_t rule, unsigned long long *out,
                    cudaStream_t st);
 void gather_z(const float *z, int32_t n, int32_t b_pad, int32_t lb, float *out, cudaStream_t st);
-void pool(const float *zsel, int32_t n, int32_t N, float inv_tau, uint64_t pool_seed, uint8_t *x, float *conf,
-          cudaStream_t st);
+void pool(const float *zsel, int32_t n, int32_t k0, int32_t N, float inv_tau, uint64_t pool_seed, uint8_t *x,
+          float *conf, cudaStream_t st);
 void topk(const uint8_t *x, const float *conf, int32_t n, int32_t n_sel, int32_t N, int32_t S, int32_t *units,
-          cudaStream_t st);
+          uint64_t *gkeys, int32_t gstride, cudaStream_t st);
 void lowconf(const float *zsel, int32_t n, int32_t d, int32_t *vars, cudaStream_t st);
 int max_sorted();
 }  // namespace launch
@@ -506,6 +506,8 @@ extern "C" int galois_cnf_original_vars(const galois_cnf *c, int32_t *n_orig)
 }
 
 // Eq.11: |S| = max(1, ceil(rho n)) over the original variables.
+constexpr int32_t kMaxUnits = 1 << 20;   // |S| per candidate (paper rho = 0.0005: n < 2^31)
+
 static int32_t units_per_candidate(const galois_cnf *c, double rho)
 {
     return std::max<int32_t>(1, (int32_t)std::ceil(rho * (double)c->n_orig - 1e-9));
@@ -828,6 +830,25 @@ extern "C" int galois_engine_bytes_per_member(const galois_cnf *c, int32_t mode,
     else
         b += 4 * (int64_t)c->n + 4 * (int64_t)c->L + 4 * (1 + launch::soft_chunks());   // P, Es, lam_f
     *bytes = b;
+    return GALOIS_OK;
+}
+
+extern "C" int galois_device_free_bytes(int32_t device, int64_t *bytes)
+{
+    if (!bytes) return fail(GALOIS_E_ARG, "bytes is NULL");
+    int cur = 0;
+    CUDA_TRY(cudaGetDevice(&cur));
+    CUDA_TRY(cudaSetDevice(device));
+    size_t free_b = 0, total_b = 0;
+    cudaError_t ce = cudaMemGetInfo(&free_b, &total_b);
+    cudaMemPool_t pool;
+    uint64_t reserved = 0, used = 0;
+    if (ce == cudaSuccess) ce = cudaDeviceGetDefaultMemPool(&pool, device);
+    if (ce == cudaSuccess) ce = cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved);
+    if (ce == cudaSuccess) ce = cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
+    cudaSetDevice(cur);
+    CUDA_TRY(ce);
+    *bytes = (int64_t)free_b + (int64_t)(reserved > used ? reserved - used : 0);
     return GALOIS_OK;
 }
 
@@ -1843,30 +1864,46 @@ extern "C" int galois_candidate_pool(galois_engine *e, int64_t global_b, int32_t
     ENGINE_ENTRY(e);
     if (N < 1 || !(rho > 0.0 && rho <= 1.0)) return fail(GALOIS_E_ARG, "need N >= 1 and 0 < rho <= 1");
     if (int rc = prepare(e)) return rc;
-    const int32_t n = e->cnf->n;
+    const int32_t n = e->cnf->n, n_sel = e->cnf->n_orig;
     const int32_t S = units_per_candidate(e->cnf, rho);
-    if (S > launch::max_sorted()) return fail(GALOIS_E_ARG, "|S| exceeds 4096");
-    if ((int64_t)N * n > (int64_t(1) << 31)) return fail(GALOIS_E_ARG, "N * n too large");
+    if (S > kMaxUnits) return fail(GALOIS_E_ARG, "|S| exceeds 2^20 units per candidate");
+    const bool full = values || confidence;          // the [N][n] arrays go to the host
+    if (full && (int64_t)N * n > (int64_t(1) << 31)) return fail(GALOIS_E_ARG, "N * n too large");
     if (S_out) *S_out = S;
+    // Units only: the pool is drawn over the original variables alone (the units come from
+    // them; counters are per variable, so the values are those of the full draw) in
+    // groups of candidates whose scratch stays within ~1.25 GB.
+    const int32_t row = full ? n : n_sel;
+    const int32_t grp = full ? N : (int32_t)std::max<int64_t>(1, std::min<int64_t>(N, (int64_t(1) << 28) / row));
+    int32_t gstride = 1;                             // bitonic width >= S for the global-memory sort
+    while (gstride < S) gstride <<= 1;
+    const bool gsort = S > launch::max_sorted();
     ENG_CUDA(e, cudaStreamSynchronize(e->stream));
     float *d_z = nullptr, *d_c = nullptr;
     uint8_t *d_x = nullptr;
     int32_t *d_u = nullptr;
+    uint64_t *d_k = nullptr;
+    auto release = [&]() {
+        for (void *p : {(void *)d_z, (void *)d_c, (void *)d_x, (void *)d_u, (void *)d_k})
+            if (p) cudaFreeAsync(p, e->stream);
+    };
     if (int rc = tmp_alloc(e, &d_z, (size_t)n)) return rc;
-    if (int rc = tmp_alloc(e, &d_c, (size_t)N * n)) return rc;
-    if (int rc = tmp_alloc(e, &d_x, (size_t)N * n)) return rc;
-    if (int rc = tmp_alloc(e, &d_u, (size_t)N * S)) return rc;
-    if (int rc = member_z(e, global_b, d_z)) {
-        for (void *p : {(void *)d_z, (void *)d_c, (void *)d_x, (void *)d_u}) cudaFreeAsync(p, e->stream);
-        return rc;
+    if (int rc = tmp_alloc(e, &d_c, (size_t)grp * row)) return release(), rc;
+    if (int rc = tmp_alloc(e, &d_x, (size_t)grp * row)) return release(), rc;
+    if (int rc = tmp_alloc(e, &d_u, (size_t)N * S)) return release(), rc;
+    if (gsort && units)
+        if (int rc = tmp_alloc(e, &d_k, (size_t)grp * gstride)) return release(), rc;
+    if (int rc = member_z(e, global_b, d_z)) return release(), rc;
+    for (int32_t k0 = 0; k0 < N; k0 += grp) {
+        const int32_t g = std::min(grp, N - k0);
+        launch::pool(d_z, row, k0, g, (float)(1.0 / e->tau), pool_seed, d_x, d_c, e->stream);
+        if (units) launch::topk(d_x, d_c, row, n_sel, g, S, d_u + (size_t)k0 * S, d_k, gstride, e->stream);
     }
-    launch::pool(d_z, n, N, (float)(1.0 / e->tau), pool_seed, d_x, d_c, e->stream);
-    if (units) launch::topk(d_x, d_c, n, e->cnf->n_orig, N, S, d_u, e->stream);
     ENG_CUDA(e, cudaGetLastError());
     if (values) ENG_CUDA(e, cudaMemcpyAsync(values, d_x, (size_t)N * n, cudaMemcpyDeviceToHost, e->stream));
     if (confidence) ENG_CUDA(e, cudaMemcpyAsync(confidence, d_c, (size_t)N * n * 4, cudaMemcpyDeviceToHost, e->stream));
     if (units) ENG_CUDA(e, cudaMemcpyAsync(units, d_u, (size_t)N * S * 4, cudaMemcpyDeviceToHost, e->stream));
-    for (void *p : {(void *)d_z, (void *)d_c, (void *)d_x, (void *)d_u}) ENG_CUDA(e, cudaFreeAsync(p, e->stream));
+    release();
     ENG_CUDA(e, cudaStreamSynchronize(e->stream));
     return GALOIS_OK;
 }

@@ -69,7 +69,9 @@ __device__ uint64_t select_threshold(int32_t n, int32_t want, KeyOf key_of)
     return s_prefix;
 }
 
-// Collect the keys >= thr (exactly `count` of them) and sort them descending (bitonic).
+// Collect the keys >= thr (exactly `count` of them) and sort them descending (bitonic) in
+// s_keys: shared memory up to kMaxSorted keys, else a global scratch row of the block
+// (__syncthreads orders the block's global accesses as it does its shared ones).
 template <typename KeyOf>
 __device__ void collect_sorted_desc(int32_t n, int32_t count, uint64_t thr, KeyOf key_of, uint64_t *s_keys)
 {
@@ -132,13 +134,15 @@ __global__ void k_gather_z(const float *__restrict__ z, int32_t n, int32_t b_pad
         out[v] = z[(size_t)v * b_pad + lb];
 }
 
-__global__ void __launch_bounds__(256) k_pool(const float *__restrict__ zsel, int32_t n, int32_t N, float inv_tau,
-                                              PhiloxKeys keys, uint8_t *__restrict__ x, float *__restrict__ conf)
+// Candidates k0 .. k0 + N - 1 over the variables 0 .. n - 1 (rows of n, candidate k0 first).
+__global__ void __launch_bounds__(256) k_pool(const float *__restrict__ zsel, int32_t n, int32_t k0, int32_t N,
+                                              float inv_tau, PhiloxKeys keys, uint8_t *__restrict__ x,
+                                              float *__restrict__ conf)
 {
     const int64_t total = (int64_t)N * n;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
          i += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t k = (int32_t)(i / n), v = (int32_t)(i - (int64_t)k * n);
+        const int32_t kr = (int32_t)(i / n), v = (int32_t)(i - (int64_t)kr * n), k = k0 + kr;
         const uint4 w = philox4x32_10(make_uint4((uint32_t)v, (uint32_t)(k >> 2), 0u, 2u), keys);
         const uint32_t wk = (k & 3) == 0 ? w.x : (k & 3) == 1 ? w.y : (k & 3) == 2 ? w.z : w.w;
         const float a = (zsel[v] + logistic_from_word(wk)) * inv_tau;
@@ -151,20 +155,23 @@ __global__ void __launch_bounds__(256) k_pool(const float *__restrict__ zsel, in
 // confidence, ties to the lower index.
 __global__ void __launch_bounds__(kSelThreads) k_topk(const uint8_t *__restrict__ x, const float *__restrict__ conf,
                                                       int32_t n, int32_t n_sel, int32_t S,
-                                                      int32_t *__restrict__ units)
+                                                      int32_t *__restrict__ units, uint64_t *__restrict__ gkeys,
+                                                      int32_t gstride)
 {
     // rows of n variables; the units come from the first n_sel (the original variables of
-    // a normalised CNF: P:214 excludes the auxiliaries)
+    // a normalised CNF: P:214 excludes the auxiliaries). |S| > kMaxSorted: the block sorts
+    // in its row of the global scratch gkeys (gstride keys, a power of two >= S)
     __shared__ uint64_t s_keys[kMaxSorted];
     const int32_t k = blockIdx.x;
     const float *c = conf + (size_t)k * n;
     auto key_of = [&](int32_t v) -> uint64_t {
         return ((uint64_t)__float_as_uint(c[v]) << 32) | (uint64_t)(0xFFFFFFFFu - (uint32_t)v);
     };
+    uint64_t *keys = S <= kMaxSorted ? s_keys : gkeys + (size_t)k * gstride;
     const uint64_t thr = select_threshold(n_sel, S, key_of);
-    collect_sorted_desc(n_sel, S, thr, key_of, s_keys);
+    collect_sorted_desc(n_sel, S, thr, key_of, keys);
     for (int32_t j = threadIdx.x; j < S; j += blockDim.x) {
-        const int32_t v = (int32_t)(0xFFFFFFFFu - (uint32_t)(s_keys[j] & 0xFFFFFFFFull));
+        const int32_t v = (int32_t)(0xFFFFFFFFu - (uint32_t)(keys[j] & 0xFFFFFFFFull));
         units[(size_t)k * S + j] = x[(size_t)k * n + v] ? v + 1 : -(v + 1);
     }
 }
@@ -198,19 +205,20 @@ void gather_z(const float *z, int32_t n, int32_t b_pad, int32_t lb, float *out, 
     k_gather_z<<<(n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096, 256, 0, st>>>(z, n, b_pad, lb, out);
 }
 
-void pool(const float *zsel, int32_t n, int32_t N, float inv_tau, uint64_t pool_seed, uint8_t *x, float *conf,
-          cudaStream_t st)
+void pool(const float *zsel, int32_t n, int32_t k0, int32_t N, float inv_tau, uint64_t pool_seed, uint8_t *x,
+          float *conf, cudaStream_t st)
 {
     const int64_t total = (int64_t)N * n;
     int64_t g = (total + 255) / 256;
     if (g > 148 * 16) g = 148 * 16;
-    k_pool<<<(unsigned)(g < 1 ? 1 : g), 256, 0, st>>>(zsel, n, N, inv_tau, philox_round_keys(pool_seed), x, conf);
+    k_pool<<<(unsigned)(g < 1 ? 1 : g), 256, 0, st>>>(zsel, n, k0, N, inv_tau, philox_round_keys(pool_seed), x,
+                                                       conf);
 }
 
 void topk(const uint8_t *x, const float *conf, int32_t n, int32_t n_sel, int32_t N, int32_t S, int32_t *units,
-          cudaStream_t st)
+          uint64_t *gkeys, int32_t gstride, cudaStream_t st)
 {
-    k_topk<<<N, kSelThreads, 0, st>>>(x, conf, n, n_sel, S, units);
+    k_topk<<<N, kSelThreads, 0, st>>>(x, conf, n, n_sel, S, units, gkeys, gstride);
 }
 
 void lowconf(const float *zsel, int32_t n, int32_t d, int32_t *vars, cudaStream_t st)

@@ -7,7 +7,8 @@
 //   k_clauses_st  a5/a8 the scalar clause sweep for batches whose word count W is not a
 //                     multiple of 4 (b_pad < 1024 padded to 32): U = AND of false-literal
 //                     words, exclusive products E = ~any | (S_i & ~atleast2) in CSC order
-//                     (negative occurrences complemented), per-member counts of U
+//                     (negative occurrences complemented), per-member counts of U; the
+//                     forward of X and the check of R in one pass over the sweep order
 //   k_best / k_gfinalize / k_extract  a8-a9 best tracking (local, over ranks) and the winner's bits
 // (the sweep for b_pad >= 1024 is k_sweep in clause_kernels.cu, the update in
 // update_kernels.cu)
@@ -33,9 +34,16 @@ __global__ void __launch_bounds__(256) k_init(StepParams p, float4 *__restrict__
     const int lane = threadIdx.x & 31;
     const uint32_t QW = (uint32_t)p.b_pad / 4u;               // a multiple of 8: whole words per 8 lanes
     const uint2 key = make_uint2((uint32_t)p.seed, (uint32_t)(p.seed >> 32));
-    // rows blockIdx.x, blockIdx.x + gridDim.x, ...; quads of a row across the CTA (no division)
-    for (int32_t v = blockIdx.x; v < p.n; v += gridDim.x)
-    for (uint32_t q = threadIdx.x; q < QW; q += blockDim.x) {
+    // A CTA pass covers rpc rows: one row's quads across the CTA (QW >= 256, a multiple of
+    // 256), or 256 / QW whole rows of QW quads (small sub-batch windows: b_pad = 32 would
+    // otherwise leave 248 of 256 threads idle). Every lane runs the same passes (ballots).
+    const uint32_t rpc = QW >= 256u ? 1u : 256u / QW;
+    const uint32_t r_t = QW >= 256u ? 0u : threadIdx.x / QW;
+    const uint32_t q_t = threadIdx.x - r_t * (QW >= 256u ? 0u : QW);
+    for (int64_t base = (int64_t)blockIdx.x * rpc; base < p.n; base += (int64_t)gridDim.x * rpc)
+    for (uint32_t q = q_t; q < (QW >= 256u ? QW : q_t + 1u); q += blockDim.x) {
+        const int32_t v = (int32_t)base + (int32_t)r_t;
+        const bool valid = r_t < rpc && v < p.n;            // uniform over each 8-lane group
         const int64_t bq = p.b0 + 4 * (int64_t)q;           // global index of member 0 of the quad
         float zz[4];
 #pragma unroll
@@ -57,7 +65,7 @@ __global__ void __launch_bounds__(256) k_init(StepParams p, float4 *__restrict__
         uint32_t xn = 0, rn = 0;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-            const int pb = pinned_bit(p, v, bq + j);
+            const int pb = valid ? pinned_bit(p, v, bq + j) : -1;
             // X_1 = [z0 + logit u >= 0] (the sign of a = (z0 + ell) / tau does not depend on
             // tau > 0), without a logarithm: with e = exp(-|z0|), u - ub e >= 0 (z0 >= 0)
             // or u e - ub >= 0 (z0 < 0), as one FMA (the update's rewrite, update_kernels.cu)
@@ -70,15 +78,15 @@ __global__ void __launch_bounds__(256) k_init(StepParams p, float4 *__restrict__
             xn |= xb << j;
             rn |= rb << j;
         }
-        const size_t idx = (size_t)v * QW + q;
-        z4[idx] = make_float4(zz[0], zz[1], zz[2], zz[3]);
-        m4[idx] = make_float4(0.f, 0.f, 0.f, 0.f);
-        v4[idx] = make_float4(0.f, 0.f, 0.f, 0.f);
-        // active lanes: whole 8-lane groups with q < QW (QW is a multiple of 8)
-        const uint32_t qb = q & ~31u;
-        const uint32_t act = QW - qb >= 32u ? 0xffffffffu : ((1u << (QW - qb)) - 1u);
-        const uint32_t xw = pack_quads(xn, lane, act), rw = pack_quads(rn, lane, act);
-        if ((lane & 7) == 0) {
+        if (valid) {
+            const size_t idx = (size_t)v * QW + q;
+            z4[idx] = make_float4(zz[0], zz[1], zz[2], zz[3]);
+            m4[idx] = make_float4(0.f, 0.f, 0.f, 0.f);
+            v4[idx] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        // every lane of the warp is here (same passes); groups of 8 lanes never straddle rows
+        const uint32_t xw = pack_quads(xn, lane), rw = pack_quads(rn, lane);
+        if (valid && (lane & 7) == 0) {
             X[xr_at(v, (int32_t)(q >> 3), p.W)] = xw;
             R[xr_at(v, (int32_t)(q >> 3), p.W)] = rw;
         }
@@ -122,17 +130,24 @@ __global__ void __launch_bounds__(256) k_resample(StepParams p, const float4 *__
 
 // ------------------------------------------------------------- a5 / a8: clause kernels
 // Lane layout: LW = min(W, 32) lanes per clause cover 32-word chunk blockIdx.y of the batch
-// words; CPW = 32 / LW clauses per warp row. kForward: write E and count U of the sample
-// X into cnt (Lambda). !kForward: count U of the rounding into cnt (exact unsat counts).
-template <bool kForward>
+// words; CPW = 32 / LW clauses per warp row; clauses in sweep order (sweep_off / sweep_slot
+// = {code, CSC position}: width-sorted, no clause_perm indirection). kForward: E of the
+// sample X and its U counts (Lambda) into lam; kCheck: the U counts of the rounding R
+// (exact unsat counts) into unsat — both in ONE pass when both are set (a literal's X and
+// R words share a 32-byte sector of the interleaved rows).
+template <bool kForward, bool kCheck>
 __global__ void __launch_bounds__(256) k_clauses_st(DevCnf c, int32_t W, int32_t b_pad,
-                                                    const uint32_t *__restrict__ bits,
-                                                    uint32_t *__restrict__ E, int32_t *__restrict__ cnt,
-                                                    Ctrl *__restrict__ ctrl)
+                                                    const uint32_t *__restrict__ X, const uint32_t *__restrict__ R,
+                                                    uint32_t *__restrict__ E, int32_t *__restrict__ lam,
+                                                    int32_t *__restrict__ unsat, Ctrl *__restrict__ ctrl)
 {
-    __shared__ int32_t s_cnt[1024];
+    __shared__ int32_t s_lam[kForward ? 1024 : 1];
+    __shared__ int32_t s_uns[kCheck ? 1024 : 1];
     if (ctrl->stopped) return;
-    for (int i = threadIdx.x; i < 1024; i += blockDim.x) s_cnt[i] = 0;
+    for (int i = threadIdx.x; i < 1024; i += blockDim.x) {
+        if (kForward) s_lam[i] = 0;
+        if (kCheck) s_uns[i] = 0;
+    }
     __syncthreads();
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -146,26 +161,36 @@ __global__ void __launch_bounds__(256) k_clauses_st(DevCnf c, int32_t W, int32_t
     for (int64_t g = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; g < ngroups; g += stride) {
         const int64_t ci = g * CPW + sub;
         if (!lane_ok || ci >= c.m) continue;
-        const int32_t cl = c.clause_perm[ci];     // width-sorted order
-        const int32_t lo = c.clause_off[cl], width = c.clause_off[cl + 1] - lo;
-        uint32_t any = 0, two = 0;       // per member bit: >= 1 / >= 2 literals true
+        const int32_t lo = c.sweep_off[ci], width = c.sweep_off[ci + 1] - lo;
+        uint32_t any = 0, two = 0;       // per member bit: >= 1 / >= 2 literals of X true
+        uint32_t anyR = 0;               // >= 1 literal of R true
         uint32_t S[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
             if (i < width) {
-                const int2 si = c.slot_info[lo + i];
-                const uint32_t s = bits[xr_at(si.x >> 1, word, W)] ^ (0u - (uint32_t)(si.x & 1));
-                S[i] = s;
-                two |= any & s;
-                any |= s;
+                const int2 si = c.sweep_slot[lo + i];
+                const size_t at = xr_at(si.x >> 1, word, W);
+                const uint32_t nm = 0u - (uint32_t)(si.x & 1);
+                if (kForward) {
+                    const uint32_t s = X[at] ^ nm;
+                    S[i] = s;
+                    two |= any & s;
+                    any |= s;
+                }
+                if (kCheck) anyR |= R[at] ^ nm;
             }
         }
         for (int i = 8; i < width; ++i) {
-            if (!kForward && any == 0xFFFFFFFFu) break;   // every member already satisfied
-            const int2 si = c.slot_info[lo + i];
-            const uint32_t s = bits[xr_at(si.x >> 1, word, W)] ^ (0u - (uint32_t)(si.x & 1));
-            two |= any & s;
-            any |= s;
+            if (!kForward && anyR == 0xFFFFFFFFu) break;   // every member already satisfied
+            const int2 si = c.sweep_slot[lo + i];
+            const size_t at = xr_at(si.x >> 1, word, W);
+            const uint32_t nm = 0u - (uint32_t)(si.x & 1);
+            if (kForward) {
+                const uint32_t s = X[at] ^ nm;
+                two |= any & s;
+                any |= s;
+            }
+            if (kCheck) anyR |= R[at] ^ nm;
         }
         if (kForward) {
             // E_i = prod_{j != i} (1 - s_j): all other literals false <=> none true, or
@@ -175,28 +200,37 @@ __global__ void __launch_bounds__(256) k_clauses_st(DevCnf c, int32_t W, int32_t
 #pragma unroll
             for (int i = 0; i < 8; ++i)
                 if (i < width) {
-                    const int2 si = c.slot_info[lo + i];
+                    const int2 si = c.sweep_slot[lo + i];
                     Ec[(size_t)si.y * LW] = (~any | (S[i] & ~two)) ^ (0u - (uint32_t)(si.x & 1));
                 }
             for (int i = 8; i < width; ++i) {
-                const int2 si = c.slot_info[lo + i];
-                const uint32_t s = bits[xr_at(si.x >> 1, word, W)] ^ (0u - (uint32_t)(si.x & 1));
+                const int2 si = c.sweep_slot[lo + i];
+                const uint32_t s = X[xr_at(si.x >> 1, word, W)] ^ (0u - (uint32_t)(si.x & 1));
                 Ec[(size_t)si.y * LW] = (~any | (s & ~two)) ^ (0u - (uint32_t)(si.x & 1));
             }
+            uint32_t U = ~any;              // U = prod_i (1 - s_i): clause unsatisfied
+            while (U) {
+                const int j = __ffs(U) - 1;
+                atomicAdd(&s_lam[wl * 32 + j], 1);
+                U &= U - 1;
+            }
         }
-        uint32_t U = ~any;                  // U = prod_i (1 - s_i): clause unsatisfied
-        while (U) {
-            const int j = __ffs(U) - 1;
-            atomicAdd(&s_cnt[wl * 32 + j], 1);
-            U &= U - 1;
+        if (kCheck) {
+            uint32_t U = ~anyR;
+            while (U) {
+                const int j = __ffs(U) - 1;
+                atomicAdd(&s_uns[wl * 32 + j], 1);
+                U &= U - 1;
+            }
         }
     }
     __syncthreads();
     const int base = blockIdx.y * 1024;
     for (int i = threadIdx.x; i < 1024; i += blockDim.x) {
-        const int32_t v = s_cnt[i];                       // i = word * 32 + bit position
-        const int mb = member_of_slot(i);
-        if (v != 0 && base + mb < b_pad) atomicAdd(&cnt[base + mb], v);
+        const int mb = member_of_slot(i);                 // i = word * 32 + bit position
+        if (base + mb >= b_pad) continue;
+        if (kForward && s_lam[i] != 0) atomicAdd(&lam[base + mb], s_lam[i]);
+        if (kCheck && s_uns[i] != 0) atomicAdd(&unsat[base + mb], s_uns[i]);
     }
 }
 
@@ -267,8 +301,10 @@ static unsigned grid_cap(uint64_t work, unsigned threads, unsigned cap)
 
 void init(const StepParams &p, float *z, float *m, float *v, uint32_t *X, uint32_t *R, cudaStream_t st)
 {
-    const unsigned rows = (unsigned)(p.n < 148 * 16 ? (p.n > 0 ? p.n : 1) : 148 * 16);
-    k_init<<<rows, 256, 0, st>>>(p, (float4 *)z, (float4 *)m, (float4 *)v, X, R);
+    const uint32_t QW = (uint32_t)p.b_pad / 4u, rpc = QW >= 256u ? 1u : 256u / QW;
+    const int64_t passes = ((int64_t)p.n + rpc - 1) / rpc;
+    const unsigned grid = (unsigned)(passes < 148 * 16 ? (passes > 0 ? passes : 1) : 148 * 16);
+    k_init<<<grid, 256, 0, st>>>(p, (float4 *)z, (float4 *)m, (float4 *)v, X, R);
 }
 
 void resample(const StepParams &p, const float *z, uint32_t *X, uint32_t *R, int32_t t_next, cudaStream_t st)
@@ -305,8 +341,13 @@ bool clauses(const DevCnf &c, int32_t W, int32_t b_pad, const uint32_t *X, const
         clauses_v4(c, W, b_pad, X, R, E, lam, unsat, ctrl, ba, st);
         return R != nullptr;
     }
-    if (X) k_clauses_st<true><<<clause_grid(c, W), 256, 0, st>>>(c, W, b_pad, X, E, lam, ctrl);
-    if (R) k_clauses_st<false><<<clause_grid(c, W), 256, 0, st>>>(c, W, b_pad, R, nullptr, unsat, ctrl);
+    const dim3 grid = clause_grid(c, W);
+    if (X && R)
+        k_clauses_st<true, true><<<grid, 256, 0, st>>>(c, W, b_pad, X, R, E, lam, unsat, ctrl);
+    else if (X)
+        k_clauses_st<true, false><<<grid, 256, 0, st>>>(c, W, b_pad, X, nullptr, E, lam, nullptr, ctrl);
+    else if (R)
+        k_clauses_st<false, true><<<grid, 256, 0, st>>>(c, W, b_pad, nullptr, R, nullptr, nullptr, unsat, ctrl);
     return false;
 }
 

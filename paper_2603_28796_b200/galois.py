@@ -39,6 +39,7 @@ EXPORTED = (
     "galois_engine_kernel_times", "galois_select_member", "galois_candidate_pool", "galois_cube_variables",
     "galois_cnf_normalize", "galois_cnf_get_csr", "galois_engine_set_subbatch", "galois_engine_set_lanes", "galois_engine_bytes_per_member",
     "galois_engine_set_graphs", "galois_engine_get_member", "galois_cnf_original_vars", "galois_candidate_pool_size",
+    "galois_device_free_bytes",
 )
 
 
@@ -97,6 +98,7 @@ def lib() -> ctypes.CDLL:
             "galois_engine_set_subbatch": [P, I32],
             "galois_engine_set_lanes": [P, I32],
             "galois_engine_bytes_per_member": [P, I32, P],
+            "galois_device_free_bytes": [I32, P],
             "galois_engine_set_graphs": [P, I32],
             "galois_engine_get_member": [P, I64, P, P, P, P, P, P, P, P, P, P],
             "galois_cnf_original_vars": [P, P],
@@ -161,6 +163,12 @@ def galois_comm_unique_id() -> bytes:
     buf = ctypes.create_string_buffer(128)
     _check(lib().galois_comm_unique_id(buf))
     return buf.raw
+
+
+def galois_device_free_bytes(device: int = 0) -> int:
+    out = ctypes.c_int64()
+    _check(lib().galois_device_free_bytes(int(device), ctypes.byref(out)))
+    return out.value
 
 
 # ------------------------------------------------------------------------- classes

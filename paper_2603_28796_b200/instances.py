@@ -160,6 +160,50 @@ def industrial(n: int, m: int, seed: int = 0, planted: bool = False,
     return Instance(name, n, offsets, lits.astype(np.int32), xstar)
 
 
+def industrial_large(n: int, m: int, seed: int = 0, wmin: int = 2, wmax: int = 30,
+                     width_exp: float = 2.5, occ_exp: float = 0.8) -> Instance:
+    """G3 at the paper's largest scale (48,505,464 variables, 130,975,382 clauses —
+    reading R17), vectorised by width so it draws ~0.5G literals in minutes: widths
+    P(w) ∝ w^-2.5 on [2, 30] in random clause order; variables by the inverse CDF of the
+    continuous law f(x) ∝ x^-0.8 on [1, n + 1) (index floor(x) - 1: G3's discrete
+    P(i) ∝ i^-0.8 up to the discretisation of the density), rows with a repeated variable
+    redrawn whole; a seeded permutation of variable ids; fair-coin signs. Not the same
+    stream as `industrial` (C4 stays as it is)."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    ws = np.arange(wmin, wmax + 1)
+    pw = ws.astype(np.float64) ** (-width_exp)
+    pw /= pw.sum()
+    widths = rng.choice(ws, size=m, p=pw).astype(np.int64)
+    offsets = np.zeros(m + 1, dtype=np.int64)
+    np.cumsum(widths, out=offsets[1:])
+    lits = np.empty(int(offsets[-1]), dtype=np.int32)
+    top = float(n + 1) ** (1.0 - occ_exp) - 1.0
+    expo = 1.0 / (1.0 - occ_exp)
+    perm = rng.permutation(n).astype(np.int32)
+
+    def draw(shape):
+        x = (1.0 + rng.random(shape) * top) ** expo
+        return np.minimum(x.astype(np.int64) - 1, n - 1)
+
+    for w in ws:
+        idx = np.nonzero(widths == w)[0]
+        if idx.size == 0:
+            continue
+        rows = draw((idx.size, int(w)))
+        while True:
+            srt = np.sort(rows, axis=1)
+            bad = np.nonzero((srt[:, 1:] == srt[:, :-1]).any(axis=1))[0]
+            if bad.size == 0:
+                break
+            rows[bad] = draw((bad.size, int(w)))
+        signs = np.where(rng.random(rows.shape) < 0.5, -1, 1).astype(np.int32)
+        vals = (perm[rows] + 1) * signs
+        pos = offsets[idx][:, None] + np.arange(int(w), dtype=np.int64)[None, :]
+        lits[pos.ravel()] = vals.ravel()
+        del rows, srt, signs, vals, pos
+    return Instance(f"industrial-large-n{n}-m{m}-s{seed}", n, offsets, lits)
+
+
 def _gather_clauses(lits: np.ndarray, off: np.ndarray, keep: np.ndarray) -> np.ndarray:
     w = off[keep + 1] - off[keep]
     starts = np.repeat(off[keep], w)

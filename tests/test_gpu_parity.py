@@ -59,7 +59,7 @@ def test_csc_is_stable_counting_sort(G, which):
 
 
 # --------------------------------------------------------------------------- a3-a8
-@pytest.mark.parametrize("batch", [32, 64, 100, 256])
+@pytest.mark.parametrize("batch", [32, 64, 100, 224, 256, 2048])
 def test_init_and_t0_check(G, batch):
     """a3 + a8 at t = 0: z0 = theta_1 - theta_0 from the same Philox counters, R_0, the
     exact unsat counts and the best at t = 0."""
@@ -234,6 +234,42 @@ def test_selection_pool_and_cubes(G, batch, n):
         assert list(vars_) == O.lowest_confidence_vars(z, d)     # same fp32 z on both sides: exact
     eng.free()
     cnf.free()
+
+
+def test_pool_large_S_units_only(G):
+    """f1 at the shape of the paper's largest instance: |S| above one CTA's
+    shared-memory sort (global-memory bitonic sort) and the units-only pool, drawn over the
+    original variables of a normalised CNF in candidate groups; against the oracle's Eq.10-11
+    on the same fp32 logits and against the full draw (identical units)."""
+    inst = I.industrial(20_000, 80_000, 13)
+    cnf0 = G.Cnf.from_instance(inst)
+    cnf = cnf0.normalize(3)
+    assert cnf.original_vars() == inst.n < cnf.n
+    eng = G.Engine(cnf, 64, 8, 0.5, 3)
+    eng.run()
+    sel = eng.select_member(0)
+    b, z = sel["global_b"], sel["z"][:inst.n].astype(np.float64)
+    N, rho = 5, 0.3
+    full = eng.candidate_pool(b, N, rho, pool_seed=9)
+    part = eng.candidate_pool(b, N, rho, pool_seed=9, arrays=False)
+    S = full["S"]
+    assert S == part["S"] == 6000 > 4096
+    np.testing.assert_array_equal(full["units"], part["units"])
+    xo, co = O.pool(z, N, 1.0, 9)
+    for k in range(N):
+        gpu_units = list(full["units"][k])
+        ora_units = O.top_confident_units(xo[k], co[k], rho)
+        assert len(gpu_units) == S == len(ora_units)
+        if gpu_units != ora_units:
+            thr = np.sort(co[k])[::-1][S - 1]
+            for u in set(gpu_units) ^ set(ora_units):
+                assert abs(co[k][abs(u) - 1] - thr) < 1e-6
+            # the order is descending confidence (ties to the lower index) up to fp32 ties
+            cg = co[k][np.abs(gpu_units) - 1]
+            assert (np.diff(cg) <= 1e-6).all()
+    eng.free()
+    cnf.free()
+    cnf0.free()
 
 
 def test_cubes(G):
