@@ -1158,7 +1158,7 @@ static int prepare(galois_engine *e)
         slab.add(&e->small_snap, (size_t)e->W * (size_t)n);
     }
     if (e->mode == GALOIS_MODE_ST) {
-        slab.add(&e->E, (size_t)c->L * e->W);
+        slab.add(&e->E, (size_t)c->L * e->W + 4);   // + 16 B: the small-window update copies whole 16-B units
         slab.add(&e->lam, 2 * (size_t)e->b_pad);
         if (c->num_hub_chunks > 0) slab.add(&e->partial, (size_t)c->num_hub_chunks * (e->b_pad / 4));
         if (e->debug) {

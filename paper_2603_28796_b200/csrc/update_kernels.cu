@@ -1367,6 +1367,218 @@ __global__ void __launch_bounds__(512) k_small_run(DevCnf c, StepParams p, int32
 }
 
 // ------------------------------------------------------------------ launch wrappers
+// ---------------- a6 + a7: fused update for sub-1024 windows, TMA-pipelined (32 % W == 0)
+// Batches of 32, 64, 128, 256 or 512 members (W = b_pad / 32 in {1, 2, 4, 8, 16}: f4's
+// sub-batch windows on instances too large for 1024 resident members). E rows are
+// W words (E[L][W], CSC order), so an item is a GROUP of R = 32 / W consecutive variables
+// x all their members — 256 quads, one per consumer thread — and its z, m, v are 3 x 4 KB
+// contiguous, its E rows one contiguous CSC range. The producer warp bulk-copies z, m, v
+// and the group's rows (minus hub variables' rows, which come from the hub partials) into
+// kSwStages-deep ring stages of kSwE bytes, splitting long ranges into pieces; a consumer
+// thread counts the rows of its own variable that fall in each piece. Same per-quad
+// arithmetic (quad_update) as k_update_st, so iterates are bit-identical to it.
+#ifndef GALOIS_UPD_SMALLW
+#define GALOIS_UPD_SMALLW 1
+#endif
+#ifndef GALOIS_SMALLW_STAGES
+#define GALOIS_SMALLW_STAGES 3
+#endif
+#ifndef GALOIS_SMALLW_E
+#define GALOIS_SMALLW_E 8192
+#endif
+#ifndef GALOIS_SMALLW_CTAS
+#define GALOIS_SMALLW_CTAS 3
+#endif
+constexpr int kSwStages = GALOIS_SMALLW_STAGES;
+constexpr int kSwCtasPerSm = GALOIS_SMALLW_CTAS;
+constexpr int kSwE = GALOIS_SMALLW_E;                     // E bytes per stage
+constexpr int kSwStageBytes = kSwE + 3 * 4096;
+constexpr int kSwSmem = kSwStages * kSwStageBytes;
+
+struct SwHdr {
+    int32_t r0, r1;    // CSC rows [r0, r1) of this piece
+    int32_t ra;        // first row copied (r0 rounded down to a 16-byte boundary)
+};
+
+template <bool kTau1, bool kAdam, bool kPins>
+__global__ void __launch_bounds__(256 + 32, kSwCtasPerSm)
+    k_update_smallw(DevCnf c, StepParams p, int32_t W, uint32_t groups, float4 *__restrict__ z4,
+                    float4 *__restrict__ m4, float4 *__restrict__ v4, uint32_t *__restrict__ X,
+                    uint32_t *__restrict__ R, const uint32_t *__restrict__ E, const short4 *__restrict__ partial,
+                    Ctrl *__restrict__ ctrl)
+{
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ uint64_t full[kSwStages], empty[kSwStages];
+    __shared__ SwHdr hdr[kSwStages];
+    __shared__ int32_t hflags[kSwStages];   // bit 0: z, m, v in this stage; bit 1: the group's last stage
+    if (ctrl->stopped) return;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t QW = 8u * (uint32_t)W;    // quads per variable row
+    const int32_t RG = 32 / W;               // variables per group
+    const uint32_t full_s = smem_u32(full), empty_s = smem_u32(empty), stage_s = smem_u32(smem);
+    if (tid == 0) {
+        for (int i = 0; i < kSwStages; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], 32 * kConsumerWarps);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    if (warp == kConsumerWarps) {          // ------------------------------ producer warp
+        const int32_t rpa = W >= 4 ? 1 : 4 / W;             // rows per 16 bytes
+        const int32_t cap = kSwE / (4 * W);                  // rows per stage (a multiple of rpa)
+        int st = 0;
+        uint32_t ph = 0;
+        bool wrapped = false;
+        for (uint32_t g = blockIdx.x; g < groups; g += gridDim.x) {
+            const int32_t v0 = (int32_t)g * RG, nv = min(RG, c.n - v0);
+            // lane j: variable v0 + j's CSC range and whether it is a hub
+            int32_t kb = 0, ke = 0;
+            bool hub = false;
+            if (lane < nv) {
+                kb = c.code_off[2 * (v0 + lane)];
+                ke = c.code_off[2 * (v0 + lane) + 2];
+                hub = c.num_hubs > 0 && c.hub_of_var[v0 + lane] >= 0;
+            }
+            uint32_t hm = __ballot_sync(0xffffffffu, hub);
+            const int32_t end = __shfl_sync(0xffffffffu, ke, nv - 1);
+            int32_t a = __shfl_sync(0xffffffffu, kb, 0);
+            bool first = true;
+            // pieces of [a, b) (the last one of the group flagged when `fin`)
+            auto pieces = [&](int32_t lo, int32_t hi, bool fin) {
+                while (true) {
+                    const int32_t ra = lo / rpa * rpa;
+                    const int32_t r1 = min(hi, ra + cap);
+                    const bool last = fin && r1 >= hi;
+                    if (r1 > lo || last || first) {
+                        if (lane == 0) {
+                            if (wrapped) {
+                                mbar_wait_s(empty_s + 8u * st, ph ^ 1u);
+                                fence_proxy_async_smem();
+                            }
+                            hdr[st] = SwHdr{lo, max(lo, r1), ra};
+                            hflags[st] = (first ? 1 : 0) | (last ? 2 : 0);
+                            const int32_t rb = r1 > lo ? (r1 + rpa - 1) / rpa * rpa : ra;
+                            const uint32_t ebytes = (uint32_t)(rb - ra) * 4u * (uint32_t)W;
+                            const uint32_t zb = (uint32_t)nv * QW * 16u;
+                            const uint32_t fb = full_s + 8u * st, sbs = stage_s + (uint32_t)(st * kSwStageBytes);
+                            mbar_arrive_expect_tx_s(fb, (first ? 3u * zb : 0u) + ebytes);
+                            if (first) {
+                                const size_t off = (size_t)v0 * QW;
+                                bulk_g2s_s(sbs + kSwE, z4 + off, zb, fb);
+                                bulk_g2s_s(sbs + kSwE + 4096, m4 + off, zb, fb);
+                                bulk_g2s_s(sbs + kSwE + 8192, v4 + off, zb, fb);
+                            }
+                            if (ebytes) bulk_g2s_s(sbs, E + (size_t)ra * W, ebytes, fb);
+                        }
+                        __syncwarp();
+                        first = false;
+                        if (++st == kSwStages) {
+                            st = 0;
+                            ph ^= 1u;
+                            wrapped = true;
+                        }
+                    }
+                    if (r1 >= hi) break;
+                    lo = r1;
+                }
+            };
+            while (hm) {                                     // skip the hub variables' rows
+                const int j = __ffs(hm) - 1;
+                hm &= hm - 1;
+                pieces(a, __shfl_sync(0xffffffffu, kb, j), false);
+                a = __shfl_sync(0xffffffffu, ke, j);
+            }
+            pieces(a, max(a, end), true);
+        }
+    } else {
+    // ------------------------------------------------------------------ consumer warps
+    const int32_t s = ctrl->t + 1;
+    const float2 ac = p.adam_consts[s];
+    bool bad = false;
+    for (int32_t i = blockIdx.x * 256 + tid; i < p.b_pad; i += gridDim.x * 256) {   // next sweep's counters
+        if (p.clear_a) p.clear_a[i] = 0;
+        if (p.clear_b) p.clear_b[i] = 0;
+    }
+    const uint32_t r_t = (uint32_t)tid / QW, q = (uint32_t)tid - r_t * QW;   // variable in group, quad
+    const int sh = tid & 7;                  // quad within its 32-member word (QW % 8 == 0)
+    const uint32_t wq = q >> 3;              // word within the row
+    int st = 0;
+    uint32_t ph = 0;
+    for (uint32_t g = blockIdx.x; g < groups; g += gridDim.x) {
+        const int32_t v = (int32_t)g * RG + (int32_t)r_t;
+        const bool valid = v < c.n;
+        int32_t k0 = 0, k1 = 0, k2 = 0, hub = -1;
+        if (valid) {
+            k0 = c.code_off[2 * v];
+            k1 = c.code_off[2 * v + 1];
+            k2 = c.code_off[2 * v + 2];
+            hub = c.num_hubs > 0 ? c.hub_of_var[v] : -1;
+        }
+        float4 z = make_float4(0.f, 0.f, 0.f, 0.f), m = z, vv = z;
+        int32_t G[4] = {0, 0, 0, 0};
+        int32_t flags = 0;
+        do {
+            mbar_wait_s(full_s + 8u * st, ph);
+            const SwHdr h = hdr[st];
+            flags = hflags[st];
+            const uint8_t *sb = smem + st * kSwStageBytes;
+            if ((flags & 1) && valid) {
+                z = reinterpret_cast<const float4 *>(sb + kSwE)[tid];
+                m = reinterpret_cast<const float4 *>(sb + kSwE + 4096)[tid];
+                vv = reinterpret_cast<const float4 *>(sb + kSwE + 8192)[tid];
+            }
+            if (valid && hub < 0) {
+                const int32_t a = max(h.r0, k0), b = min(h.r1, k2);
+                if (b > a) {
+                    const uint32_t *srow = reinterpret_cast<const uint32_t *>(sb) + (a - h.ra) * W + wq;
+                    static_assert(kHubDegree <= 256, "one SWAR pass + one row");
+                    // SWAR bytes: a non-hub variable has <= kHubDegree = 256 rows, so 255 of
+                    // them fit a byte and at most one more is added on its own
+                    const int32_t nr = b - a, n1 = min(nr, 255);
+                    uint32_t acc = 0;
+#pragma unroll 8
+                    for (int32_t k = 0; k < n1; ++k) acc += quad_bits(srow[k * W], sh);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) G[j] += (int32_t)((acc >> (8 * j)) & 255u);
+                    if (nr > 255) {
+                        const uint32_t last = quad_bits(srow[255 * W], sh);
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) G[j] += (int32_t)((last >> (8 * j)) & 1u);
+                    }
+                    const int32_t nneg = b - max(a, k1);          // negative rows are complemented
+                    if (nneg > 0) { G[0] -= nneg; G[1] -= nneg; G[2] -= nneg; G[3] -= nneg; }
+                }
+            }
+            mbar_arrive_s(empty_s + 8u * st);
+            if (++st == kSwStages) {
+                st = 0;
+                ph ^= 1u;
+            }
+        } while (!(flags & 2));
+        uint32_t xn = 0, rn = 0;
+        if (valid) {
+            if (hub >= 0) hub_signal(c, partial, QW, hub, q, G);
+            const int64_t bq = p.b0 + 4 * (int64_t)q;
+            float g1o[4];
+            quad_update<kTau1, kAdam, kPins>(p, ac, v, bq, s, G, z, m, vv, xn, rn, g1o, bad);
+            const size_t idx = (size_t)v * QW + q;
+            z4[idx] = z;
+            m4[idx] = m;
+            v4[idx] = vv;
+        }
+        const uint32_t xw = pack_quads(xn, lane), rw = pack_quads(rn, lane);   // 8-lane groups stay in a row
+        if (valid && (lane & 7) == 0) {
+            X[xr_at(v, (int32_t)wq, p.W)] = xw;
+            R[xr_at(v, (int32_t)wq, p.W)] = rw;
+        }
+    }
+    if (bad) atomicOr(&ctrl->nonfinite, 1);
+    }                                      // consumer warps
+    last_cta_tick(ctrl);
+}
+
 namespace launch {
 
 RowMap make_rowmap(uint32_t rows, uint32_t b_pad)
@@ -1447,6 +1659,16 @@ static PairKernel pick_pair(int variant)   // variant bits: 4 tau1, 2 adam, 1 pi
 #ifndef GALOIS_UPD_PAIR
 #define GALOIS_UPD_PAIR 1
 #endif
+using SmallWKernel = void (*)(DevCnf, StepParams, int32_t, uint32_t, float4 *, float4 *, float4 *, uint32_t *,
+                              uint32_t *, const uint32_t *, const short4 *, Ctrl *);
+static SmallWKernel pick_smallw(int variant)   // variant bits: 4 tau1, 2 adam, 1 pins
+{
+    static const SmallWKernel table[8] = {k_update_smallw<false, false, false>, k_update_smallw<false, false, true>,
+                                          k_update_smallw<false, true, false>,  k_update_smallw<false, true, true>,
+                                          k_update_smallw<true, false, false>,  k_update_smallw<true, false, true>,
+                                          k_update_smallw<true, true, false>,   k_update_smallw<true, true, true>};
+    return table[variant & 7];
+}
 
 template <bool a, bool b, bool c, bool d>
 struct SelTmaSliced {
@@ -1513,6 +1735,10 @@ cudaError_t configure_kernels()
         e = cudaFuncSetAttribute((const void *)pick_pair(v), cudaFuncAttributeMaxDynamicSharedMemorySize, kPairSmem);
         if (e != cudaSuccess) return e;
     }
+    for (int v = 0; v < 8; ++v) {
+        e = cudaFuncSetAttribute((const void *)pick_smallw(v), cudaFuncAttributeMaxDynamicSharedMemorySize, kSwSmem);
+        if (e != cudaSuccess) return e;
+    }
     e = cudaFuncSetAttribute((const void *)k_hub_partial_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              kHubStages * kHubStageBytes);
     if (e != cudaSuccess) return e;
@@ -1536,6 +1762,12 @@ void update_st(const DevCnf &c, const StepParams &p, float *z, float *m, float *
         const UpdKernel k = use_sliced(c) ? pick<SelTmaSliced>(variant) : pick<SelTma>(variant);
         k<<<item_grid(rm, kTmaCtasPerSm), 256 + 32, kTmaSmem, st>>>(c, p, rm, (float4 *)z, (float4 *)m, (float4 *)v, X, R, E,
                                                    partial, ctrl, (int4 *)dbg_G, (float4 *)dbg_g1);
+    } else if (GALOIS_UPD_SMALLW && !dbg_G && p.W < 32 && 32 % p.W == 0) {
+        const uint32_t RG = 32u / (uint32_t)p.W, groups = ((uint32_t)p.n + RG - 1u) / RG;
+        unsigned grid = 148u * kSwCtasPerSm;
+        if (groups < grid) grid = groups < 1 ? 1 : groups;
+        pick_smallw(variant)<<<grid, 256 + 32, kSwSmem, st>>>(c, p, p.W, groups, (float4 *)z, (float4 *)m,
+                                                             (float4 *)v, X, R, E, partial, ctrl);
     } else {
         const UpdKernel k = pick<SelGeneric>(variant);
         k<<<item_grid(rm, 8), 256, 0, st>>>(c, p, rm, (float4 *)z, (float4 *)m, (float4 *)v, X, R, E, partial,

@@ -134,6 +134,29 @@ def test_pair_update_odd_n_stepwise(G, batch, pinned):
     cnf.free()
 
 
+@pytest.mark.parametrize("batch,pinned", [(32, False), (64, True), (128, False), (256, True), (512, False)])
+def test_small_window_update_stepwise(G, batch, pinned):
+    """The production update of sub-1024 batches (k_update_smallw: groups of 32 / W
+    variables per item, E rows of W words staged by bulk copy, hub rows skipped for the
+    hub partials; f4's windows on instances too large for 1024 resident members): an
+    odd variable count (a ragged last group), hubs, degrees past one 16 KB piece at W = 16,
+    cube pins on hub and low-degree variables. Sampled members incl. the last, 4 steps."""
+    inst = I.industrial(2501, 30_000, 21, occ_exp=0.9)
+    deg = I.degrees(inst)
+    assert inst.n % 2 == 1 and (deg > 256).any()
+    pins = ()
+    if pinned:
+        low = [v for v in range(inst.n) if 0 < deg[v] <= 8][:2]
+        pins = tuple(sorted(set(I.top_degree_vars(inst, 2)) | {v + 1 for v in low}))
+    cnf = G.Cnf.from_instance(inst)
+    eng = G.Engine(cnf, batch, 20, 0.5, 0, cubes=pins)
+    members = tuple(sorted({0, 3, batch // 2 + 1, batch - 1}))
+    rep = parity.stepwise_sampled(G, inst, eng, members, 4, seed=0, cubes=pins)
+    assert rep["compared"] >= len(members) * 4 - 2, rep
+    eng.free()
+    cnf.free()
+
+
 def test_c2_lanes_stepwise(G):
     """configs[1] (B = 4096) split into the bench's 4 lanes (4 streams): sampled members of
     every lane, 4 steps."""

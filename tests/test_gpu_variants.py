@@ -126,7 +126,7 @@ def test_lanes_first_sat_vs_oracle(G):
     cnf.free()
 
 
-@pytest.mark.parametrize("K,sub", [(1, 1024), (3, 992)])
+@pytest.mark.parametrize("K,sub", [(1, 1024), (3, 992), (1, 256), (2, 64)])
 def test_windows_vs_oracle(G, K, sub):
     """f4 sub-batching: 3000 members in windows of `sub`, each run from t = 0; the
     best record over the windows, the bits and every member's last count against the

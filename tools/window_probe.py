@@ -5,7 +5,7 @@ inst = I.CONFIGS["C4"][0]()
 dev = torch.device("cuda:0")
 cnf = G.Cnf.from_instance(inst)
 print("bytes/member", cnf.bytes_per_member(), flush=True)
-for sub in [1024, 512, 256, 128, 64, 32]:
+for sub in [int(x) for x in os.environ.get('WINDOW_SUBS', '1024,512,256,128,64,32').split(',')]:
     for rep in range(3):
         eng = G.Engine(cnf, 3072 if sub >= 256 else 1024, 10, 0.5, 0, sub_batch=sub)
         if rep == 2: eng.set_profiling(True)
