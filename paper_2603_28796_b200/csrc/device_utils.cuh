@@ -8,6 +8,19 @@
 
 namespace galois {
 
+// Bounds checks of the staged kernels for a checking build (-DGALOIS_BOUNDS_CHECK: a failed
+// check traps the kernel, the launch returns an error); compiled out otherwise.
+#ifdef GALOIS_BOUNDS_CHECK
+#define GALOIS_DEV_CHECK(cond) \
+    do {                       \
+        if (!(cond)) __trap(); \
+    } while (0)
+#else
+#define GALOIS_DEV_CHECK(cond) \
+    do {                       \
+    } while (0)
+#endif
+
 // Member-in-word layout of every bit plane (X, R, E): member i (0..31) of a 32-member word
 // sits at bit 8 (i mod 4) + i / 4, i.e. member j of quad q' (i = 4 q' + j) at bit 8 j + q'.
 // A thread owning quad q' reads its 4 members as (w >> q') & 0x01010101 — already one

@@ -167,6 +167,7 @@ __global__ void __launch_bounds__(kSelThreads) k_topk(const uint8_t *__restrict_
     auto key_of = [&](int32_t v) -> uint64_t {
         return ((uint64_t)__float_as_uint(c[v]) << 32) | (uint64_t)(0xFFFFFFFFu - (uint32_t)v);
     };
+    GALOIS_DEV_CHECK(S <= kMaxSorted || (gkeys != nullptr && gstride >= S));
     uint64_t *keys = S <= kMaxSorted ? s_keys : gkeys + (size_t)k * gstride;
     const uint64_t thr = select_threshold(n_sel, S, key_of);
     collect_sorted_desc(n_sel, S, thr, key_of, keys);

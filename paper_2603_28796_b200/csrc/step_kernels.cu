@@ -80,6 +80,7 @@ __global__ void __launch_bounds__(256) k_init(StepParams p, float4 *__restrict__
         }
         if (valid) {
             const size_t idx = (size_t)v * QW + q;
+            GALOIS_DEV_CHECK(q < QW && v < p.n);
             z4[idx] = make_float4(zz[0], zz[1], zz[2], zz[3]);
             m4[idx] = make_float4(0.f, 0.f, 0.f, 0.f);
             v4[idx] = make_float4(0.f, 0.f, 0.f, 0.f);

@@ -1461,6 +1461,8 @@ __global__ void __launch_bounds__(256 + 32, kSwCtasPerSm)
                             hflags[st] = (first ? 1 : 0) | (last ? 2 : 0);
                             const int32_t rb = r1 > lo ? (r1 + rpa - 1) / rpa * rpa : ra;
                             const uint32_t ebytes = (uint32_t)(rb - ra) * 4u * (uint32_t)W;
+                            GALOIS_DEV_CHECK(ra >= 0 && ra <= lo && rb >= ra && ebytes <= (uint32_t)kSwE &&
+                                             (int64_t)rb * W <= (int64_t)c.L * W + 4);
                             const uint32_t zb = (uint32_t)nv * QW * 16u;
                             const uint32_t fb = full_s + 8u * st, sbs = stage_s + (uint32_t)(st * kSwStageBytes);
                             mbar_arrive_expect_tx_s(fb, (first ? 3u * zb : 0u) + ebytes);
@@ -1532,6 +1534,7 @@ __global__ void __launch_bounds__(256 + 32, kSwCtasPerSm)
             if (valid && hub < 0) {
                 const int32_t a = max(h.r0, k0), b = min(h.r1, k2);
                 if (b > a) {
+                    GALOIS_DEV_CHECK(a >= h.ra && (b - h.ra) * W <= kSwE / 4 && b - a <= 256);
                     const uint32_t *srow = reinterpret_cast<const uint32_t *>(sb) + (a - h.ra) * W + wq;
                     static_assert(kHubDegree <= 256, "one SWAR pass + one row");
                     // SWAR bytes: a non-hub variable has <= kHubDegree = 256 rows, so 255 of

@@ -6,7 +6,8 @@ parts: small (k_small_run, cooperative grid barrier: C1 through run()), tma (the
 TMA-pipelined updates k_update_pair / k_update_tma, sweep, hub partials, k_extract), lanes (2 lanes on
 their own streams, CUDA graph chunks), loop (k_sweep<kLoop>), v4 (b_pad < 1024 sweep and
 k_update_st), soft (SOFT mode), select (theta_sel / pool / top-|S| / cube variables),
-tseitin (device normalisation), window (f4 sub-batching). Default: all.
+tseitin (device normalisation), window (f4 sub-batching), smallw (sub-1024 windows: k_update_smallw,
+the fused scalar sweep, k_init's row packing, the units-only pool with a global-memory sort). Default: all.
 """
 import os
 import sys
@@ -147,8 +148,36 @@ def part_window():
     cnf.free()
 
 
+def part_smallw():
+    # k_update_smallw for every power-of-two window (W = 1..16) on an odd n with hubs, the
+    # fused scalar sweep (W = 1, 3), the small-window k_init mapping, and the units-only pool
+    # with |S| > 4096 (global-memory sort) on a normalised CNF
+    inst = I.industrial(2501, 30_000, 21, occ_exp=0.9)
+    cnf = G.Cnf.from_instance(inst)
+    for B in (32, 64, 96, 128, 256, 512):
+        e = G.Engine(cnf, B, 3, 0.5, 1, cubes=(1, 2) if B == 64 else ())
+        e.enqueue(3)
+        e.best_assignment()
+        e.free()
+    e = G.Engine(cnf, 600, 4, 0.5, 0, sub_batch=64)
+    e.run()
+    e.best_assignment()
+    e.free()
+    cnf.free()
+    inst = I.industrial(12_000, 48_000, 13)
+    cnf0 = G.Cnf.from_instance(inst)
+    cnf = cnf0.normalize(3)
+    e = G.Engine(cnf, 64, 3, 0.5, 3)
+    e.run()
+    s = e.select_member(0)
+    e.candidate_pool(s["global_b"], 3, 0.4, 9, arrays=False)
+    e.free()
+    cnf.free()
+    cnf0.free()
+
+
 PARTS = dict(small=part_small, tma=part_tma, lanes=part_lanes, loop=part_loop, v4=part_v4, soft=part_soft,
-             select=part_select, tseitin=part_tseitin, window=part_window)
+             select=part_select, tseitin=part_tseitin, window=part_window, smallw=part_smallw)
 
 if __name__ == "__main__":
     import torch
