@@ -187,7 +187,11 @@ int galois_engine_set_cubes(galois_engine *eng, int32_t d, const int32_t *vars);
  * the single-GPU result; a rank that did not hold the SAT member may run one update past t*
  * (its iterate then is one step ahead; no further check runs). All ranks must make the same
  * sequence of step / enqueue / run / info / unsat_counts / best_assignment calls: each may
- * run the pending check and its collective exchange. */
+ * run the pending check and its collective exchange.
+ * nccl_unique_id = NULL: no communicator — the engine runs rank `rank`'s slice of the
+ * world-rank split alone (same slice, global member indices and RNG counters as with NCCL)
+ * and its best record, bits and stop decision are the slice's own; the caller combines the
+ * ranks' records (lexicographic minimum of (u, t, b), the key the exchange reduces). */
 int galois_engine_set_comm(galois_engine *eng, int32_t rank, int32_t world, const void *nccl_unique_id);
 
 /* Use the caller's CUDA stream (a cudaStream_t, e.g. torch.cuda.current_stream()). */

@@ -803,11 +803,11 @@ extern "C" int galois_engine_set_comm(galois_engine *e, int32_t rank, int32_t wo
 {
     SETTER_ENTRY(e);
     if (world < 1 || rank < 0 || rank >= world) return fail(GALOIS_E_ARG, "need 0 <= rank < world");
-    if (world > 1 && !id) return fail(GALOIS_E_ARG, "nccl_unique_id is NULL");
     e->rank = rank;
     e->world = world;
     if (id) memcpy(e->nccl_id, id, 128);
-    e->use_comm = world > 1 || id != nullptr;   // world = 1 with an id: the NCCL path on one GPU
+    // id: the NCCL path (world = 1 with an id: on one GPU); no id: rank's slice alone
+    e->use_comm = id != nullptr;
     return GALOIS_OK;
 }
 

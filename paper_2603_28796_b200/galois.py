@@ -287,7 +287,7 @@ class Engine:
         if graphs:
             _check(L.galois_engine_set_graphs(self.handle, int(graphs)))
         if world > 1 or nccl_id is not None:
-            buf = ctypes.create_string_buffer(bytes(nccl_id), 128)
+            buf = ctypes.create_string_buffer(bytes(nccl_id), 128) if nccl_id is not None else None
             _check(L.galois_engine_set_comm(self.handle, int(rank), int(world), buf))
 
     # -- driving

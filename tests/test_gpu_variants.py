@@ -142,6 +142,47 @@ def test_windows_vs_oracle(G, K, sub):
     print(res)
 
 
+@pytest.mark.parametrize("world,B", [(2, 1000), (3, 100)])
+def test_rank_slices_equal_one_gpu_and_oracle(G, world, B):
+    """Row e's sharding without the transport: `world` engines each running one rank's slice
+    (set_comm with no communicator — same slices, global member indices and RNG counters as
+    the NCCL path) merged by the exchange's key, lexicographic min (u, t, b), equal the
+    single engine's record and bits, and that engine's run equals the oracle's. B = 100 at
+    world 3 leaves the last rank with no members (b_per = 64)."""
+    inst = I.random_ksat(120, 510, 3, 8)
+    cnf = G.Cnf.from_instance(inst)
+    T = 24
+    st = _init_state(G, cnf, inst, B, T, 1)
+    one = G.Engine(cnf, B, T, 0.5, 1)
+    z_one = one.get_iterate()[0]
+    parity.compare_run_variant(G, inst, one, parity.oracle_cfg(1), st, T, check_t0=True, compare_state=False,
+                               max_near=200, counts_after_sat=False)
+    best1 = one.best_assignment()
+    counts1, _ = one.unsat_counts()
+    b_per = -(-(-(-B // world)) // 32) * 32
+    recs = []
+    for r in range(world):
+        e = G.Engine(cnf, B, T, 0.5, 1, rank=r, world=world)
+        lo, hi = min(B, r * b_per), min(B, (r + 1) * b_per)
+        z = e.get_iterate()[0]
+        np.testing.assert_array_equal(z[:hi - lo], z_one[lo:hi])       # global RNG counters
+        e.run()
+        if hi > lo:
+            b = e.best_assignment()
+            assert lo <= b["global_b"] < hi
+            recs.append(((b["unsat"], b["step"], b["global_b"]), b["values"]))
+            if best1["unsat"] > 0:                                       # no SAT stop anywhere
+                c, first = e.unsat_counts()
+                assert first == lo
+                np.testing.assert_array_equal(c[:hi - lo], counts1[lo:hi])
+        e.free()
+    key, values = min(recs, key=lambda kv: kv[0])
+    assert key == (best1["unsat"], best1["step"], best1["global_b"])
+    np.testing.assert_array_equal(values, best1["values"])
+    one.free()
+    cnf.free()
+
+
 def test_nccl_single_rank_vs_oracle(G):
     """The NCCL exchange path (1-rank communicator: MIN all-reduce and the global record on
     the exchange stream, winner broadcast) against the oracle from one injected iterate."""
