@@ -91,7 +91,7 @@ def paper_largest(G, torch, dev, args):
         else:
             cnf = cnf0
         info = cnf.info()
-        sub = cnf.sub_batch_for(G.galois_device_free_bytes(dev.index) - margin)
+        sub = cnf.sub_batch_for(G.galois_device_free_bytes(dev.index) - margin, steps)
         eng = G.Engine(cnf, B, steps, 0.5, 0, sub_batch=sub)
         eng.set_profiling(bool(os.environ.get("GALOIS_PL_PROFILE")))
         clocks = ClockSampler(0)

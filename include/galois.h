@@ -241,6 +241,20 @@ int galois_engine_set_graphs(galois_engine *eng, int32_t mode);
  * buffers, counters), for sizing sub_batch to a memory budget. */
 int galois_engine_bytes_per_member(const galois_cnf *cnf, int32_t mode, int64_t *bytes);
 
+/* Exact device bytes of an engine (or f4 window) of `members` resident members for
+ * `steps` steps in the given mode, with_cubes != 0 if it holds cube pins: the allocation
+ * prepare makes (members padded to 32, or to 1024-member chunks above 1024; X/R rows are
+ * at least 4 words, so windows below 128 members cost more per member than
+ * bytes_per_member says). */
+int galois_engine_window_bytes(const galois_cnf *cnf, int32_t mode, int32_t members, int32_t steps,
+                               int32_t with_cubes, int64_t *bytes);
+
+/* The largest multiple of 32 members whose window_bytes fit budget_bytes (f4's
+ * sub_batch for a memory budget, e.g. galois_device_free_bytes minus a margin).
+ * E_OOM if not even 32 members fit. */
+int galois_engine_max_sub_batch(const galois_cnf *cnf, int32_t mode, int32_t steps, int32_t with_cubes,
+                                int64_t budget_bytes, int32_t *sub_batch);
+
 /* Device memory available to a new engine on `device`: the driver's free bytes plus what
  * the library's stream-ordered pool holds unused (freed engines and CNFs stay reserved in
  * it for reuse). Divide by bytes_per_member for the largest resident sub_batch (f4). */

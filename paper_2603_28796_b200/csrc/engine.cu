@@ -833,6 +833,60 @@ extern "C" int galois_engine_bytes_per_member(const galois_cnf *c, int32_t mode,
     return GALOIS_OK;
 }
 
+static void engine_layout(Slab &slab, galois_engine *e);
+
+static int32_t padded_members(int64_t resident)   // prepare's b_pad for `resident` members
+{
+    return resident <= 1024 ? (int32_t)std::max<int64_t>(32, (resident + 31) / 32 * 32)
+                            : (int32_t)((resident + 1023) / 1024 * 1024);
+}
+
+static int64_t window_bytes(const galois_cnf *c, int32_t mode, int64_t members, int32_t steps, bool cubes)
+{
+    galois_engine tmp;
+    tmp.cnf = const_cast<galois_cnf *>(c);
+    tmp.mode = mode;
+    tmp.T = steps;
+    tmp.b_pad = padded_members(members);
+    tmp.W = tmp.b_pad / 32;
+    if (cubes) tmp.pins.assign(1, 1);
+    Slab slab;
+    engine_layout(slab, &tmp);
+    tmp.cnf = nullptr;
+    return (int64_t)slab.total();
+}
+
+extern "C" int galois_engine_window_bytes(const galois_cnf *c, int32_t mode, int32_t members, int32_t steps,
+                                          int32_t with_cubes, int64_t *bytes)
+{
+    if (!c || !bytes) return fail(GALOIS_E_ARG, "cnf and bytes are required");
+    if (mode != GALOIS_MODE_ST && mode != GALOIS_MODE_SOFT) return fail(GALOIS_E_ARG, "mode must be 0 or 1");
+    if (members < 1 || steps < 0) return fail(GALOIS_E_ARG, "need members >= 1 and steps >= 0");
+    *bytes = window_bytes(c, mode, members, steps, with_cubes != 0);
+    return GALOIS_OK;
+}
+
+extern "C" int galois_engine_max_sub_batch(const galois_cnf *c, int32_t mode, int32_t steps, int32_t with_cubes,
+                                           int64_t budget_bytes, int32_t *sub_batch)
+{
+    if (!c || !sub_batch) return fail(GALOIS_E_ARG, "cnf and sub_batch are required");
+    if (mode != GALOIS_MODE_ST && mode != GALOIS_MODE_SOFT) return fail(GALOIS_E_ARG, "mode must be 0 or 1");
+    if (steps < 0) return fail(GALOIS_E_ARG, "steps must be >= 0");
+    const bool cubes = with_cubes != 0;
+    if (window_bytes(c, mode, 32, steps, cubes) > budget_bytes)
+        return fail(GALOIS_E_OOM, "a 32-member window does not fit the budget");
+    int64_t lo = 1, hi = (int64_t)(INT32_MAX - 1024) / 32;   // multiples of 32 members: lo fits
+    while (lo < hi) {
+        const int64_t mid = (lo + hi + 1) / 2;
+        if (window_bytes(c, mode, 32 * mid, steps, cubes) <= budget_bytes)
+            lo = mid;
+        else
+            hi = mid - 1;
+    }
+    *sub_batch = (int32_t)(32 * lo);
+    return GALOIS_OK;
+}
+
 extern "C" int galois_device_free_bytes(int32_t device, int64_t *bytes)
 {
     if (!bytes) return fail(GALOIS_E_ARG, "bytes is NULL");
@@ -1094,6 +1148,47 @@ static int prepare_lanes(galois_engine *e, int64_t ls, int64_t lspan)
     return GALOIS_OK;
 }
 
+// The engine's device buffers (ONE slab, see prepare): shared by prepare and the sizing
+// calls (galois_engine_window_bytes), so a window's size is exactly what prepare allocates.
+static void engine_layout(Slab &slab, galois_engine *e)
+{
+    const galois_cnf *c = e->cnf;
+    const int32_t n = c->n;
+    const size_t nb = (size_t)n * (size_t)e->b_pad;
+    slab.add(&e->z, nb);
+    slab.add(&e->m, nb);
+    slab.add(&e->v, nb);
+    slab.add(&e->X, (size_t)n * 2 * xr_pad(e->W));   // interleaved X/R rows (galois_internal.h)
+    slab.add(&e->unsat, (size_t)e->b_pad);
+    slab.add(&e->unsat_last, (size_t)e->b_pad);
+    slab.add(&e->ctrl, 1);
+    slab.add(&e->best_bits, (size_t)n);
+    slab.add(&e->adam_consts, (size_t)e->T + 2);
+    if (!e->pins.empty()) slab.add(&e->pin_rank, (size_t)n);
+    if (e->mode == GALOIS_MODE_ST && launch::small_run_smem(n, (int32_t)c->L) <= kSmallRunSmem) {
+        slab.add(&e->small_gs, 1);
+        slab.add(&e->small_recs, 2 * (size_t)e->W);
+        slab.add(&e->small_snap, (size_t)e->W * (size_t)n);
+    }
+    if (e->mode == GALOIS_MODE_ST) {
+        slab.add(&e->E, (size_t)c->L * e->W + 4);   // + 16 B: the small-window update copies whole 16-B units
+        slab.add(&e->lam, 2 * (size_t)e->b_pad);
+        if (c->num_hub_chunks > 0) slab.add(&e->partial, (size_t)c->num_hub_chunks * (e->b_pad / 4));
+        if (e->debug) {
+            slab.add(&e->dbg_G, nb);
+            slab.add(&e->dbg_g1, nb);
+        }
+    } else {
+        slab.add(&e->P, nb);
+        slab.add(&e->Es, (size_t)c->L * e->b_pad);
+        slab.add(&e->lam_f, (size_t)e->b_pad * (1 + launch::soft_chunks()));
+        if (e->debug) {
+            slab.add(&e->dbg_Gf, nb);
+            slab.add(&e->dbg_g1, nb);
+        }
+    }
+}
+
 static int prepare(galois_engine *e)
 {
     if (e->prepared) return GALOIS_OK;
@@ -1130,7 +1225,7 @@ static int prepare(galois_engine *e)
     const int32_t resident = e->windows > 1 ? e->sub : e->b_loc;
     // pad to 32 members (one bit word) up to 1024, then to whole 1024-member chunks, so that
     // W <= 32 or W % 32 == 0 (chunk-major E, TMA-staged update)
-    e->b_pad = resident <= 1024 ? std::max<int32_t>(32, (resident + 31) / 32 * 32) : (resident + 1023) / 1024 * 1024;
+    e->b_pad = padded_members(resident);
     e->W = e->b_pad / 32;
     if ((uint64_t)n * (uint64_t)e->b_pad / 4 >= (1ull << 40))
         return poison(e, GALOIS_E_ARG, "n * local batch too large");
@@ -1142,38 +1237,7 @@ static int prepare(galois_engine *e)
     // all device buffers of the engine live in ONE stream-ordered allocation from the
     // device's memory pool (cheap to create and free repeatedly, e.g. time-to-SAT runs)
     Slab slab;
-    slab.add(&e->z, nb);
-    slab.add(&e->m, nb);
-    slab.add(&e->v, nb);
-    slab.add(&e->X, (size_t)n * 2 * xr_pad(e->W));   // interleaved X/R rows (galois_internal.h)
-    slab.add(&e->unsat, (size_t)e->b_pad);
-    slab.add(&e->unsat_last, (size_t)e->b_pad);
-    slab.add(&e->ctrl, 1);
-    slab.add(&e->best_bits, (size_t)n);
-    slab.add(&e->adam_consts, (size_t)e->T + 2);
-    if (!e->pins.empty()) slab.add(&e->pin_rank, (size_t)n);
-    if (e->mode == GALOIS_MODE_ST && launch::small_run_smem(n, (int32_t)c->L) <= kSmallRunSmem) {
-        slab.add(&e->small_gs, 1);
-        slab.add(&e->small_recs, 2 * (size_t)e->W);
-        slab.add(&e->small_snap, (size_t)e->W * (size_t)n);
-    }
-    if (e->mode == GALOIS_MODE_ST) {
-        slab.add(&e->E, (size_t)c->L * e->W + 4);   // + 16 B: the small-window update copies whole 16-B units
-        slab.add(&e->lam, 2 * (size_t)e->b_pad);
-        if (c->num_hub_chunks > 0) slab.add(&e->partial, (size_t)c->num_hub_chunks * (e->b_pad / 4));
-        if (e->debug) {
-            slab.add(&e->dbg_G, nb);
-            slab.add(&e->dbg_g1, nb);
-        }
-    } else {
-        slab.add(&e->P, nb);
-        slab.add(&e->Es, (size_t)c->L * e->b_pad);
-        slab.add(&e->lam_f, (size_t)e->b_pad * (1 + launch::soft_chunks()));
-        if (e->debug) {
-            slab.add(&e->dbg_Gf, nb);
-            slab.add(&e->dbg_g1, nb);
-        }
-    }
+    engine_layout(slab, e);
     ENG_CUDA(e, use_pool_for_device(e->device));
     ENG_CUDA(e, cudaMallocAsync(&e->slab, slab.total(), e->stream));
     slab.assign(e->slab);

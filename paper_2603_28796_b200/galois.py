@@ -39,7 +39,7 @@ EXPORTED = (
     "galois_engine_kernel_times", "galois_select_member", "galois_candidate_pool", "galois_cube_variables",
     "galois_cnf_normalize", "galois_cnf_get_csr", "galois_engine_set_subbatch", "galois_engine_set_lanes", "galois_engine_bytes_per_member",
     "galois_engine_set_graphs", "galois_engine_get_member", "galois_cnf_original_vars", "galois_candidate_pool_size",
-    "galois_device_free_bytes",
+    "galois_device_free_bytes", "galois_engine_window_bytes", "galois_engine_max_sub_batch",
 )
 
 
@@ -99,6 +99,8 @@ def lib() -> ctypes.CDLL:
             "galois_engine_set_lanes": [P, I32],
             "galois_engine_bytes_per_member": [P, I32, P],
             "galois_device_free_bytes": [I32, P],
+            "galois_engine_window_bytes": [P, I32, I32, I32, I32, P],
+            "galois_engine_max_sub_batch": [P, I32, I32, I32, I64, P],
             "galois_engine_set_graphs": [P, I32],
             "galois_engine_get_member": [P, I64, P, P, P, P, P, P, P, P, P, P],
             "galois_cnf_original_vars": [P, P],
@@ -219,9 +221,19 @@ class Cnf:
         _check(lib().galois_engine_bytes_per_member(self.handle, int(mode), ctypes.byref(out)))
         return out.value
 
-    def sub_batch_for(self, budget_bytes: int, mode: int = 0) -> int:
-        """Largest multiple of 32 members whose engine state fits budget_bytes (f4)."""
-        return max(32, int(budget_bytes // self.bytes_per_member(mode)) // 32 * 32)
+    def window_bytes(self, members: int, steps: int, mode: int = 0, cubes: bool = False) -> int:
+        out = ctypes.c_int64()
+        _check(lib().galois_engine_window_bytes(self.handle, int(mode), int(members), int(steps), int(cubes),
+                                                ctypes.byref(out)))
+        return out.value
+
+    def sub_batch_for(self, budget_bytes: int, steps: int, mode: int = 0, cubes: bool = False) -> int:
+        """Largest multiple of 32 members whose engine fits budget_bytes (f4; the library's
+        galois_engine_max_sub_batch)."""
+        out = ctypes.c_int32()
+        _check(lib().galois_engine_max_sub_batch(self.handle, int(mode), int(steps), int(cubes), int(budget_bytes),
+                                                 ctypes.byref(out)))
+        return out.value
 
     def csr(self):
         info = self.info()

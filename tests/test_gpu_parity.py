@@ -493,7 +493,15 @@ def test_subbatch_gating_and_sizing(G):
     eng.free()
     per = cnf.bytes_per_member()
     assert per >= 12 * inst.n + inst.lits.size // 8
-    assert cnf.sub_batch_for(per * 1000) == 992
+    # exact window sizing (galois_engine_window_bytes mirrors prepare's allocation)
+    wb = cnf.window_bytes(992, 10)
+    assert per * 992 <= wb < cnf.window_bytes(1024, 10)
+    assert cnf.sub_batch_for(wb, 10) == 992
+    assert cnf.sub_batch_for(wb - 1, 10) == 960
+    assert cnf.window_bytes(32, 1000) - cnf.window_bytes(32, 0) >= 1000 * 8 - 256   # adam constants per step
+    assert cnf.window_bytes(32, 10) >= 32 * 12 * inst.n + inst.n * 32        # 4-word X/R rows at W = 1
+    with pytest.raises(G.GaloisError):
+        cnf.sub_batch_for(1000, 10)                                          # not even 32 members
     # the resident footprint scales with sub_batch, not B
     torch.cuda.synchronize()
     free0 = torch.cuda.mem_get_info()[0]
