@@ -154,28 +154,43 @@ __global__ void __launch_bounds__(256) k_clauses_v4(DevCnf c, int32_t W, int32_t
     for (int64_t g = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; g < ngroups; g += stride) {
         const int64_t ci = g * CPW + sub;
         if (!lane_ok || ci >= c.m) continue;
-        const int32_t cl = c.clause_perm[ci];     // width-sorted order
-        const int32_t lo = c.clause_off[cl], width = c.clause_off[cl + 1] - lo;
+        // sweep order (width-sorted, the CSR regrouped: no clause_perm -> clause_off hop);
+        // forward + check: a literal's X and R vectors in one 256-bit load
+        const int32_t lo = c.sweep_off[ci], width = c.sweep_off[ci + 1] - lo;
         uint4 any = make_uint4(0, 0, 0, 0), two = make_uint4(0, 0, 0, 0), anyR = make_uint4(0, 0, 0, 0);
         uint4 S[kCached];
         int2 si[kCached];
 #pragma unroll
         for (int i = 0; i < kCached; ++i)
-            if (i < width) si[i] = c.slot_info[lo + i];
+            if (i < width) si[i] = c.sweep_slot[lo + i];
 #pragma unroll
         for (int i = 0; i < kCached; ++i) {
             if (i < width) {
-                if (kForward) {
-                    S[i] = lit4(BX, RS, si[i].x);
+                if (kForward && kCheck) {
+                    uint4 r;
+                    lit_xr(BX, RS, si[i].x, S[i], r);
                     acc2(any, two, S[i]);
+                    or4(anyR, r);
+                } else {
+                    if (kForward) {
+                        S[i] = lit4(BX, RS, si[i].x);
+                        acc2(any, two, S[i]);
+                    }
+                    if (kCheck) or4(anyR, lit4(BR, RS, si[i].x));
                 }
-                if (kCheck) or4(anyR, lit4(BR, RS, si[i].x));
             }
         }
         for (int i = kCached; i < width; ++i) {
-            const int2 sj = c.slot_info[lo + i];
-            if (kForward) acc2(any, two, lit4(BX, RS, sj.x));
-            if (kCheck) or4(anyR, lit4(BR, RS, sj.x));
+            const int2 sj = c.sweep_slot[lo + i];
+            if (kForward && kCheck) {
+                uint4 x, r;
+                lit_xr(BX, RS, sj.x, x, r);
+                acc2(any, two, x);
+                or4(anyR, r);
+            } else {
+                if (kForward) acc2(any, two, lit4(BX, RS, sj.x));
+                if (kCheck) or4(anyR, lit4(BR, RS, sj.x));
+            }
         }
         if (kForward) {
 #pragma unroll
@@ -188,7 +203,7 @@ __global__ void __launch_bounds__(256) k_clauses_v4(DevCnf c, int32_t W, int32_t
                     *reinterpret_cast<uint4 *>(Ecol + (size_t)si[i].y * CW) = e;
                 }
             for (int i = kCached; i < width; ++i) {
-                const int2 sj = c.slot_info[lo + i];
+                const int2 sj = c.sweep_slot[lo + i];
                 const uint4 s = lit4(BX, RS, sj.x);
                 const uint32_t nm = 0u - (uint32_t)(sj.x & 1);
                 const uint4 e = make_uint4((~any.x | (s.x & ~two.x)) ^ nm, (~any.y | (s.y & ~two.y)) ^ nm,
