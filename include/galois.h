@@ -334,8 +334,8 @@ int galois_engine_get_member(galois_engine *eng, int64_t global_b, float *z, flo
 int galois_engine_get_grad(galois_engine *eng, int32_t *G, float *g1);
 
 /* Of the last forward: Lambda_b = sum_c U_c (= L_b + m; the unsat count of the sample
- * in ST mode), host b_loc floats. */
-int galois_engine_get_loss(galois_engine *eng, float *lambda);
+ * in ST mode, exact: double holds every count up to 2^53), host b_loc doubles. */
+int galois_engine_get_loss(galois_engine *eng, double *lambda);
 
 /* The sample bits X_{t+1} the next forward will use and the rounding R_t of the last
  * update, host [b_loc][n] bytes 0/1 each (NULL to skip). */

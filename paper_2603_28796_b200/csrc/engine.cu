@@ -2139,7 +2139,7 @@ extern "C" int galois_engine_get_grad(galois_engine *e, int32_t *G, float *g1)
     return GALOIS_OK;
 }
 
-extern "C" int galois_engine_get_loss(galois_engine *e, float *lambda)
+extern "C" int galois_engine_get_loss(galois_engine *e, double *lambda)
 {
     ENGINE_ENTRY(e);
     if (!lambda) return fail(GALOIS_E_ARG, "lambda is NULL");
@@ -2155,10 +2155,12 @@ extern "C" int galois_engine_get_loss(galois_engine *e, float *lambda)
         ENG_CUDA(e, cudaMemcpyAsync(tmp.data(), e->lam + (size_t)(h.t & 1) * e->b_pad, tmp.size() * 4,
                                     cudaMemcpyDeviceToHost, e->stream));
         ENG_CUDA(e, cudaStreamSynchronize(e->stream));
-        for (int32_t b = 0; b < e->b_loc; ++b) lambda[b] = (float)tmp[b];
+        for (int32_t b = 0; b < e->b_loc; ++b) lambda[b] = (double)tmp[b];   // exact: counts reach 2^24 on P:559's sizes
     } else {
-        ENG_CUDA(e, cudaMemcpyAsync(lambda, e->lam_f, (size_t)e->b_loc * 4, cudaMemcpyDeviceToHost, e->stream));
+        std::vector<float> tmp((size_t)e->b_loc);
+        ENG_CUDA(e, cudaMemcpyAsync(tmp.data(), e->lam_f, (size_t)e->b_loc * 4, cudaMemcpyDeviceToHost, e->stream));
         ENG_CUDA(e, cudaStreamSynchronize(e->stream));
+        for (int32_t b = 0; b < e->b_loc; ++b) lambda[b] = (double)tmp[b];
     }
     return GALOIS_OK;
 }

@@ -373,7 +373,7 @@ class Engine:
 
     def get_loss(self):
         nb = self.local_batch
-        lam = np.zeros(max(nb, 1), np.float32)
+        lam = np.zeros(max(nb, 1), np.float64)        # exact counts (ST) beyond 2^24
         _check(lib().galois_engine_get_loss(self.handle, _p(lam)))
         return lam[:nb]
 

@@ -439,3 +439,77 @@ def compare_run_variant(G, inst, eng, cfg, oracle_st, T, K=1, check_t0=False, zo
             if err.size:
                 assert (err <= z_rel * np.maximum(1, np.abs(zo[ok]))).all(), f"z drift {err.max()}"
     return dict(near=int(near.sum()), best=gbest, oracle_best=ref["best"], rc=rc, stop=ref["stop"])
+
+
+def stepwise_sampled_large(G, inst, eng, members, steps, seed=0, *, tau=1.0, lr=0.5, optimizer=0):
+    """stepwise_sampled for instances with ~1e8 variables, where every member-step has some
+    variables inside the fp32 tie zone (~5e-7 of them): ties are handled per VARIABLE, not
+    per member. Per step and member, from the member's fp32 iterate (exact map, R24):
+      * X the forward used = the oracle's sample outside the tie zone (per variable);
+      * Lambda = the oracle's forward on the engine's own bits X (oracle.member_signal), exact;
+      * z, m, v within the one-step bounds and R bit-exact outside R's tie zone, on every
+        variable that shares no clause with a tied variable (a tie flips that variable's
+        literal, so only the signal of its clause mates moves);
+      * the engine's exact count of its rounding R = oracle.unsat_count of the same bits.
+    Returns a report dict (compared variables, ties, excluded variables per member-step)."""
+    f = O.Cnf(inst.n, inst.offsets, inst.lits)
+    cfg = oracle_cfg(seed, 0, tau, lr, optimizer)
+    var_of = (np.abs(inst.lits).astype(np.int64) - 1)
+    cid = np.repeat(np.arange(inst.m, dtype=np.int64), np.diff(inst.offsets))
+    rep = dict(steps=0, member_steps=0, ties_x=0, ties_r=0, excluded_vars=0, compared_vars=0, counts=0)
+    states = {b: eng.get_member(b) for b in members}
+    t0 = states[members[0]]["t"]
+    prev_u = {b: O.unsat_count(f, s["r"]) for b, s in states.items()}
+    for t in range(steps):
+        ora = {}
+        for b, s in states.items():
+            st = O.State.from_reduced(s["z"][None], s["m"][None], s["v"][None], s["t"], b0=b)
+            ora[b] = (O.step(f, cfg, st), st)
+        eng.enqueue(1)
+        lam = eng.get_loss()
+        new = {b: eng.get_member(b) for b in members}
+        for b in members:
+            s, n_ = states[b], new[b]
+            out, st = ora[b]
+            tt = t0 + t
+            assert n_["t"] == tt + 1 and n_["check_t"] == tt, (b, n_["t"], n_["check_t"], tt)
+            assert n_["unsat"] == prev_u[b], f"unsat(R_{tt}) member {b}: {n_['unsat']} vs {prev_u[b]}"
+            rep["counts"] += 1
+            z = s["z"].astype(np.float64)
+            xg = s["x_next"]
+            dx = xg != out["xhat"][0]
+            zone = (1e-6 + 1e-6 * np.abs(z)) / tau
+            bad = dx & ~(np.abs(out["a"][0]) <= zone)
+            assert not bad.any(), f"X_{tt + 1}[{b}] mismatch outside the tie zone at {np.argwhere(bad)[:3].ravel()}"
+            lam_o = O.member_signal(f, xg.astype(np.float64))[0]
+            assert lam[b] == lam_o, f"Lambda_{tt + 1} member {b}: {lam[b]} vs oracle on the same bits {lam_o}"
+            # variables sharing a clause with a tied one
+            tied = np.zeros(inst.n, bool)
+            tied[np.nonzero(dx)[0]] = True
+            hit = np.zeros(inst.m, bool)
+            hit[cid[tied[var_of]]] = True
+            affected = np.zeros(inst.n, bool)
+            affected[var_of[hit[cid]]] = True
+            ok = ~affected
+            go = out["grad1"][0]
+            dg = 1e-5 * np.abs(go) + 1e-30
+            zo, mo, vo = (a[0] for a in st.reduced())
+            tol_m, tol_v, tol_z = update_tolerances(s["m"], s["v"], go, dg, zo, mo, vo, tt + 1, lr, optimizer)
+            dr = (n_["r"] != out["r"][0]) & ok
+            badr = dr & ~(np.abs(zo) <= tol_z)
+            assert not badr.any(), f"R_{tt + 1}[{b}] mismatch outside the tie zone at {np.argwhere(badr)[:3].ravel()}"
+            ok &= ~dr
+            if tol_m is not None:
+                assert (np.abs(n_["m"] - mo) <= tol_m)[ok].all(), f"m member {b} step {tt + 1}"
+                assert (np.abs(n_["v"] - vo) <= tol_v)[ok].all(), f"v member {b} step {tt + 1}"
+            zbad = (np.abs(n_["z"] - zo) > tol_z) & ok
+            assert not zbad.any(), f"z member {b} step {tt + 1}: {np.argwhere(zbad)[:3].ravel()}"
+            prev_u[b] = O.unsat_count(f, n_["r"])
+            rep["ties_x"] += int(dx.sum())
+            rep["ties_r"] += int(dr.sum())
+            rep["excluded_vars"] += int(affected.sum())
+            rep["compared_vars"] += int(ok.sum())
+            rep["member_steps"] += 1
+        states = new
+        rep["steps"] = t + 1
+    return rep

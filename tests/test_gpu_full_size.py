@@ -157,6 +157,19 @@ def test_small_window_update_stepwise(G, batch, pinned):
     cnf.free()
 
 
+def test_stepwise_large_harness(G):
+    """The per-variable tie harness that tools/pl_parity.py runs at the paper's largest size
+    (stepwise_sampled_large), on a small instance in the same kernel configuration (64
+    members: k_update_smallw + the fused scalar sweep)."""
+    inst = I.industrial_large(30_000, 120_000, 3)
+    cnf = G.Cnf.from_instance(inst)
+    eng = G.Engine(cnf, 64, 10, 0.5, 0)
+    rep = parity.stepwise_sampled_large(G, inst, eng, (0, 63), 3)
+    assert rep["member_steps"] == 6 and rep["compared_vars"] > 0.9 * 6 * inst.n, rep
+    eng.free()
+    cnf.free()
+
+
 def test_c2_lanes_stepwise(G):
     """configs[1] (B = 4096) split into the bench's 4 lanes (4 streams): sampled members of
     every lane, 4 steps."""
