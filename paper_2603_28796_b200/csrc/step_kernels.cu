@@ -130,12 +130,6 @@ __global__ void __launch_bounds__(256) k_resample(StepParams p, const float4 *__
 }
 
 // ------------------------------------------------------------- a5 / a8: clause kernels
-// Lane layout: LW = min(W, 32) lanes per clause cover 32-word chunk blockIdx.y of the batch
-// words; CPW = 32 / LW clauses per warp row; clauses in sweep order (sweep_off / sweep_slot
-// = {code, CSC position}: width-sorted, no clause_perm indirection). kForward: E of the
-// sample X and its U counts (Lambda) into lam; kCheck: the U counts of the rounding R
-// (exact unsat counts) into unsat — both in ONE pass when both are set (a literal's X and
-// R words share a 32-byte sector of the interleaved rows).
 template <bool kForward, bool kCheck>
 __global__ void __launch_bounds__(256) k_clauses_st(DevCnf c, int32_t W, int32_t b_pad,
                                                     const uint32_t *__restrict__ X, const uint32_t *__restrict__ R,
@@ -162,36 +156,59 @@ __global__ void __launch_bounds__(256) k_clauses_st(DevCnf c, int32_t W, int32_t
     for (int64_t g = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; g < ngroups; g += stride) {
         const int64_t ci = g * CPW + sub;
         if (!lane_ok || ci >= c.m) continue;
+        uint32_t Ux = 0, Ur = 0;         // U words of this lane's clause
         const int32_t lo = c.sweep_off[ci], width = c.sweep_off[ci + 1] - lo;
         uint32_t any = 0, two = 0;       // per member bit: >= 1 / >= 2 literals of X true
         uint32_t anyR = 0;               // >= 1 literal of R true
-        uint32_t S[8];
+        // literals in batches of 4, loads issued back to back (index clamped to the last
+        // literal, an absent literal masked to 0): under `if (i < width)` each gather waited
+        // for the previous one; the first batch's X words are kept for E
+        uint32_t S[4];
+        int2 s0[4];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            if (i < width) {
-                const int2 si = c.sweep_slot[lo + i];
-                const size_t at = xr_at(si.x >> 1, word, W);
-                const uint32_t nm = 0u - (uint32_t)(si.x & 1);
+        for (int j = 0; j < 4; ++j) s0[j] = c.sweep_slot[lo + min(j, width - 1)];
+        {
+            uint32_t xv[4], rv[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const size_t at = xr_at(s0[j].x >> 1, word, W);
+                if (kForward) xv[j] = X[at];
+                if (kCheck) rv[j] = R[at];
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const uint32_t keep = j < width ? 0xFFFFFFFFu : 0u, nm = 0u - (uint32_t)(s0[j].x & 1);
                 if (kForward) {
-                    const uint32_t s = X[at] ^ nm;
-                    S[i] = s;
-                    two |= any & s;
-                    any |= s;
+                    const uint32_t sv = (xv[j] ^ nm) & keep;
+                    S[j] = sv;
+                    two |= any & sv;
+                    any |= sv;
                 }
-                if (kCheck) anyR |= R[at] ^ nm;
+                if (kCheck) anyR |= (rv[j] ^ nm) & keep;
             }
         }
-        for (int i = 8; i < width; ++i) {
+        for (int i0 = 4; i0 < width; i0 += 4) {
             if (!kForward && anyR == 0xFFFFFFFFu) break;   // every member already satisfied
-            const int2 si = c.sweep_slot[lo + i];
-            const size_t at = xr_at(si.x >> 1, word, W);
-            const uint32_t nm = 0u - (uint32_t)(si.x & 1);
-            if (kForward) {
-                const uint32_t s = X[at] ^ nm;
-                two |= any & s;
-                any |= s;
+            int2 sj[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) sj[j] = c.sweep_slot[lo + min(i0 + j, width - 1)];
+            uint32_t xv[4], rv[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const size_t at = xr_at(sj[j].x >> 1, word, W);
+                if (kForward) xv[j] = X[at];
+                if (kCheck) rv[j] = R[at];
             }
-            if (kCheck) anyR |= R[at] ^ nm;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const uint32_t keep = i0 + j < width ? 0xFFFFFFFFu : 0u, nm = 0u - (uint32_t)(sj[j].x & 1);
+                if (kForward) {
+                    const uint32_t sv = (xv[j] ^ nm) & keep;
+                    two |= any & sv;
+                    any |= sv;
+                }
+                if (kCheck) anyR |= (rv[j] ^ nm) & keep;
+            }
         }
         if (kForward) {
             // E_i = prod_{j != i} (1 - s_j): all other literals false <=> none true, or
@@ -199,31 +216,29 @@ __global__ void __launch_bounds__(256) k_clauses_st(DevCnf c, int32_t W, int32_t
             // rows of negative occurrences are stored complemented (galois_internal.h).
             uint32_t *Ec = E + (size_t)blockIdx.y * c.L * LW + wl;
 #pragma unroll
-            for (int i = 0; i < 8; ++i)
-                if (i < width) {
-                    const int2 si = c.sweep_slot[lo + i];
-                    Ec[(size_t)si.y * LW] = (~any | (S[i] & ~two)) ^ (0u - (uint32_t)(si.x & 1));
-                }
-            for (int i = 8; i < width; ++i) {
-                const int2 si = c.sweep_slot[lo + i];
-                const uint32_t s = X[xr_at(si.x >> 1, word, W)] ^ (0u - (uint32_t)(si.x & 1));
-                Ec[(size_t)si.y * LW] = (~any | (s & ~two)) ^ (0u - (uint32_t)(si.x & 1));
+            for (int j = 0; j < 4; ++j)
+                if (j < width) Ec[(size_t)s0[j].y * LW] = (~any | (S[j] & ~two)) ^ (0u - (uint32_t)(s0[j].x & 1));
+            for (int i0 = 4; i0 < width; i0 += 4) {
+                int2 sj[4];
+                uint32_t xv[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) sj[j] = c.sweep_slot[lo + min(i0 + j, width - 1)];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) xv[j] = X[xr_at(sj[j].x >> 1, word, W)];
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (i0 + j < width) {
+                        const uint32_t nm = 0u - (uint32_t)(sj[j].x & 1);
+                        Ec[(size_t)sj[j].y * LW] = (~any | ((xv[j] ^ nm) & ~two)) ^ nm;
+                    }
             }
-            uint32_t U = ~any;              // U = prod_i (1 - s_i): clause unsatisfied
-            while (U) {
-                const int j = __ffs(U) - 1;
-                atomicAdd(&s_lam[wl * 32 + j], 1);
-                U &= U - 1;
-            }
+            Ux = ~any;                      // U = prod_i (1 - s_i): clause unsatisfied
         }
-        if (kCheck) {
-            uint32_t U = ~anyR;
-            while (U) {
-                const int j = __ffs(U) - 1;
-                atomicAdd(&s_uns[wl * 32 + j], 1);
-                U &= U - 1;
-            }
-        }
+        if (kCheck) Ur = ~anyR;
+        if (kForward)
+            for (uint32_t U = Ux; U; U &= U - 1) atomicAdd(&s_lam[wl * 32 + __ffs(U) - 1], 1);
+        if (kCheck)
+            for (uint32_t U = Ur; U; U &= U - 1) atomicAdd(&s_uns[wl * 32 + __ffs(U) - 1], 1);
     }
     __syncthreads();
     const int base = blockIdx.y * 1024;
