@@ -509,6 +509,33 @@ def test_planted_instances_are_satisfied_by_their_model():
         assert O.unsat_count(f, inst.planted) == 0
 
 
+def test_industrial_large_generator_laws():
+    """PL's generator (instances.industrial_large, the paper's largest size P:559): widths in
+    [2, 30] with P(w) ~ w^-2.5, distinct variables within a clause, literals in range, both
+    signs, occurrence counts falling with the pre-permutation rank (P(i) ~ i^-0.8), and the
+    same formula for the same seed."""
+    n, m = 200_000, 840_000
+    a = I.industrial_large(n, m, 7)
+    b = I.industrial_large(n, m, 7)
+    np.testing.assert_array_equal(a.offsets, b.offsets)
+    np.testing.assert_array_equal(a.lits, b.lits)
+    w = np.diff(a.offsets)
+    assert w.min() >= 2 and w.max() <= 30 and a.m == m
+    ws = np.arange(2, 31)
+    pw = ws ** -2.5 / (ws ** -2.5).sum()
+    freq = np.bincount(w, minlength=31)[2:] / m
+    assert np.abs(freq - pw).max() < 3e-3
+    v = np.abs(a.lits)
+    assert v.min() >= 1 and v.max() <= n and (a.lits < 0).mean() == pytest.approx(0.5, abs=2e-3)
+    cid = np.repeat(np.arange(m), w)
+    key = cid * (n + 1) + v
+    assert np.unique(key).size == key.size                          # no variable twice in a clause
+    deg = np.sort(I.degrees(a))[::-1]
+    # rank-frequency of a ~ i^-0.8 law: the top 1 % of variables carry far more than 1 %
+    top = deg[: n // 100].sum() / deg.sum()
+    assert 0.2 < top < 0.6, top
+
+
 # --------------------------------------------- f1 / f3: pool, partial assignments, cubes
 def test_extract_partial_spec_example():
     """SPEC extract_partial: top-|S| by descending confidence, Eq.11 literals."""

@@ -1,10 +1,10 @@
 #!/usr/bin/env bash
 # One GPU session's evidence: tests, smoke, bench lines, launch list and ncu captures.
 #   gpurun --timeout 1800 -- 'bash tools/gpu_round.sh <tag> [parts]'
-# parts (default all): tests bench launches full
+# parts (default all): tests bench launches full paper
 set -u
 TAG=${1:-r01}
-PARTS=${2:-"tests bench launches full"}
+PARTS=${2:-"tests bench launches full paper"}
 OUT=gpurun_out/$TAG
 mkdir -p "$OUT"
 python -m paper_2603_28796_b200.build > "$OUT/build.log" 2>&1 || { cat "$OUT/build.log"; exit 1; }
@@ -36,7 +36,7 @@ if has launches; then
 fi
 if has full; then
     for W in C2 C4; do
-        for K in k_update_pair k_update_tma k_sweep k_hub_partial_tma; do
+        for K in k_update_pair k_sweep k_hub_partial_tma; do
             timeout 900 $NCU --set full --clock-control none --import-source on -k regex:$K -s 20 -c 1 \
                 -o "$OUT/full_${W}_$K" python bench.py --workload $W --steps 24 --warmup 3 --lanes 1 --no-cpu-baseline \
                 --no-e2e > "$OUT/full_${W}_$K.log" 2>&1
@@ -52,4 +52,12 @@ if has sanitize; then
             echo "sanitize $tool $part rc=$? $(grep -E 'ERROR SUMMARY|RACECHECK SUMMARY' $OUT/san_${tool}_$part.log | tail -1)"
         done
     done 2>&1 | tee "$OUT/sanitize_summary.txt"
+fi
+if has paper; then
+    timeout 900 python bench.py --workload P4 > "$OUT/paper_P4.json" 2> "$OUT/paper_P4.err"
+    tail -c 400 "$OUT/paper_P4.json"; echo
+    timeout 1500 python bench.py --workload PL > "$OUT/paper_PL.json" 2> "$OUT/paper_PL.err"
+    tail -c 600 "$OUT/paper_PL.json"; echo
+    timeout 1800 python tools/pl_parity.py > "$OUT/pl_parity.json" 2> "$OUT/pl_parity.err"
+    echo "pl_parity rc=$?"; tail -c 600 "$OUT/pl_parity.json"; echo
 fi
