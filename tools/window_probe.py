@@ -4,6 +4,8 @@ from paper_2603_28796_b200 import galois as G, instances as I
 inst = I.CONFIGS["C4"][0]()
 dev = torch.device("cuda:0")
 cnf = G.Cnf.from_instance(inst)
+if os.environ.get("WINDOW_NORM"):
+    cnf = cnf.normalize(3)
 print("bytes/member", cnf.bytes_per_member(), flush=True)
 for sub in [int(x) for x in os.environ.get('WINDOW_SUBS', '1024,512,256,128,64,32').split(',')]:
     for rep in range(3):
