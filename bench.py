@@ -747,8 +747,9 @@ def default_lanes(batch_per_gpu):
 
 
 def effective_lanes(b_loc, lanes, world):
-    """Lanes the engine actually forms (galois.h, galois_engine_set_lanes)."""
-    if lanes <= 1:
+    """Lanes the engine actually forms (galois.h, galois_engine_set_lanes: none with an NCCL
+    communicator, i.e. under torchrun)."""
+    if lanes <= 1 or world > 1:
         return 1
     ls = (-(-b_loc // lanes) + 1023) // 1024 * 1024     # (ranks hold equal slices in the bench)
     return -(-b_loc // ls) if b_loc > ls else 1

@@ -55,6 +55,7 @@ def test_batch_sharding_and_lanes_rules():
     assert bench.effective_lanes(4096, 4, 1) == 4
     assert bench.effective_lanes(3000, 4, 1) == 3          # 1024 + 1024 + 952
     assert bench.effective_lanes(16384, 4, 1) == 4
-    assert bench.effective_lanes(2100, 2, 8) == 2          # 2048 + 52
+    assert bench.effective_lanes(2100, 2, 1) == 2          # 2048 + 52
+    assert bench.effective_lanes(4096, 4, 8) == 1          # no lanes with an NCCL communicator
     assert bench.effective_lanes(1024, 4, 1) == 1
     assert bench.effective_lanes(8192, 1, 1) == 1
