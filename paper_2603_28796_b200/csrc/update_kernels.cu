@@ -1411,6 +1411,7 @@ __global__ void __launch_bounds__(256 + 32, kSwCtasPerSm)
     __shared__ uint64_t full[kSwStages], empty[kSwStages];
     __shared__ SwHdr hdr[kSwStages];
     __shared__ int32_t hflags[kSwStages];   // bit 0: z, m, v in this stage; bit 1: the group's last stage
+    __shared__ int4 vinfo[kSwStages][32];   // first stage of a group: {k0, k1, k2, hub} per variable
     if (ctrl->stopped) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t QW = 8u * (uint32_t)W;    // quads per variable row
@@ -1434,12 +1435,14 @@ __global__ void __launch_bounds__(256 + 32, kSwCtasPerSm)
         for (uint32_t g = blockIdx.x; g < groups; g += gridDim.x) {
             const int32_t v0 = (int32_t)g * RG, nv = min(RG, c.n - v0);
             // lane j: variable v0 + j's CSC range and whether it is a hub
-            int32_t kb = 0, ke = 0;
+            int32_t kb = 0, kn = 0, ke = 0, hubi = -1;
             bool hub = false;
             if (lane < nv) {
                 kb = c.code_off[2 * (v0 + lane)];
+                kn = c.code_off[2 * (v0 + lane) + 1];
                 ke = c.code_off[2 * (v0 + lane) + 2];
-                hub = c.num_hubs > 0 && c.hub_of_var[v0 + lane] >= 0;
+                hubi = c.num_hubs > 0 ? c.hub_of_var[v0 + lane] : -1;
+                hub = hubi >= 0;
             }
             uint32_t hm = __ballot_sync(0xffffffffu, hub);
             const int32_t end = __shfl_sync(0xffffffffu, ke, nv - 1);
@@ -1452,11 +1455,16 @@ __global__ void __launch_bounds__(256 + 32, kSwCtasPerSm)
                     const int32_t r1 = min(hi, ra + cap);
                     const bool last = fin && r1 >= hi;
                     if (r1 > lo || last || first) {
+                        if (lane == 0 && wrapped) {
+                            mbar_wait_s(empty_s + 8u * st, ph ^ 1u);
+                            fence_proxy_async_smem();
+                        }
+                        __syncwarp();
+                        // the group's variable table travels with its first stage (the
+                        // consumers read it from shared memory instead of global)
+                        if (first && lane < nv) vinfo[st][lane] = make_int4(kb, kn, ke, hubi);
+                        __syncwarp();
                         if (lane == 0) {
-                            if (wrapped) {
-                                mbar_wait_s(empty_s + 8u * st, ph ^ 1u);
-                                fence_proxy_async_smem();
-                            }
                             hdr[st] = SwHdr{lo, max(lo, r1), ra};
                             hflags[st] = (first ? 1 : 0) | (last ? 2 : 0);
                             const int32_t rb = r1 > lo ? (r1 + rpa - 1) / rpa * rpa : ra;
@@ -1512,12 +1520,6 @@ __global__ void __launch_bounds__(256 + 32, kSwCtasPerSm)
         const int32_t v = (int32_t)g * RG + (int32_t)r_t;
         const bool valid = v < c.n;
         int32_t k0 = 0, k1 = 0, k2 = 0, hub = -1;
-        if (valid) {
-            k0 = c.code_off[2 * v];
-            k1 = c.code_off[2 * v + 1];
-            k2 = c.code_off[2 * v + 2];
-            hub = c.num_hubs > 0 ? c.hub_of_var[v] : -1;
-        }
         float4 z = make_float4(0.f, 0.f, 0.f, 0.f), m = z, vv = z;
         int32_t G[4] = {0, 0, 0, 0};
         int32_t flags = 0;
@@ -1527,6 +1529,11 @@ __global__ void __launch_bounds__(256 + 32, kSwCtasPerSm)
             flags = hflags[st];
             const uint8_t *sb = smem + st * kSwStageBytes;
             if ((flags & 1) && valid) {
+                const int4 vi = vinfo[st][r_t];
+                k0 = vi.x;
+                k1 = vi.y;
+                k2 = vi.z;
+                hub = vi.w;
                 z = reinterpret_cast<const float4 *>(sb + kSwE)[tid];
                 m = reinterpret_cast<const float4 *>(sb + kSwE + 4096)[tid];
                 vv = reinterpret_cast<const float4 *>(sb + kSwE + 8192)[tid];
