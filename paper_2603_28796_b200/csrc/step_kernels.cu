@@ -33,7 +33,6 @@ __global__ void __launch_bounds__(256) k_init(StepParams p, float4 *__restrict__
 {
     const int lane = threadIdx.x & 31;
     const uint32_t QW = (uint32_t)p.b_pad / 4u;               // a multiple of 8: whole words per 8 lanes
-    const uint2 key = make_uint2((uint32_t)p.seed, (uint32_t)(p.seed >> 32));
     // A CTA pass covers rpc rows: one row's quads across the CTA (QW >= 256, a multiple of
     // 256), or 256 / QW whole rows of QW quads (small sub-batch windows: b_pad = 32 would
     // otherwise leave 248 of 256 threads idle). Every lane runs the same passes (ballots).
@@ -48,7 +47,7 @@ __global__ void __launch_bounds__(256) k_init(StepParams p, float4 *__restrict__
         float zz[4];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {                        // init counter (v, b/2, 0, 0)
-            const uint4 w = philox4x32_10(make_uint4((uint32_t)v, (uint32_t)((bq >> 1) + h), 0u, 0u), key);
+            const uint4 w = philox4x32_10(make_uint4((uint32_t)v, (uint32_t)((bq >> 1) + h), 0u, 0u), p.keys);
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
                 // Box-Muller theta_0 = rho cos(2 pi u1), theta_1 = rho sin(2 pi u1), rho =
@@ -60,7 +59,7 @@ __global__ void __launch_bounds__(256) k_init(StepParams p, float4 *__restrict__
                 zz[2 * h + j] = sqrtf(-4.0f * logf(u0)) * sinpif(fmaf(2.0f, u1, -0.25f));
             }
         }
-        const uint4 wn = philox4x32_10(make_uint4((uint32_t)v, (uint32_t)(bq >> 2), 1u, 1u), key);
+        const uint4 wn = philox4x32_10(make_uint4((uint32_t)v, (uint32_t)(bq >> 2), 1u, 1u), p.keys);
         const uint32_t wv[4] = {wn.x, wn.y, wn.z, wn.w};
         uint32_t xn = 0, rn = 0;
 #pragma unroll
@@ -101,14 +100,13 @@ __global__ void __launch_bounds__(256) k_resample(StepParams p, const float4 *__
 {
     const int lane = threadIdx.x & 31;
     const uint32_t QW = (uint32_t)p.b_pad / 4u;               // a multiple of 8: whole words per 8 lanes
-    const uint2 key = make_uint2((uint32_t)p.seed, (uint32_t)(p.seed >> 32));
     // rows blockIdx.x, blockIdx.x + gridDim.x, ...; quads of a row across the CTA (no division)
     for (int32_t v = blockIdx.x; v < p.n; v += gridDim.x)
     for (uint32_t q = threadIdx.x; q < QW; q += blockDim.x) {
         const int64_t bq = p.b0 + 4 * (int64_t)q;
         const float4 z = z4[(size_t)v * QW + q];
         const float zz[4] = {z.x, z.y, z.z, z.w};
-        const uint4 wn = philox4x32_10(make_uint4((uint32_t)v, (uint32_t)(bq >> 2), (uint32_t)t_next, 1u), key);
+        const uint4 wn = philox4x32_10(make_uint4((uint32_t)v, (uint32_t)(bq >> 2), (uint32_t)t_next, 1u), p.keys);
         const uint32_t wv[4] = {wn.x, wn.y, wn.z, wn.w};
         uint32_t xn = 0, rn = 0;
 #pragma unroll
