@@ -1241,7 +1241,7 @@ static int prepare(galois_engine *e)
     ENG_CUDA(e, use_pool_for_device(e->device));
     ENG_CUDA(e, cudaMallocAsync(&e->slab, slab.total(), e->stream));
     slab.assign(e->slab);
-    e->R = e->X + 4;
+    e->R = e->X + xr_roff(e->W);
     ENG_CUDA(e, cudaMemsetAsync(e->unsat, 0, sizeof(int32_t) * (size_t)e->b_pad, e->stream));
     ENG_CUDA(e, cudaMemsetAsync(e->unsat_last, 0, sizeof(int32_t) * (size_t)e->b_pad, e->stream));
     ENG_CUDA(e, cudaMemsetAsync(e->best_bits, 0, (size_t)n, e->stream));
@@ -2183,7 +2183,7 @@ extern "C" int galois_engine_get_bits(galois_engine *e, uint8_t *x_next, uint8_t
     uint8_t *outs[2] = {x_next, r};
     for (int a = 0; a < 2; ++a) {
         if (!outs[a]) continue;
-        const uint32_t *base = tmp.data() + 4 * a;   // R = X + 4 words
+        const uint32_t *base = tmp.data() + (size_t)xr_roff(e->W) * a;   // R = X + xr_roff(W) words
         for (int32_t b = 0; b < e->b_loc; ++b)
             for (int32_t v = 0; v < n; ++v)
                 outs[a][(size_t)b * n + v] =   // member i of a word at bit 8 (i mod 4) + i / 4

@@ -9,6 +9,8 @@
 //   bits  X, R interleaved in one array: row v = 2 WP words (WP = W rounded up to 4),
 //         16-byte groups alternating X words 4g..4g+3 and R words 4g..4g+3, R = X + 4 words
 //         (xr_at); a sweep lane's X and R vectors of a literal are one 32-byte sector.
+//         W < 4 (windows of 32-96 members): compact rows of 2W words, the W X words then
+//         the W R words, R = X + W words — four variables' rows per sector at W = 1.
 //         Word w holds members 32w..32w+31; member 32w + i at bit 8 (i mod 4) + i / 4
 //         (device_utils.cuh bitpos)
 //   E     uint32 [L][W] in CSC order (exclusive products of each occurrence); the row of a
@@ -26,10 +28,13 @@ namespace galois {
 constexpr int kHubDegree = 256;      // variables with more occurrences use the hub path
 constexpr int kSweepOffPad = 128;    // sweep_off entries past m (all = L): whole-tile copies
 
-// word w of row v of the interleaved X/R array (apply to X for X words, to R = X + 4 for R)
-__host__ __device__ __forceinline__ int32_t xr_pad(int32_t W) { return (W + 3) & ~3; }
+// word w of row v of the interleaved X/R array (apply to X for X words, to R = X + xr_roff(W)
+// for R)
+__host__ __device__ __forceinline__ int32_t xr_pad(int32_t W) { return W < 4 ? W : (W + 3) & ~3; }
+__host__ __device__ __forceinline__ int32_t xr_roff(int32_t W) { return W < 4 ? W : 4; }
 __host__ __device__ __forceinline__ size_t xr_at(int32_t v, int32_t w, int32_t W)
 {
+    if (W < 4) return (size_t)v * 2 * (size_t)W + (size_t)w;
     return (size_t)v * 2 * (size_t)xr_pad(W) + ((size_t)(w >> 2) << 3) + (size_t)(w & 3);
 }
 #ifndef GALOIS_HUB_CHUNK

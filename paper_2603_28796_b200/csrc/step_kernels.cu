@@ -293,7 +293,7 @@ __global__ void k_member_bits(const uint32_t *__restrict__ X, int32_t n, int32_t
     for (int32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
         const size_t at = xr_at(v, (int32_t)w, W);
         if (x_out) x_out[v] = (uint8_t)((X[at] >> bit) & 1u);
-        if (r_out) r_out[v] = (uint8_t)((X[at + 4] >> bit) & 1u);   // R = X + 4 words
+        if (r_out) r_out[v] = (uint8_t)((X[at + xr_roff(W)] >> bit) & 1u);   // R = X + xr_roff(W) words
     }
 }
 
