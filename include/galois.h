@@ -243,9 +243,8 @@ int galois_engine_bytes_per_member(const galois_cnf *cnf, int32_t mode, int64_t 
 
 /* Exact device bytes of an engine (or f4 window) of `members` resident members for
  * `steps` steps in the given mode, with_cubes != 0 if it holds cube pins: the allocation
- * prepare makes (members padded to 32, or to 1024-member chunks above 1024; X/R rows are
- * at least 4 words, so windows below 128 members cost more per member than
- * bytes_per_member says). */
+ * prepare makes (members padded to 32, or to 1024-member chunks above 1024, plus E, hub
+ * partials and counters: a window's bytes are not its members times bytes_per_member). */
 int galois_engine_window_bytes(const galois_cnf *cnf, int32_t mode, int32_t members, int32_t steps,
                                int32_t with_cubes, int64_t *bytes);
 
