@@ -499,7 +499,7 @@ def test_subbatch_gating_and_sizing(G):
     assert cnf.sub_batch_for(wb, 10) == 992
     assert cnf.sub_batch_for(wb - 1, 10) == 960
     assert cnf.window_bytes(32, 1000) - cnf.window_bytes(32, 0) >= 1000 * 8 - 256   # adam constants per step
-    assert cnf.window_bytes(32, 10) >= 32 * 12 * inst.n + inst.n * 32        # 4-word X/R rows at W = 1
+    assert cnf.window_bytes(32, 10) >= 32 * 12 * inst.n + 8 * inst.n + 4 * inst.L   # z/m/v, compact X/R, E at W = 1
     with pytest.raises(G.GaloisError):
         cnf.sub_batch_for(1000, 10)                                          # not even 32 members
     # the resident footprint scales with sub_batch, not B
