@@ -32,9 +32,9 @@ constexpr int kSweepOffPad = 128;    // sweep_off entries past m (all = L): whol
 // for R)
 __host__ __device__ __forceinline__ int32_t xr_pad(int32_t W) { return W < 4 ? W : (W + 3) & ~3; }
 __host__ __device__ __forceinline__ int32_t xr_roff(int32_t W) { return W < 4 ? W : 4; }
+// (one formula for both layouts: below W = 4 the word index w < 4 adds just w)
 __host__ __device__ __forceinline__ size_t xr_at(int32_t v, int32_t w, int32_t W)
 {
-    if (W < 4) return (size_t)v * 2 * (size_t)W + (size_t)w;
     return (size_t)v * 2 * (size_t)xr_pad(W) + ((size_t)(w >> 2) << 3) + (size_t)(w & 3);
 }
 #ifndef GALOIS_HUB_CHUNK
