@@ -523,6 +523,9 @@ constexpr int kConsumerWarps = 8;
 #endif
 constexpr int kSlicedMinDegree = GALOIS_SLICED_MIN_DEGREE;
 constexpr int kSlicedPlanes = 6;
+#ifndef GALOIS_SLICED_SMALL
+#define GALOIS_SLICED_SMALL 1   // variables of <= 120 rows: 4 planes and a 7-plane butterfly
+#endif
 #ifndef GALOIS_SLICED_MIN_AVG_DEGREE
 #define GALOIS_SLICED_MIN_AVG_DEGREE 48
 #endif
@@ -584,7 +587,7 @@ __global__ void __launch_bounds__(256 + 32, kTmaCtasPerSm) k_update_tma(DevCnf c
                     const int32_t r1 = hub ? k0 : min(k2, r0 + kStageRows);
                     hdr[st] = StageHdr{(int32_t)v, k1, r0, r1};
                     hflags[st] = (pc == 0 ? 1 : 0) | (pc == pieces - 1 ? 2 : 0) | (hub ? 4 : 0) | (pinned ? 8 : 0) |
-                                 (sliced ? 16 : 0);
+                                 (sliced ? 16 : 0) | (sliced && GALOIS_SLICED_SMALL && k2 - k0 <= 8 * 15 ? 32 : 0);
                     const uint32_t ebytes = (uint32_t)(r1 - r0) * 128u;
                     const uint32_t fb = full_s + 8u * st, sbs = stage_s + (uint32_t)(st * kStageBytes);
                     mbar_arrive_expect_tx_s(fb, (pc == 0 ? 3u * 4096u : 0u) + ebytes);
@@ -647,7 +650,9 @@ __global__ void __launch_bounds__(256 + 32, kTmaCtasPerSm) k_update_tma(DevCnf c
                 const int32_t nrows = h.r1 - h.r0, nneg = h.r1 - max(h.k1, h.r0);
                 if (kSliced) {
                     negs += max(0, nneg);
-                    if (flags & 16) {               // uniform over the CTA: a high-degree variable
+                    if (flags & 32) {               // <= 120 rows: <= 15 per thread, 4 planes
+                        sliced_add<4>(*reinterpret_cast<uint32_t(*)[4]>(&PS), srow, nrows, tid & 7);
+                    } else if (flags & 16) {        // uniform over the CTA: a high-degree variable
                         sliced_add(PS, srow, nrows, tid & 7);
                     } else {
 #pragma unroll 8
@@ -671,7 +676,9 @@ __global__ void __launch_bounds__(256 + 32, kTmaCtasPerSm) k_update_tma(DevCnf c
         if (kSliced && (flags & 4)) {
             hub_signal(c, partial, QW, c.hub_of_var[v], q, G);
         } else if (kSliced) {
-            if (flags & 16)
+            if (flags & 32)
+                sliced_finish<4>(*reinterpret_cast<const uint32_t(*)[4]>(&PS), sh, G);
+            else if (flags & 16)
                 sliced_finish(PS, sh, G);           // one butterfly per variable
             else
 #pragma unroll
